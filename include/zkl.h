@@ -1,0 +1,141 @@
+/*
+ * zkl — B200-native tlookup prover (zkLLM, arXiv 2404.16109, §4 Protocol 1) : the C ABI.
+ *
+ * The hot path of Protocol 1 without the commitments:
+ *   zkl_tlookup_prepare  tlookup-Prep: m_i = |{j : S_j = T_i}|
+ *                        (Eq. hab22-coefs)
+ *   zkl_tlookup_prove    tlookup-Prove: A = 1/(beta+S), B = 1/(beta+T)
+ *                        (Eq. hab22-invs), then the sumcheck
+ *                        of Eq. tlookup-sumcheck
+ *   zkl_sumcheck_prove   the same sumcheck on caller-supplied A, S, B, T, m
+ * plus the boundary encoders (import/export of field vectors) and the table handle.
+ *
+ * Field: BLS12-381 scalar field Fr, r = 0x73eda753299d7d483339d80809a1d80553bda402fffe5bfeffffffff00000001
+ * (PAPER.md:543, 627).
+ *
+ * Conventions ("readings"):
+ *   - a host field element (zkl_fr) is canonical: 8 little-endian 32-bit words, value < r;
+ *   - a device field vector (zkl_vec) is Montgomery form (x * 2^256 mod r) in limb-interleaved
+ *     SoA layout: limb l of element i at limbs[l*n + i]; limbs must be 16-byte aligned and n a
+ *     multiple of 4 (or n < 4);
+ *   - coordinate 0 of the hypercube is the MSB of the row-major index; table index j = x mod N;
+ *     the table's eq point is u[log2(D/N):];
+ *   - sumcheck round k (1-based) binds coordinate d-k (LSB first) with r[k-1]; round polynomial
+ *     g_k is returned by its values g_k(0), g_k(1), g_k(2), g_k(3);
+ *   - weights (1, alpha1, alpha2) of the three constraints (paper: alpha2 = alpha1^2);
+ *     the claimed sum is alpha1 + alpha2 (ZKL_VARIANT_PAPER) or alpha1 (ZKL_VARIANT_LOGUP);
+ *   - final evaluations: A(v), S(v), B(v'), T(v'), m(v') with v_c = r[d-1-c], v' = v[d-n:].
+ *
+ * Ownership: the caller owns every device buffer (inputs, outputs, the workspace and the table
+ * memory).  The library owns only the opaque zkl_ctx / zkl_table objects (paired create/destroy).
+ * Streams: all device work is enqueued on the ctx's CUDA stream (plus internal events); every call
+ * returns when its host-visible outputs are ready and its device outputs are complete.
+ * Errors: every int-returning call returns a zkl_status; err_index (when given) is set to the
+ * smallest offending index, or -1.  Outputs are unspecified on error.  No exception or abort
+ * crosses the ABI.  An asynchronous CUDA fault poisons the ctx (ZKL_E_STATE afterwards).
+ * Multi-rank (nranks > 1) calls are collective: every rank passes identical scalars/challenges and
+ * its own contiguous slice S_local = S[rank*D/P, (rank+1)*D/P) (top log2 P coordinates = rank).
+ */
+#ifndef ZKL_H
+#define ZKL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct { uint32_t w[8]; } zkl_fr;                  /* canonical, little-endian, < r */
+typedef struct { uint32_t* limbs; uint64_t n; } zkl_vec;   /* device, SoA Montgomery */
+typedef struct zkl_ctx zkl_ctx;
+typedef struct zkl_table zkl_table;
+
+typedef enum {
+    ZKL_OK = 0,
+    ZKL_E_ARG = 1,            /* null pointer / bad argument */
+    ZKL_E_SHAPE = 2,          /* D, N not powers of two, N > D, P does not divide D, ... */
+    ZKL_E_NONCANONICAL = 3,   /* an input element >= r (err_index = element) */
+    ZKL_E_DUP_TABLE = 4,      /* T has repeated entries (err_index = smallest later duplicate) */
+    ZKL_E_NOT_IN_TABLE = 5,   /* S_i not in T (err_index = smallest global i) */
+    ZKL_E_DIV_ZERO_T = 6,     /* beta + T_j = 0 (err_index = smallest j; checked before S) */
+    ZKL_E_DIV_ZERO_S = 7,     /* beta + S_i = 0 (err_index = smallest global i) */
+    ZKL_E_CUDA = 8,
+    ZKL_E_NCCL = 9,
+    ZKL_E_OOM = 10,           /* workspace / table memory too small */
+    ZKL_E_STATE = 11          /* ctx poisoned by an earlier asynchronous fault */
+} zkl_status;
+
+typedef enum { ZKL_VARIANT_PAPER = 0, ZKL_VARIANT_LOGUP = 1 } zkl_variant;
+
+/* Verifier challenges, canonical, host memory.  beta is the paper's beta (the north star's X);
+ * u[0..d-1] is the eq point (u[0] pairs with coordinate 0, the MSB); r[k-1] is round k's challenge. */
+typedef struct {
+    zkl_fr beta, alpha1, alpha2;
+    const zkl_fr* u;
+    const zkl_fr* r;
+} zkl_challenges;
+
+typedef struct { zkl_fr A, S, B, T, m; } zkl_final_evals;
+
+/* ---------------------------------------------------------------- context */
+const char* zkl_strerror(int status);
+/* Create a context on `device` enqueuing on `cuda_stream` (cudaStream_t; NULL = legacy stream). */
+int zkl_ctx_create(int device, void* cuda_stream, zkl_ctx** out);
+/* Multi-rank context: nccl_id is the 128-byte ncclUniqueId from rank 0 (zkl_nccl_unique_id),
+ * broadcast by the caller (torch.distributed).  NCCL is loaded at run time (libnccl.so.2). */
+int zkl_nccl_unique_id(uint8_t id[128]);
+int zkl_ctx_create_dist(int device, void* cuda_stream, const uint8_t nccl_id[128], int rank, int nranks,
+                        zkl_ctx** out);
+void zkl_ctx_destroy(zkl_ctx* ctx);
+const char* zkl_last_error(const zkl_ctx* ctx);
+/* Workspace for prepare/prove/sumcheck with local length D_local and table size N (bytes, 256-B aligned). */
+size_t zkl_workspace_bytes(uint64_t D_local, uint64_t N, int nranks);
+int zkl_ctx_set_workspace(zkl_ctx* ctx, void* device_ptr, size_t bytes);
+/* Kernel launches issued by this ctx since creation (for launch accounting). */
+uint64_t zkl_ctx_launch_count(const zkl_ctx* ctx);
+
+/* ---------------------------------------------------------------- boundary encode (a1) */
+/* canonical 32-byte LE elements (host or device, AoS) -> dst (SoA Montgomery).  E_NONCANONICAL(i). */
+int zkl_vec_import(zkl_ctx* ctx, const void* canon_le32, int src_on_device, zkl_vec dst, int64_t* err_index);
+/* signed 64-bit integers (device) -> Fr (x < 0 maps to r - |x|, reading 15). */
+int zkl_vec_import_i64(zkl_ctx* ctx, const int64_t* x_dev, zkl_vec dst);
+/* function lookup input: dst_i = x_i + alpha_f * y_i from int32 device arrays. */
+int zkl_vec_import_pair(zkl_ctx* ctx, const int32_t* x_dev, const int32_t* y_dev, const zkl_fr* alpha_f,
+                        zkl_vec dst);
+/* src (SoA Montgomery) -> canonical 32-byte LE elements (host or device, AoS). */
+int zkl_vec_export(zkl_ctx* ctx, zkl_vec src, void* canon_le32, int dst_on_device);
+
+/* ---------------------------------------------------------------- table handle (a2) */
+/* Device memory the caller provides for a table of N entries. */
+size_t zkl_table_bytes(uint64_t N);
+/* Validate (N power of two, entries distinct) and index T (a copy is kept in `mem`).
+ * E_SHAPE, E_DUP_TABLE(smallest later duplicate), E_OOM. */
+int zkl_table_create(zkl_ctx* ctx, zkl_vec T, void* mem, size_t mem_bytes, zkl_table** out, int64_t* err_index);
+void zkl_table_destroy(zkl_table* table);
+
+/* ---------------------------------------------------------------- the hot path */
+/* tlookup-Prep (Eq. hab22-coefs): m_dev[j] = #{i : S_i = T_j}
+ * over ALL ranks (u32, device, N entries).  D is the global length.  E_NOT_IN_TABLE(smallest i). */
+int zkl_tlookup_prepare(zkl_ctx* ctx, zkl_vec S_local, uint64_t D, const zkl_table* T, uint32_t* m_dev,
+                        int64_t* err_index);
+
+/* tlookup-Prove: A_local_out = 1/(beta + S_local), B_out = 1/(beta + T)
+ * (LOGUP: m/(beta + T)), then the log2(D)-round sumcheck of Eq. tlookup-sumcheck.
+ * round_evals: host, log2(D) x 4 canonical values g_k(0..3), k = 1..log2 D.  finals: host.
+ * A_local_out / B_out may have limbs == NULL (not materialised for the caller; A is still computed).
+ * E_DIV_ZERO_T / E_DIV_ZERO_S (err_index), E_SHAPE. */
+int zkl_tlookup_prove(zkl_ctx* ctx, zkl_vec S_local, uint64_t D, const zkl_table* T, const uint32_t* m_dev,
+                      const zkl_challenges* ch, zkl_variant variant, zkl_vec A_local_out, zkl_vec B_out,
+                      zkl_fr* round_evals, zkl_final_evals* finals, int64_t* err_index);
+
+/* The sumcheck alone on caller-supplied vectors (any values: tamper trials, benchmarking); inputs are
+ * never modified.  m_fr is m as field elements (SoA Montgomery, N).  B is the variant's B. */
+int zkl_sumcheck_prove(zkl_ctx* ctx, zkl_vec A_local, zkl_vec S_local, uint64_t D, zkl_vec B, zkl_vec T,
+                       zkl_vec m_fr, const zkl_challenges* ch, zkl_variant variant, zkl_fr* round_evals,
+                       zkl_final_evals* finals);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZKL_H */

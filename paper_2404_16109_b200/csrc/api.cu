@@ -1,0 +1,759 @@
+// The zkl C ABI (include/zkl.h): host orchestration of the tlookup hot path on sm_100a.
+//
+// Per proof:
+//   main stream: setup scalars, eq tables -> [D side] batched inversion of A fused with round 1,
+//                fused fold+eval rounds, single-CTA tail -> per-round rank sums
+//   side stream: [table side] B = 1/(beta+T) (batch inversion), m, e~(u', .), table rounds
+//   join:        (P > 1: all-gather of rank sums + folded finals, replicated last log2 P rounds)
+//                derivation of every g_k(0..3) and the final evaluations, one D2H copy.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <stdarg.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "kernels.cuh"
+#include "nccl_loader.h"
+
+using namespace zkl;
+
+namespace {
+
+constexpr int kSMs = 148;
+
+int set_err(zkl_ctx* ctx, int st, const char* fmt, ...) {
+    if (ctx) {
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(ctx->last_error, sizeof(ctx->last_error), fmt, ap);
+        va_end(ap);
+    }
+    return st;
+}
+
+#define CUDA_TRY(ctx, call)                                                                         \
+    do {                                                                                            \
+        cudaError_t e_ = (call);                                                                    \
+        if (e_ != cudaSuccess) {                                                                    \
+            if (e_ != cudaErrorInvalidValue && e_ != cudaErrorMemoryAllocation) (ctx)->poisoned = 1; \
+            return set_err((ctx), ZKL_E_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_),       \
+                           __FILE__, __LINE__);                                                     \
+        }                                                                                           \
+    } while (0)
+
+#define LAUNCH(ctx, kern, grid, block, smem, stream, ...)                                           \
+    do {                                                                                            \
+        kern<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                                   \
+        (ctx)->launches++;                                                                          \
+        CUDA_TRY(ctx, cudaGetLastError());                                                          \
+    } while (0)
+
+bool is_pow2(uint64_t x) { return x && !(x & (x - 1)); }
+int ilog2(uint64_t x) { int k = 0; while ((1ull << k) < x) ++k; return k; }
+size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+size_t soa_bytes(uint64_t n) { return align_up(8 * 4 * std::max<uint64_t>(n, 4)); }
+
+unsigned grid_for(uint64_t work, unsigned threads, unsigned cap = kSMs * 8) {
+    uint64_t g = (work + threads - 1) / threads;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (unsigned)g;
+}
+
+int hist_rows_for(uint64_t Dp, uint64_t N) {
+    uint64_t ntiles = (Dp + kHistTile - 1) / kHistTile;
+    uint64_t cap = std::max<uint64_t>(1, (256ull << 20) / (4 * N));
+    return (int)std::min<uint64_t>(std::min<uint64_t>(kSMs, ntiles), cap);
+}
+
+// ------------------------------------------------------------------ plan + workspace layout
+struct Plan {
+    uint64_t D, Dp, N;
+    int d, dl, n, pbits, P, rank;
+    bool small;          // Dp < kInvTile: the tail kernel does everything
+    int k0;              // first tail round
+    int fold_in;         // the tail folds its input on load
+    RoundDesc rd[kMaxRounds];
+    uint32_t tnb[kMaxRounds];
+    EqJob jobs[2 * kMaxRounds];
+    int njobs;
+    uint64_t arena;
+    uint64_t ntiles;     // inversion tiles (Dp / 4096)
+    int inv_blocks;
+    int hist_rows;
+    // workspace offsets
+    size_t o_out, o_sc, o_err, o_rounds, o_jobs, o_chal, o_part, o_tpart, o_tnb, o_rank, o_gath, o_repl, o_tsum,
+        o_fin, o_tfin, o_gfin, o_arena, o_hist, o_tot, o_totinv, o_A, o_A1, o_S1, o_A2, o_S2, o_tB, o_tX, o_tM,
+        o_tE, o_tp[2][4], total;
+};
+
+void choose_round(Plan& p, int k, uint64_t npairs, int gbits, int nblocks) {
+    RoundDesc& r = p.rd[k - 1];
+    r.gbits = gbits;
+    r.nblocks = nblocks;
+    (void)npairs;
+}
+
+void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode, const zkl_fr* u) {
+    memset(&p, 0, sizeof(p));
+    p.D = D; p.N = N; p.P = P; p.rank = rank;
+    p.d = ilog2(D); p.n = ilog2(N); p.pbits = ilog2(P);
+    p.dl = p.d - p.pbits;
+    p.Dp = D / P;
+    p.small = p.Dp < (uint64_t)kInvTile;
+    p.ntiles = p.small ? 0 : p.Dp / kInvTile;
+    p.inv_blocks = p.small ? 0 : (int)std::min<uint64_t>(p.ntiles, kSMs * 4);
+    p.hist_rows = hist_rows_for(p.Dp, N);
+    // ---- D-side local rounds
+    if (p.small) {
+        p.k0 = 1;
+        p.fold_in = 0;
+    } else {
+        int k = 1;
+        // round 1: inversion tiles (prove) or k_round<false> (sumcheck)
+        if (prove_mode) {
+            choose_round(p, 1, p.Dp / 2, 11, p.inv_blocks);
+        }
+        for (k = 1; k <= p.dl; ++k) {
+            const uint64_t nk = p.Dp >> (k - 1);   // elements at round k
+            if (nk <= (uint64_t)kTailMax) break;
+            if (k == 1 && prove_mode) continue;
+            const uint64_t np = nk / 2;
+            int gbits = 12;
+            while (gbits > 8 && (np >> gbits) < (uint64_t)kSMs) --gbits;
+            if ((1ull << gbits) > np) gbits = ilog2(np);
+            const int nb = (int)std::min<uint64_t>(np >> gbits, (uint64_t)kMaxBlocks);
+            choose_round(p, k, np, gbits, nb);
+        }
+        p.k0 = k;
+        p.fold_in = 1;
+    }
+    for (int k = p.k0; k <= p.dl; ++k) {
+        p.rd[k - 1].gbits = p.dl - k;
+        p.rd[k - 1].nblocks = 1;
+        p.rd[k - 1].direct_h1 = 1;
+    }
+    for (int k = 1; k <= p.dl; ++k) {
+        if (k == 1 && !prove_mode) p.rd[0].direct_h1 = 1;
+        const zkl_fr& uc = u[p.d - k];
+        bool zero = true;
+        for (int l = 0; l < 8; ++l) zero &= uc.w[l] == 0;
+        if (zero) p.rd[k - 1].direct_h1 = 1;
+    }
+    // replicated rounds (P > 1): all remaining coordinates are global
+    for (int k = p.dl + 1; k <= p.d; ++k) {
+        p.rd[k - 1].gbits = p.d - k;
+        p.rd[k - 1].nblocks = 1;
+        p.rd[k - 1].direct_h1 = 1;
+    }
+    // ---- eq arena jobs: per round E_lo then E_hi
+    uint64_t off = 0;
+    int nj = 0;
+    for (int k = 1; k <= p.d; ++k) {
+        RoundDesc& r = p.rd[k - 1];
+        const bool local = k <= p.dl;
+        r.elo_off = off;
+        p.jobs[nj++] = EqJob{off, r.gbits, (uint32_t)(p.d - k - r.gbits), 0, 0};
+        off += 1ull << r.gbits;
+        r.ehi_off = off;
+        const uint32_t hb = local ? (uint32_t)(p.dl - k - r.gbits) : 0;
+        p.jobs[nj++] = EqJob{off, hb, local ? (uint32_t)p.pbits : 0u, local ? 1u : 0u, 0};
+        off += 1ull << hb;
+    }
+    p.njobs = nj;
+    p.arena = off;
+    // ---- table rounds
+    for (int k = 1; k <= p.n; ++k) p.tnb[k - 1] = grid_for(N >> k, 256, kMaxBlocks);
+    // ---- workspace layout
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t r = o; o += align_up(bytes); return r; };
+    p.o_out = take(sizeof(ProofOut));
+    p.o_sc = take(sizeof(ProofScalars));
+    p.o_err = take(4 * sizeof(unsigned long long));
+    p.o_rounds = take(sizeof(RoundDesc) * kMaxRounds);
+    p.o_jobs = take(sizeof(EqJob) * 2 * kMaxRounds);
+    p.o_chal = take(sizeof(zkl_fr) * (3 + 2 * kMaxRounds));
+    p.o_part = take(sizeof(fr) * (size_t)kMaxRounds * kSlots * kMaxBlocks);
+    p.o_tpart = take(sizeof(fr) * (size_t)kMaxRounds * 4 * kMaxBlocks);
+    p.o_tnb = take(sizeof(uint32_t) * kMaxRounds);
+    p.o_rank = take(sizeof(fr) * kMaxRounds * kSlots);
+    p.o_gath = take(sizeof(fr) * (size_t)P * kMaxRounds * kSlots);
+    p.o_repl = take(sizeof(fr) * kMaxRounds * kSlots);
+    p.o_tsum = take(sizeof(fr) * kMaxRounds * 4);
+    p.o_fin = take(sizeof(fr) * 4);
+    p.o_tfin = take(sizeof(fr) * 4);
+    p.o_gfin = take(sizeof(fr) * 2 * (size_t)P);
+    p.o_arena = take(sizeof(fr) * p.arena);
+    p.o_hist = take(sizeof(uint32_t) * (size_t)p.hist_rows * N);
+    p.o_tot = take(soa_bytes(p.ntiles));
+    p.o_totinv = take(soa_bytes(p.ntiles));
+    p.o_A = take(soa_bytes(p.Dp));
+    p.o_A1 = take(soa_bytes(p.Dp / 2));
+    p.o_S1 = take(soa_bytes(p.Dp / 2));
+    p.o_A2 = take(soa_bytes(p.Dp / 4));
+    p.o_S2 = take(soa_bytes(p.Dp / 4));
+    p.o_tB = take(soa_bytes(N));
+    p.o_tX = take(soa_bytes(N));
+    p.o_tM = take(soa_bytes(N));
+    p.o_tE = take(soa_bytes(N));
+    for (int q = 0; q < 4; ++q) p.o_tp[0][q] = take(soa_bytes(N / 2));
+    for (int q = 0; q < 4; ++q) p.o_tp[1][q] = take(soa_bytes(N / 4));
+    p.total = o;
+}
+
+template <typename T>
+T* at(zkl_ctx* ctx, size_t off) { return reinterpret_cast<T*>(ctx->ws + off); }
+
+int check_ctx(zkl_ctx* ctx) {
+    if (!ctx) return ZKL_E_ARG;
+    if (ctx->poisoned) return set_err(ctx, ZKL_E_STATE, "context poisoned by an earlier CUDA fault");
+    CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    return ZKL_OK;
+}
+
+int check_vec(zkl_ctx* ctx, const zkl_vec& v, uint64_t n, const char* name) {
+    if (!v.limbs) return set_err(ctx, ZKL_E_ARG, "%s: null", name);
+    if (v.n != n) return set_err(ctx, ZKL_E_SHAPE, "%s: length %llu, expected %llu", name,
+                                 (unsigned long long)v.n, (unsigned long long)n);
+    if (n >= 4 && ((n & 3) || ((uintptr_t)v.limbs & 15)))
+        return set_err(ctx, ZKL_E_ARG, "%s: limbs must be 16-byte aligned and n a multiple of 4", name);
+    return ZKL_OK;
+}
+
+int check_shape(zkl_ctx* ctx, uint64_t D, uint64_t N) {
+    if (!is_pow2(D) || !is_pow2(N) || N > D)
+        return set_err(ctx, ZKL_E_SHAPE, "D=%llu N=%llu: need powers of two with N | D (PAPER.md:258)",
+                       (unsigned long long)D, (unsigned long long)N);
+    if (ilog2(D) > kMaxRounds) return set_err(ctx, ZKL_E_SHAPE, "log2 D > %d", kMaxRounds);
+    if (D % (uint64_t)ctx->nranks || !is_pow2((uint64_t)ctx->nranks) || D / ctx->nranks < 1)
+        return set_err(ctx, ZKL_E_SHAPE, "P=%d must be a power of two dividing D", ctx->nranks);
+    return ZKL_OK;
+}
+
+int need_ws(zkl_ctx* ctx, const Plan& p) {
+    if (!ctx->ws || ctx->ws_bytes < p.total)
+        return set_err(ctx, ZKL_E_OOM, "workspace %zu bytes < %zu required (zkl_workspace_bytes)", ctx->ws_bytes,
+                       p.total);
+    return ZKL_OK;
+}
+
+int sync_stream(zkl_ctx* ctx) {
+    cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) {
+        ctx->poisoned = 1;
+        return set_err(ctx, ZKL_E_CUDA, "asynchronous CUDA error: %s", cudaGetErrorString(e));
+    }
+    return ZKL_OK;
+}
+
+// ------------------------------------------------------------------ shared proof driver
+struct ProveArgs {
+    bool prove_mode;
+    zkl_vec S, A_in, A_out, B_out;       // A_in: sumcheck mode
+    const zkl_table* table;              // prove mode
+    const uint32_t* m_dev;               // prove mode
+    zkl_vec B_in, T_in, m_fr_in;         // sumcheck mode
+    const zkl_challenges* ch;
+    int variant;
+};
+
+int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals, zkl_final_evals* finals,
+              int64_t* err_index) {
+    if (err_index) *err_index = -1;
+    const uint64_t N = a.prove_mode ? a.table->N : a.T_in.n;
+    int st;
+    if ((st = check_shape(ctx, D, N))) return st;
+    if (!a.ch || !a.ch->u || !a.ch->r || !round_evals || !finals) return set_err(ctx, ZKL_E_ARG, "null argument");
+    Plan p;
+    make_plan(p, D, N, ctx->nranks, ctx->rank, a.prove_mode, a.ch->u);
+    if ((st = need_ws(ctx, p))) return st;
+    if ((st = check_vec(ctx, a.S, p.Dp, "S_local"))) return st;
+    if (!a.prove_mode) {
+        if ((st = check_vec(ctx, a.A_in, p.Dp, "A_local"))) return st;
+        if ((st = check_vec(ctx, a.B_in, N, "B"))) return st;
+        if ((st = check_vec(ctx, a.T_in, N, "T"))) return st;
+        if ((st = check_vec(ctx, a.m_fr_in, N, "m_fr"))) return st;
+    } else {
+        if (!a.m_dev) return set_err(ctx, ZKL_E_ARG, "m_dev null");
+        if (a.A_out.limbs && (st = check_vec(ctx, a.A_out, p.Dp, "A_local_out"))) return st;
+        if (a.B_out.limbs && (st = check_vec(ctx, a.B_out, N, "B_out"))) return st;
+    }
+    cudaStream_t s = ctx->stream, s2 = ctx->side;
+    ProofScalars* sc = at<ProofScalars>(ctx, p.o_sc);
+    unsigned long long* err = at<unsigned long long>(ctx, p.o_err);   // [0] S, [1] T
+    RoundDesc* rounds = at<RoundDesc>(ctx, p.o_rounds);
+    EqJob* jobs = at<EqJob>(ctx, p.o_jobs);
+    zkl_fr* chal = at<zkl_fr>(ctx, p.o_chal);
+    fr* partials = at<fr>(ctx, p.o_part);
+    fr* tpart = at<fr>(ctx, p.o_tpart);
+    uint32_t* tnb = at<uint32_t>(ctx, p.o_tnb);
+    fr* rank_sums = at<fr>(ctx, p.o_rank);
+    fr* gath = at<fr>(ctx, p.o_gath);
+    fr* repl = at<fr>(ctx, p.o_repl);
+    fr* tsum = at<fr>(ctx, p.o_tsum);
+    fr* fin = at<fr>(ctx, p.o_fin);
+    fr* tfin = at<fr>(ctx, p.o_tfin);
+    fr* arena = at<fr>(ctx, p.o_arena);
+    ProofOut* out = at<ProofOut>(ctx, p.o_out);
+
+    // ---- host -> device: challenges and the plan (one staging buffer, pinned)
+    struct Staging {
+        zkl_fr chal[3 + 2 * kMaxRounds];
+        RoundDesc rounds[kMaxRounds];
+        EqJob jobs[2 * kMaxRounds];
+        uint32_t tnb[kMaxRounds];
+    };
+    Staging* hs = reinterpret_cast<Staging*>((uint8_t*)ctx->host_out + sizeof(ProofOut));
+    hs->chal[0] = a.ch->beta;
+    hs->chal[1] = a.ch->alpha1;
+    hs->chal[2] = a.ch->alpha2;
+    for (int c = 0; c < p.d; ++c) hs->chal[3 + c] = a.ch->u[c];
+    for (int k = 0; k < p.d; ++k) hs->chal[3 + p.d + k] = a.ch->r[k];
+    memcpy(hs->rounds, p.rd, sizeof(p.rd));
+    memcpy(hs->jobs, p.jobs, sizeof(p.jobs));
+    memcpy(hs->tnb, p.tnb, sizeof(p.tnb));
+    CUDA_TRY(ctx, cudaMemcpyAsync(chal, hs->chal, sizeof(hs->chal), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(rounds, hs->rounds, sizeof(hs->rounds), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(jobs, hs->jobs, sizeof(hs->jobs), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(tnb, hs->tnb, sizeof(hs->tnb), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(ctx, cudaMemsetAsync(err, 0xff, 4 * sizeof(unsigned long long), s));
+    LAUNCH(ctx, k_setup, 1, 1, 0, s, chal, p.d, p.pbits, p.rank, N, D, sc);
+    LAUNCH(ctx, k_eq_fill, grid_for(p.arena, 256), 256, 0, s, jobs, p.njobs, p.arena, sc, arena);
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, s));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(s2, ctx->ev_fork, 0));
+
+    // ================= table side (side stream)
+    uint32_t* tB = at<uint32_t>(ctx, p.o_tB);
+    uint32_t* tX = at<uint32_t>(ctx, p.o_tX);
+    uint32_t* tM = at<uint32_t>(ctx, p.o_tM);
+    uint32_t* tE = at<uint32_t>(ctx, p.o_tE);
+    const uint32_t* Tsrc = a.prove_mode ? a.table->T : a.T_in.limbs;
+    if (a.prove_mode) {
+        LAUNCH(ctx, k_add_beta, grid_for(N, 256), 256, 0, s2, Tsrc, N, sc, tX, err + 1);
+        const unsigned bt = (unsigned)std::min<uint64_t>(1024, std::max<uint64_t>(32, N));
+        LAUNCH(ctx, k_batch_invert, 1, bt, 4 * bt * sizeof(fr), s2, tX, N, tB);
+        LAUNCH(ctx, k_tab_init, grid_for(N, 256), 256, 0, s2, a.m_dev, N, tM, tB, sc, p.d, p.n, a.variant, tE);
+        if (a.B_out.limbs) LAUNCH(ctx, k_copy_vec, grid_for(8 * N, 256), 256, 0, s2, tB, N, a.B_out.limbs);
+    } else {
+        LAUNCH(ctx, k_copy_vec, grid_for(8 * N, 256), 256, 0, s2, a.B_in.limbs, N, tB);
+        LAUNCH(ctx, k_copy_vec, grid_for(8 * N, 256), 256, 0, s2, a.m_fr_in.limbs, N, tM);
+        // E2 = e~(u[d-n:], .) only (m == nullptr)
+        LAUNCH(ctx, k_tab_init, grid_for(N, 256), 256, 0, s2, (const uint32_t*)nullptr, N, tX, tB, sc, p.d, p.n,
+               a.variant, tE);
+    }
+    {
+        const uint32_t *cB = tB, *cT = Tsrc, *cM = tM, *cE = tE;
+        uint64_t len = N;
+        if (p.n == 0) LAUNCH(ctx, k_tab_fin0, 1, 32, 0, s2, cB, cT, cM, cE, tfin);
+        for (int k = 1; k <= p.n; ++k) {
+            const int pp = (k - 1) & 1;
+            uint32_t* nB = at<uint32_t>(ctx, p.o_tp[pp][0]);
+            uint32_t* nT = at<uint32_t>(ctx, p.o_tp[pp][1]);
+            uint32_t* nM = at<uint32_t>(ctx, p.o_tp[pp][2]);
+            uint32_t* nE = at<uint32_t>(ctx, p.o_tp[pp][3]);
+            LAUNCH(ctx, k_tab_round, p.tnb[k - 1], 256, 0, s2, cB, cT, cM, cE, len, nB, nT, nM, nE, sc, k, a.variant,
+                   tpart + (size_t)(k - 1) * 4 * kMaxBlocks, tfin);
+            cB = nB; cT = nT; cM = nM; cE = nE;
+            len /= 2;
+        }
+        if (p.n > 0) LAUNCH(ctx, k_reduce_tab, p.n, 256, 0, s2, tpart, tnb, p.n, tsum);
+    }
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join, s2));
+
+    // ================= D side (main stream)
+    uint32_t* Abuf = a.prove_mode ? (a.A_out.limbs ? a.A_out.limbs : at<uint32_t>(ctx, p.o_A)) : nullptr;
+    const uint32_t* A1in = a.prove_mode ? Abuf : a.A_in.limbs;
+    const uint32_t* S1in = a.S.limbs;
+    const uint64_t errS_off = (uint64_t)p.rank * p.Dp;
+    const size_t tail_smem = (2 * kTailMax + 4 * kTailThreads) * sizeof(fr) + 5 * (kTailThreads / 32) * sizeof(fr);
+    if (p.small) {
+        LAUNCH(ctx, k_tail, 1, kTailThreads, tail_smem, s, A1in, S1in, p.Dp, 0, a.prove_mode ? 1 : 0, Abuf,
+               errS_off, err, sc, 1, p.dl, rounds, arena, partials, fin);
+    } else {
+        if (a.prove_mode) {
+            uint32_t* tot = at<uint32_t>(ctx, p.o_tot);
+            uint32_t* totinv = at<uint32_t>(ctx, p.o_totinv);
+            LAUNCH(ctx, k_inv_fwd, p.inv_blocks, kInvThreads, 0, s, a.S.limbs, p.Dp, sc, Abuf, tot, p.ntiles, errS_off,
+                   err);
+            const unsigned bt = (unsigned)std::min<uint64_t>(1024, std::max<uint64_t>(32, p.ntiles));
+            LAUNCH(ctx, k_batch_invert, 1, bt, 4 * bt * sizeof(fr), s, tot, p.ntiles, totinv);
+            LAUNCH(ctx, k_inv_bwd, p.inv_blocks, kInvThreads, 0, s, a.S.limbs, p.Dp, sc, Abuf, totinv, p.ntiles,
+                   arena + p.rd[0].elo_off, arena + p.rd[0].ehi_off, 1, partials);
+        }
+        const uint32_t *cA = A1in, *cS = S1in;
+        uint64_t len = p.Dp;
+        for (int k = a.prove_mode ? 2 : 1; k < p.k0; ++k) {
+            const RoundDesc& r = p.rd[k - 1];
+            fr* part = partials + (size_t)(k - 1) * kSlots * kMaxBlocks;
+            if (k == 1) {
+                LAUNCH(ctx, k_round<false>, r.nblocks, kRoundThreads, 0, s, cA, cS, len, nullptr, nullptr, sc, k,
+                       arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, (int)r.direct_h1, part);
+            } else {
+                const bool odd = (k & 1) == 0;   // k = 2 -> buffers 1
+                uint32_t* nA = at<uint32_t>(ctx, odd ? p.o_A1 : p.o_A2);
+                uint32_t* nS = at<uint32_t>(ctx, odd ? p.o_S1 : p.o_S2);
+                LAUNCH(ctx, k_round<true>, r.nblocks, kRoundThreads, 0, s, cA, cS, len, nA, nS, sc, k,
+                       arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, (int)r.direct_h1, part);
+                cA = nA; cS = nS;
+                len /= 2;
+            }
+        }
+        // tail input: the vectors of round k0-1 (len elements), folded with r_{k0-1} on load
+        LAUNCH(ctx, k_tail, 1, kTailThreads, tail_smem, s, cA, cS, len, 1, 0, (uint32_t*)nullptr, errS_off, err, sc,
+               p.k0, p.dl, rounds, arena, partials, fin);
+    }
+    if (p.dl > 0) LAUNCH(ctx, k_reduce_rounds, p.dl, 256, 0, s, partials, rounds, p.dl, rank_sums);
+    const fr* gathered = rank_sums;
+    if (ctx->nranks > 1) {
+        int rc = zkl_dist_exchange(ctx, p.dl, rank_sums, gath, fin, at<fr>(ctx, p.o_gfin));
+        if (rc) return rc;
+        gathered = gath;
+        // replicated last log2 P rounds on the gathered folded (A, S) pairs: P elements
+        // gfin layout: [A_0..A_{P-1}] [S_0..S_{P-1}] as AoS fr -> treat as SoA? use tail via AoS copy
+        LAUNCH(ctx, k_tail, 1, kTailThreads, tail_smem, s, (const uint32_t*)at<fr>(ctx, p.o_gfin),
+               (const uint32_t*)(at<fr>(ctx, p.o_gfin) + p.P), (uint64_t)p.P, 0, 0, (uint32_t*)nullptr, 0, err, sc,
+               p.dl + 1, p.d, rounds, arena, partials, fin);
+        LAUNCH(ctx, k_reduce_rounds, p.d - p.dl, 256, 0, s, partials + (size_t)p.dl * kSlots * kMaxBlocks,
+               rounds + p.dl, p.d - p.dl, repl);
+    }
+    CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
+    LAUNCH(ctx, k_derive, 1, 32, 0, s, gathered, ctx->nranks, p.dl, repl, rounds, tsum, sc, p.d, p.n, a.variant,
+           a.prove_mode ? 1 : 0, fin, tfin, out);
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->host_out, out, sizeof(ProofOut), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync((uint8_t*)ctx->host_out + offsetof(ProofOut, err_index), err,
+                                  2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    if ((st = sync_stream(ctx))) return st;
+    const ProofOut* ho = reinterpret_cast<const ProofOut*>(ctx->host_out);
+    const unsigned long long* he = reinterpret_cast<const unsigned long long*>(&ho->err_index);
+    unsigned long long eS = he[0], eT = he[1];
+    if (ctx->nranks > 1) {
+        int rc = zkl_dist_min_u64(ctx, &eS);
+        if (rc) return rc;
+    }
+    if (eT != ~0ull) {
+        if (err_index) *err_index = (int64_t)eT;
+        return set_err(ctx, ZKL_E_DIV_ZERO_T, "beta + T_%llu = 0", eT);
+    }
+    if (eS != ~0ull) {
+        if (err_index) *err_index = (int64_t)eS;
+        return set_err(ctx, ZKL_E_DIV_ZERO_S, "beta + S_%llu = 0", eS);
+    }
+    memcpy(round_evals, ho->evals, sizeof(zkl_fr) * 4 * p.d);
+    finals->A = ho->finals[0];
+    finals->S = ho->finals[1];
+    finals->B = ho->finals[2];
+    finals->T = ho->finals[3];
+    finals->m = ho->finals[4];
+    return ZKL_OK;
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+const char* zkl_strerror(int st) {
+    switch (st) {
+        case ZKL_OK: return "ok";
+        case ZKL_E_ARG: return "bad argument";
+        case ZKL_E_SHAPE: return "bad shape";
+        case ZKL_E_NONCANONICAL: return "non-canonical field element";
+        case ZKL_E_DUP_TABLE: return "duplicate table entry";
+        case ZKL_E_NOT_IN_TABLE: return "lookup not in table";
+        case ZKL_E_DIV_ZERO_T: return "division by zero (beta + T_j = 0)";
+        case ZKL_E_DIV_ZERO_S: return "division by zero (beta + S_i = 0)";
+        case ZKL_E_CUDA: return "CUDA error";
+        case ZKL_E_NCCL: return "NCCL error";
+        case ZKL_E_OOM: return "insufficient workspace";
+        case ZKL_E_STATE: return "context poisoned";
+        default: return "unknown status";
+    }
+}
+
+static int ctx_create_common(int device, void* stream, zkl_ctx** out) {
+    if (!out) return ZKL_E_ARG;
+    *out = nullptr;
+    zkl_ctx* c = (zkl_ctx*)calloc(1, sizeof(zkl_ctx));
+    if (!c) return ZKL_E_OOM;
+    c->device = device;
+    c->stream = (cudaStream_t)stream;
+    c->nranks = 1;
+    if (cudaSetDevice(device) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaMallocHost(&c->host_out, 1 << 16) != cudaSuccess) {
+        cudaGetLastError();
+        free(c);
+        return ZKL_E_CUDA;
+    }
+    const size_t tail_smem = (2 * kTailMax + 4 * kTailThreads) * sizeof(fr) + 5 * (kTailThreads / 32) * sizeof(fr);
+    cudaFuncSetAttribute(k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tail_smem);
+    cudaFuncSetAttribute(k_batch_invert, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 1024 * (int)sizeof(fr));
+    *out = c;
+    return ZKL_OK;
+}
+
+int zkl_ctx_create(int device, void* cuda_stream, zkl_ctx** out) { return ctx_create_common(device, cuda_stream, out); }
+
+int zkl_nccl_unique_id(uint8_t id[128]) { return zkl_nccl_get_unique_id(id); }
+
+int zkl_ctx_create_dist(int device, void* cuda_stream, const uint8_t nccl_id[128], int rank, int nranks,
+                        zkl_ctx** out) {
+    int st = ctx_create_common(device, cuda_stream, out);
+    if (st) return st;
+    if (nranks > 1) {
+        st = zkl_nccl_init(*out, nccl_id, rank, nranks);
+        if (st) {
+            zkl_ctx_destroy(*out);
+            *out = nullptr;
+            return st;
+        }
+    }
+    (*out)->rank = rank;
+    (*out)->nranks = nranks;
+    return ZKL_OK;
+}
+
+void zkl_ctx_destroy(zkl_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->nccl_comm) zkl_nccl_destroy(c);
+    cudaStreamSynchronize(c->side);
+    cudaStreamDestroy(c->side);
+    cudaEventDestroy(c->ev_fork);
+    cudaEventDestroy(c->ev_join);
+    cudaFreeHost(c->host_out);
+    free(c);
+}
+
+const char* zkl_last_error(const zkl_ctx* c) { return c ? c->last_error : "null ctx"; }
+
+size_t zkl_workspace_bytes(uint64_t D_local, uint64_t N, int nranks) {
+    if (!is_pow2(D_local) || !is_pow2(N) || nranks < 1) return 0;
+    std::vector<zkl_fr> u(kMaxRounds);
+    for (auto& x : u) { memset(&x, 0, sizeof(x)); x.w[0] = 1; }
+    Plan p, q;
+    make_plan(p, D_local * nranks, N, nranks, 0, true, u.data());
+    make_plan(q, D_local * nranks, N, nranks, 0, false, u.data());
+    return std::max(p.total, q.total);
+}
+
+int zkl_ctx_set_workspace(zkl_ctx* c, void* ptr, size_t bytes) {
+    if (!c) return ZKL_E_ARG;
+    if (((uintptr_t)ptr) & 255) return set_err(c, ZKL_E_ARG, "workspace must be 256-byte aligned");
+    c->ws = (uint8_t*)ptr;
+    c->ws_bytes = bytes;
+    return ZKL_OK;
+}
+
+uint64_t zkl_ctx_launch_count(const zkl_ctx* c) { return c ? c->launches : 0; }
+
+// ---------------------------------------------------------------- a1
+int zkl_vec_import(zkl_ctx* ctx, const void* canon, int src_on_device, zkl_vec dst, int64_t* err_index) {
+    int st;
+    if ((st = check_ctx(ctx))) return st;
+    if (err_index) *err_index = -1;
+    if (!canon) return set_err(ctx, ZKL_E_ARG, "null source");
+    if ((st = check_vec(ctx, dst, dst.n, "dst"))) return st;
+    if (dst.n == 0) return ZKL_OK;
+    const uint32_t* src = (const uint32_t*)canon;
+    void* tmp = nullptr;
+    if (!src_on_device) {
+        CUDA_TRY(ctx, cudaMallocAsync(&tmp, 32 * dst.n, ctx->stream));
+        CUDA_TRY(ctx, cudaMemcpyAsync(tmp, canon, 32 * dst.n, cudaMemcpyHostToDevice, ctx->stream));
+        src = (const uint32_t*)tmp;
+    }
+    unsigned long long* err = reinterpret_cast<unsigned long long*>((uint8_t*)ctx->host_out + 60000);
+    unsigned long long* derr = nullptr;
+    CUDA_TRY(ctx, cudaMallocAsync((void**)&derr, sizeof(unsigned long long), ctx->stream));
+    CUDA_TRY(ctx, cudaMemsetAsync(derr, 0xff, sizeof(unsigned long long), ctx->stream));
+    LAUNCH(ctx, k_import_canon, grid_for(dst.n, 256), 256, 0, ctx->stream, src, dst.n, dst.limbs, derr);
+    CUDA_TRY(ctx, cudaMemcpyAsync(err, derr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaFreeAsync(derr, ctx->stream));
+    if (tmp) CUDA_TRY(ctx, cudaFreeAsync(tmp, ctx->stream));
+    if ((st = sync_stream(ctx))) return st;
+    if (*err != ~0ull) {
+        if (err_index) *err_index = (int64_t)*err;
+        return set_err(ctx, ZKL_E_NONCANONICAL, "element %llu >= r", *err);
+    }
+    return ZKL_OK;
+}
+
+int zkl_vec_import_i64(zkl_ctx* ctx, const int64_t* x, zkl_vec dst) {
+    int st;
+    if ((st = check_ctx(ctx))) return st;
+    if (!x) return set_err(ctx, ZKL_E_ARG, "null source");
+    if ((st = check_vec(ctx, dst, dst.n, "dst"))) return st;
+    if (dst.n == 0) return ZKL_OK;
+    LAUNCH(ctx, k_import_i64, grid_for(dst.n, 256), 256, 0, ctx->stream, x, dst.n, dst.limbs);
+    return sync_stream(ctx);
+}
+
+int zkl_vec_import_pair(zkl_ctx* ctx, const int32_t* x, const int32_t* y, const zkl_fr* alpha_f, zkl_vec dst) {
+    int st;
+    if ((st = check_ctx(ctx))) return st;
+    if (!x || !y || !alpha_f) return set_err(ctx, ZKL_E_ARG, "null argument");
+    if ((st = check_vec(ctx, dst, dst.n, "dst"))) return st;
+    if (dst.n == 0) return ZKL_OK;
+    // alpha_f -> Montgomery on the device (one launch, no host arithmetic)
+    fr* af = nullptr;
+    CUDA_TRY(ctx, cudaMallocAsync((void**)&af, sizeof(fr), ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpyAsync(af, alpha_f, sizeof(fr), cudaMemcpyHostToDevice, ctx->stream));
+    LAUNCH(ctx, k_import_canon, 1, 32, 0, ctx->stream, (const uint32_t*)af, 1, (uint32_t*)af,
+           (unsigned long long*)nullptr);
+    LAUNCH(ctx, k_import_pair_dev, grid_for(dst.n, 256), 256, 0, ctx->stream, x, y, dst.n, af, dst.limbs);
+    CUDA_TRY(ctx, cudaFreeAsync(af, ctx->stream));
+    return sync_stream(ctx);
+}
+
+int zkl_vec_export(zkl_ctx* ctx, zkl_vec src, void* canon, int dst_on_device) {
+    int st;
+    if ((st = check_ctx(ctx))) return st;
+    if (!canon) return set_err(ctx, ZKL_E_ARG, "null destination");
+    if ((st = check_vec(ctx, src, src.n, "src"))) return st;
+    if (src.n == 0) return ZKL_OK;
+    uint32_t* dst = (uint32_t*)canon;
+    void* tmp = nullptr;
+    if (!dst_on_device) {
+        CUDA_TRY(ctx, cudaMallocAsync(&tmp, 32 * src.n, ctx->stream));
+        dst = (uint32_t*)tmp;
+    }
+    LAUNCH(ctx, k_export, grid_for(src.n, 256), 256, 0, ctx->stream, src.limbs, src.n, dst);
+    if (tmp) {
+        CUDA_TRY(ctx, cudaMemcpyAsync(canon, tmp, 32 * src.n, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(ctx, cudaFreeAsync(tmp, ctx->stream));
+    }
+    return sync_stream(ctx);
+}
+
+// ---------------------------------------------------------------- a2
+size_t zkl_table_bytes(uint64_t N) {
+    if (!is_pow2(N)) return 0;
+    uint64_t slots = std::max<uint64_t>(64, 2 * N);
+    return soa_bytes(N) + align_up(4 * slots);
+}
+
+int zkl_table_create(zkl_ctx* ctx, zkl_vec T, void* mem, size_t mem_bytes, zkl_table** out, int64_t* err_index) {
+    int st;
+    if (err_index) *err_index = -1;
+    if (!out) return ZKL_E_ARG;
+    *out = nullptr;
+    if ((st = check_ctx(ctx))) return st;
+    if (!is_pow2(T.n)) return set_err(ctx, ZKL_E_SHAPE, "N=%llu is not a power of two", (unsigned long long)T.n);
+    if ((st = check_vec(ctx, T, T.n, "T"))) return st;
+    const uint64_t N = T.n;
+    if (!mem || mem_bytes < zkl_table_bytes(N) || ((uintptr_t)mem & 255))
+        return set_err(ctx, ZKL_E_OOM, "table memory: need %zu bytes, 256-byte aligned", zkl_table_bytes(N));
+    zkl_table* t = (zkl_table*)calloc(1, sizeof(zkl_table));
+    if (!t) return ZKL_E_OOM;
+    const uint64_t nslots = std::max<uint64_t>(64, 2 * N);
+    t->N = N;
+    t->T = (uint32_t*)mem;
+    t->slots = (uint32_t*)((uint8_t*)mem + soa_bytes(N));
+    t->slot_mask = (uint32_t)(nslots - 1);
+    t->device = ctx->device;
+    unsigned long long* derr = nullptr;
+    auto fail = [&](int code) { free(t); return code; };
+    if (cudaMallocAsync((void**)&derr, sizeof(unsigned long long), ctx->stream) != cudaSuccess) return fail(ZKL_E_CUDA);
+    cudaMemsetAsync(derr, 0xff, sizeof(unsigned long long), ctx->stream);
+    cudaMemsetAsync(t->slots, 0, 4 * nslots, ctx->stream);
+    k_table_copy<<<grid_for(N, 256), 256, 0, ctx->stream>>>(T.limbs, N, t->T);
+    k_table_insert<<<grid_for(N, 256), 256, 0, ctx->stream>>>(t->T, N, t->slots, t->slot_mask);
+    k_table_dups<<<grid_for(N, 256), 256, 0, ctx->stream>>>(t->T, N, t->slots, t->slot_mask, derr);
+    ctx->launches += 3;
+    unsigned long long* herr = reinterpret_cast<unsigned long long*>((uint8_t*)ctx->host_out + 60000);
+    cudaMemcpyAsync(herr, derr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream);
+    cudaFreeAsync(derr, ctx->stream);
+    if ((st = sync_stream(ctx))) return fail(st);
+    if (*herr != ~0ull) {
+        if (err_index) *err_index = (int64_t)*herr;
+        set_err(ctx, ZKL_E_DUP_TABLE, "T_%llu repeats an earlier entry", *herr);
+        return fail(ZKL_E_DUP_TABLE);
+    }
+    *out = t;
+    return ZKL_OK;
+}
+
+void zkl_table_destroy(zkl_table* t) { free(t); }
+
+// ---------------------------------------------------------------- a3
+int zkl_tlookup_prepare(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T, uint32_t* m_dev, int64_t* err_index) {
+    int st;
+    if (err_index) *err_index = -1;
+    if ((st = check_ctx(ctx))) return st;
+    if (!T || !m_dev) return set_err(ctx, ZKL_E_ARG, "null argument");
+    if ((st = check_shape(ctx, D, T->N))) return st;
+    Plan p;
+    std::vector<zkl_fr> u(kMaxRounds);
+    for (auto& x : u) { memset(&x, 0, sizeof(x)); x.w[0] = 1; }
+    make_plan(p, D, T->N, ctx->nranks, ctx->rank, true, u.data());
+    if ((st = need_ws(ctx, p))) return st;
+    if ((st = check_vec(ctx, S, p.Dp, "S_local"))) return st;
+    unsigned long long* err = at<unsigned long long>(ctx, p.o_err);
+    uint32_t* rows = at<uint32_t>(ctx, p.o_hist);
+    CUDA_TRY(ctx, cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), ctx->stream));
+    TableView tv{T->T, T->slots, T->N, T->slot_mask};
+    LAUNCH(ctx, k_hist_rows, p.hist_rows, kHistThreads, 0, ctx->stream, S.limbs, p.Dp, (uint64_t)ctx->rank * p.Dp,
+           tv, rows, p.n + 1, err);
+    LAUNCH(ctx, k_hist_colsum, grid_for(T->N, 256), 256, 0, ctx->stream, rows, p.hist_rows, T->N, m_dev);
+    if (ctx->nranks > 1) {
+        int rc = zkl_dist_allreduce_u32(ctx, m_dev, T->N);
+        if (rc) return rc;
+    }
+    unsigned long long* herr = reinterpret_cast<unsigned long long*>((uint8_t*)ctx->host_out + 60000);
+    CUDA_TRY(ctx, cudaMemcpyAsync(herr, err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+    if ((st = sync_stream(ctx))) return st;
+    unsigned long long e = *herr;
+    if (ctx->nranks > 1) {
+        int rc = zkl_dist_min_u64(ctx, &e);
+        if (rc) return rc;
+    }
+    if (e != ~0ull) {
+        if (err_index) *err_index = (int64_t)e;
+        return set_err(ctx, ZKL_E_NOT_IN_TABLE, "S_%llu is not in T", e);
+    }
+    return ZKL_OK;
+}
+
+// ---------------------------------------------------------------- a4-a9
+int zkl_tlookup_prove(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T, const uint32_t* m_dev,
+                      const zkl_challenges* ch, zkl_variant variant, zkl_vec A_out, zkl_vec B_out,
+                      zkl_fr* round_evals, zkl_final_evals* finals, int64_t* err_index) {
+    int st;
+    if ((st = check_ctx(ctx))) return st;
+    if (!T) return set_err(ctx, ZKL_E_ARG, "null table");
+    ProveArgs a;
+    memset(&a, 0, sizeof(a));
+    a.prove_mode = true;
+    a.S = S;
+    a.A_out = A_out;
+    a.B_out = B_out;
+    a.table = T;
+    a.m_dev = m_dev;
+    a.ch = ch;
+    a.variant = variant;
+    return run_proof(ctx, D, a, round_evals, finals, err_index);
+}
+
+int zkl_sumcheck_prove(zkl_ctx* ctx, zkl_vec A, zkl_vec S, uint64_t D, zkl_vec B, zkl_vec T, zkl_vec m_fr,
+                       const zkl_challenges* ch, zkl_variant variant, zkl_fr* round_evals, zkl_final_evals* finals) {
+    int st;
+    if ((st = check_ctx(ctx))) return st;
+    ProveArgs a;
+    memset(&a, 0, sizeof(a));
+    a.prove_mode = false;
+    a.S = S;
+    a.A_in = A;
+    a.B_in = B;
+    a.T_in = T;
+    a.m_fr_in = m_fr;
+    a.ch = ch;
+    a.variant = variant;
+    return run_proof(ctx, D, a, round_evals, finals, nullptr);
+}
+
+}  // extern "C"

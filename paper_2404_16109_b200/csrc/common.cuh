@@ -1,0 +1,158 @@
+// Shared device/host helpers of the zkl library (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/zkl.h"
+#include "fr.cuh"
+
+namespace zkl {
+
+constexpr int kMaxRounds = 40;          // log2 D <= 40
+constexpr int kSlots = 5;               // per-round D-side partial sums: H0, H1, Hinf, a0, a1
+enum { SLOT_H0 = 0, SLOT_H1 = 1, SLOT_HINF = 2, SLOT_A0 = 3, SLOT_A1 = 4 };
+constexpr int kMaxBlocks = 1184;        // partial-sum rows per round (148 SMs x 8)
+constexpr int kTailMax = 2048;          // the single-CTA tail holds <= 2048 elements of A and S
+
+// ------------------------------------------------------------------ SoA access
+__device__ __forceinline__ fr ld_fr(const uint32_t* __restrict__ base, uint64_t n, uint64_t i) {
+    fr x;
+#pragma unroll
+    for (int l = 0; l < 8; ++l) x.v[l] = base[(uint64_t)l * n + i];
+    return x;
+}
+
+__device__ __forceinline__ void st_fr(uint32_t* __restrict__ base, uint64_t n, uint64_t i, const fr& x) {
+#pragma unroll
+    for (int l = 0; l < 8; ++l) base[(uint64_t)l * n + i] = x.v[l];
+}
+
+// 4 consecutive elements i..i+3 (i % 4 == 0, n % 4 == 0): one 128-bit load per limb plane
+__device__ __forceinline__ void ld_fr4(const uint32_t* __restrict__ base, uint64_t n, uint64_t i, fr (&x)[4]) {
+#pragma unroll
+    for (int l = 0; l < 8; ++l) {
+        uint4 q = __ldg(reinterpret_cast<const uint4*>(base + (uint64_t)l * n + i));
+        x[0].v[l] = q.x; x[1].v[l] = q.y; x[2].v[l] = q.z; x[3].v[l] = q.w;
+    }
+}
+
+__device__ __forceinline__ void st_fr4(uint32_t* __restrict__ base, uint64_t n, uint64_t i, const fr (&x)[4]) {
+#pragma unroll
+    for (int l = 0; l < 8; ++l) {
+        uint4 q = make_uint4(x[0].v[l], x[1].v[l], x[2].v[l], x[3].v[l]);
+        *reinterpret_cast<uint4*>(base + (uint64_t)l * n + i) = q;
+    }
+}
+
+// 2 consecutive elements (i even, n even): one 64-bit access per plane
+__device__ __forceinline__ void ld_fr2(const uint32_t* __restrict__ base, uint64_t n, uint64_t i, fr (&x)[2]) {
+#pragma unroll
+    for (int l = 0; l < 8; ++l) {
+        uint2 q = __ldg(reinterpret_cast<const uint2*>(base + (uint64_t)l * n + i));
+        x[0].v[l] = q.x; x[1].v[l] = q.y;
+    }
+}
+
+__device__ __forceinline__ void st_fr2(uint32_t* __restrict__ base, uint64_t n, uint64_t i, const fr& a,
+                                       const fr& b) {
+#pragma unroll
+    for (int l = 0; l < 8; ++l)
+        *reinterpret_cast<uint2*>(base + (uint64_t)l * n + i) = make_uint2(a.v[l], b.v[l]);
+}
+
+// AoS Fr in global/shared memory
+__device__ __forceinline__ fr ld_aos(const fr* p) { return *p; }
+
+// ------------------------------------------------------------------ reductions
+__device__ __forceinline__ fr shfl_down_fr(const fr& x, int off) {
+    fr y;
+#pragma unroll
+    for (int l = 0; l < 8; ++l) y.v[l] = __shfl_down_sync(0xffffffffu, x.v[l], off);
+    return y;
+}
+
+// Sum of NV Fr values over the block; result valid in thread 0.  `scratch` holds
+// NV * (blockDim/32) fr.  Contains __syncthreads (all threads must call).
+template <int NV>
+__device__ __forceinline__ void block_sum_fr(fr (&v)[NV], fr* scratch) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) v[k] = fr_add(v[k], shfl_down_fr(v[k], off));
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) scratch[k * nw + warp] = v[k];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) v[k] = lane < nw ? scratch[k * nw + lane] : fr_zero();
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+            for (int k = 0; k < NV; ++k) v[k] = fr_add(v[k], shfl_down_fr(v[k], off));
+        }
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void atomic_min_i64(unsigned long long* p, uint64_t v) {
+    atomicMin(p, (unsigned long long)v);
+}
+
+// ------------------------------------------------------------------ device-side proof state
+// Scalars of one proof, Montgomery form, in the workspace.
+struct RoundDesc {
+    uint64_t elo_off, ehi_off;   // offsets (in fr) of E_lo / E_hi in the eq arena
+    uint32_t gbits;              // log2 of the group size G (pairs sharing one E_hi entry)
+    uint32_t nblocks;            // blocks that wrote partial rows for this round
+    uint32_t direct_h1;          // 1: H(1) summed directly (round 1 of sumcheck_prove, u_c = 0)
+    uint32_t pad;
+};
+
+struct ProofScalars {
+    fr beta, alpha1, alpha2;
+    fr u[kMaxRounds];
+    fr r[kMaxRounds];
+    fr rank_eq;            // eq(u[0:log2 P], bits(rank)) — this rank's factor of e~(u, .)
+    fr w;                  // N D^{-1}
+};
+
+struct ProofOut {
+    zkl_fr evals[kMaxRounds][4];
+    zkl_fr finals[5];
+    unsigned long long err_index;   // atomicMin target (ULLONG_MAX = none)
+    int status;
+    int pad;
+};
+
+}  // namespace zkl
+
+// ------------------------------------------------------------------ opaque ABI objects
+struct zkl_ctx {
+    int device;
+    cudaStream_t stream;
+    cudaStream_t side;             // table-side work overlapping the D side
+    cudaEvent_t ev_fork, ev_join;
+    int rank, nranks;
+    void* nccl_comm;               // ncclComm_t (loaded at run time) when nranks > 1
+    uint8_t* ws;
+    size_t ws_bytes;
+    void* host_out;                // pinned host copy of ProofOut
+    int poisoned;
+    uint64_t launches;
+    char last_error[512];
+};
+
+struct zkl_table {
+    uint64_t N;
+    uint32_t* T;        // SoA Montgomery copy, N entries
+    uint32_t* slots;    // open-addressing hash: slot -> index+1 (0 = empty)
+    uint32_t slot_mask;
+    int device;
+};

@@ -1,0 +1,313 @@
+// Fr, the BLS12-381 scalar field, on sm_100a.
+//
+// Field: r = 0x73eda753299d7d483339d80809a1d80553bda402fffe5bfeffffffff00000001
+// ("BLS12-381 ... |F| ~ 2^254", §7; value: DESIGN.md reading 1).
+//
+// Representation: 8 x 32-bit little-endian limbs in Montgomery form x*2^256 mod r, kept in
+// [0, r).  In HBM field vectors are stored limb-interleaved (SoA): limb l of element i at
+// limbs[l*n + i], so a warp reads 128 contiguous bytes per limb plane and 4 consecutive
+// elements per thread with one 128-bit load per plane.
+//
+// Multiplication is CIOS Montgomery on the integer multiply-add pipe with PTX carry chains
+// (mad.lo.cc / madc.hi.cc).  r = 1 (mod 2^32), so r' = -r^{-1} = -1 (mod 2^32) and the
+// reduction quotient is q = -t0: no multiply.  Since 4r < 2^256, CIOS on inputs < r
+// returns a value < 2r and one conditional subtraction restores [0, r).
+#pragma once
+#include <stdint.h>
+
+namespace zkl {
+
+struct fr {
+    uint32_t v[8];
+};
+
+// r, little-endian 32-bit limbs
+#define ZKL_R0 0x00000001u
+#define ZKL_R1 0xffffffffu
+#define ZKL_R2 0xfffe5bfeu
+#define ZKL_R3 0x53bda402u
+#define ZKL_R4 0x09a1d805u
+#define ZKL_R5 0x3339d808u
+#define ZKL_R6 0x299d7d48u
+#define ZKL_R7 0x73eda753u
+
+__device__ __forceinline__ fr fr_zero() {
+    fr z;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) z.v[i] = 0;
+    return z;
+}
+
+// 1 in Montgomery form: 2^256 mod r
+__device__ __forceinline__ fr fr_one() {
+    fr o;
+    o.v[0] = 0xfffffffeu; o.v[1] = 0x00000001u; o.v[2] = 0x00034802u; o.v[3] = 0x5884b7fau;
+    o.v[4] = 0xecbc4ff5u; o.v[5] = 0x998c4fefu; o.v[6] = 0xacc5056fu; o.v[7] = 0x1824b159u;
+    return o;
+}
+
+// R^2 mod r = 2^512 mod r (to-Montgomery multiplier)
+__device__ __forceinline__ fr fr_r2() {
+    fr o;
+    o.v[0] = 0xf3f29c6du; o.v[1] = 0xc999e990u; o.v[2] = 0x87925c23u; o.v[3] = 0x2b6cedcbu;
+    o.v[4] = 0x7254398fu; o.v[5] = 0x05d31496u; o.v[6] = 0x9f59ff11u; o.v[7] = 0x0748d9d9u;
+    return o;
+}
+
+__device__ __forceinline__ bool fr_is_zero(const fr& a) {
+    uint32_t x = a.v[0] | a.v[1] | a.v[2] | a.v[3] | a.v[4] | a.v[5] | a.v[6] | a.v[7];
+    return x == 0;
+}
+
+__device__ __forceinline__ bool fr_eq(const fr& a, const fr& b) {
+    uint32_t x = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x |= a.v[i] ^ b.v[i];
+    return x == 0;
+}
+
+// x in [0, 2r) -> [0, r): subtract r, keep the difference if no borrow.
+__device__ __forceinline__ void fr_reduce_once(fr& x) {
+    uint32_t d[8], borrow;
+    asm("sub.cc.u32  %0, %9,  %17;\n\t"
+        "subc.cc.u32 %1, %10, %18;\n\t"
+        "subc.cc.u32 %2, %11, %19;\n\t"
+        "subc.cc.u32 %3, %12, %20;\n\t"
+        "subc.cc.u32 %4, %13, %21;\n\t"
+        "subc.cc.u32 %5, %14, %22;\n\t"
+        "subc.cc.u32 %6, %15, %23;\n\t"
+        "subc.cc.u32 %7, %16, %24;\n\t"
+        "subc.u32    %8, 0, 0;"
+        : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]),
+          "=r"(borrow)
+        : "r"(x.v[0]), "r"(x.v[1]), "r"(x.v[2]), "r"(x.v[3]), "r"(x.v[4]), "r"(x.v[5]), "r"(x.v[6]),
+          "r"(x.v[7]), "n"(ZKL_R0), "n"(ZKL_R1), "n"(ZKL_R2), "n"(ZKL_R3), "n"(ZKL_R4), "n"(ZKL_R5),
+          "n"(ZKL_R6), "n"(ZKL_R7));
+    // borrow == 0xffffffff if x < r (keep x), 0 otherwise (take d)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x.v[i] = borrow ? x.v[i] : d[i];
+}
+
+__device__ __forceinline__ fr fr_add(const fr& a, const fr& b) {
+    fr s;
+    asm("add.cc.u32  %0, %8,  %16;\n\t"
+        "addc.cc.u32 %1, %9,  %17;\n\t"
+        "addc.cc.u32 %2, %10, %18;\n\t"
+        "addc.cc.u32 %3, %11, %19;\n\t"
+        "addc.cc.u32 %4, %12, %20;\n\t"
+        "addc.cc.u32 %5, %13, %21;\n\t"
+        "addc.cc.u32 %6, %14, %22;\n\t"
+        "addc.u32    %7, %15, %23;"
+        : "=r"(s.v[0]), "=r"(s.v[1]), "=r"(s.v[2]), "=r"(s.v[3]), "=r"(s.v[4]), "=r"(s.v[5]), "=r"(s.v[6]),
+          "=r"(s.v[7])
+        : "r"(a.v[0]), "r"(a.v[1]), "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]), "r"(a.v[6]), "r"(a.v[7]),
+          "r"(b.v[0]), "r"(b.v[1]), "r"(b.v[2]), "r"(b.v[3]), "r"(b.v[4]), "r"(b.v[5]), "r"(b.v[6]), "r"(b.v[7]));
+    fr_reduce_once(s);   // a + b < 2r < 2^256
+    return s;
+}
+
+// a - b mod r: compute a - b; on borrow add r.
+__device__ __forceinline__ fr fr_sub(const fr& a, const fr& b) {
+    fr d;
+    uint32_t borrow;
+    asm("sub.cc.u32  %0, %9,  %17;\n\t"
+        "subc.cc.u32 %1, %10, %18;\n\t"
+        "subc.cc.u32 %2, %11, %19;\n\t"
+        "subc.cc.u32 %3, %12, %20;\n\t"
+        "subc.cc.u32 %4, %13, %21;\n\t"
+        "subc.cc.u32 %5, %14, %22;\n\t"
+        "subc.cc.u32 %6, %15, %23;\n\t"
+        "subc.cc.u32 %7, %16, %24;\n\t"
+        "subc.u32    %8, 0, 0;"
+        : "=r"(d.v[0]), "=r"(d.v[1]), "=r"(d.v[2]), "=r"(d.v[3]), "=r"(d.v[4]), "=r"(d.v[5]), "=r"(d.v[6]),
+          "=r"(d.v[7]), "=r"(borrow)
+        : "r"(a.v[0]), "r"(a.v[1]), "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]), "r"(a.v[6]), "r"(a.v[7]),
+          "r"(b.v[0]), "r"(b.v[1]), "r"(b.v[2]), "r"(b.v[3]), "r"(b.v[4]), "r"(b.v[5]), "r"(b.v[6]), "r"(b.v[7]));
+    // add (r & borrow)
+    asm("add.cc.u32  %0, %0, %8;\n\t"
+        "addc.cc.u32 %1, %1, %9;\n\t"
+        "addc.cc.u32 %2, %2, %10;\n\t"
+        "addc.cc.u32 %3, %3, %11;\n\t"
+        "addc.cc.u32 %4, %4, %12;\n\t"
+        "addc.cc.u32 %5, %5, %13;\n\t"
+        "addc.cc.u32 %6, %6, %14;\n\t"
+        "addc.u32    %7, %7, %15;"
+        : "+r"(d.v[0]), "+r"(d.v[1]), "+r"(d.v[2]), "+r"(d.v[3]), "+r"(d.v[4]), "+r"(d.v[5]), "+r"(d.v[6]),
+          "+r"(d.v[7])
+        : "r"(ZKL_R0 & borrow), "r"(ZKL_R1 & borrow), "r"(ZKL_R2 & borrow), "r"(ZKL_R3 & borrow),
+          "r"(ZKL_R4 & borrow), "r"(ZKL_R5 & borrow), "r"(ZKL_R6 & borrow), "r"(ZKL_R7 & borrow));
+    return d;
+}
+
+__device__ __forceinline__ fr fr_neg(const fr& a) { return fr_sub(fr_zero(), a); }
+
+// ---------------------------------------------------------------------------------------
+// Montgomery multiplication, CIOS with aligned register pairs.
+//
+// The running value T (< 2r) is held as X + Y*2^32: X = x0..x8 aligned at word 0, Y = y0..y7
+// aligned at word 1.  Each iteration adds a_even*b_i and q*r_even to X (pairs (x_j, x_j+1), j
+// even) and a_odd*b_i / 2^32 and q*r_odd / 2^32 to Y (pairs (y_j-1, y_j), j odd): every
+// lo/hi product pair lands on an aligned register pair, so ptxas emits one IMAD.WIDE.U32(.X)
+// per pair.  q = -x0 because r' = -1 (mod 2^32); r0 = 1 makes the j = 0 reduction pair an add.
+// The division by 2^32 is a renaming: the next X is Y (with x1 merged into word 0) and the
+// next Y is x2..x8 read as the addends of the next odd-product chain.  The Y chains never
+// carry out: X >= 0 and T + a b_i + q r < 2r * 2^32 bound Y below 2^256 (checked word by word
+// in tools/sim_fr_mul.py).
+// ---------------------------------------------------------------------------------------
+#define ZKL_MADPAIR(dl, dh, a, b, al, ah) \
+    "madc.lo.cc.u32 " dl ", " a ", " b ", " al ";\n\t" "madc.hi.cc.u32 " dh ", " a ", " b ", " ah ";\n\t"
+
+__device__ __forceinline__ fr fr_mul(const fr& a, const fr& b) {
+    uint32_t x0, x1, x2, x3, x4, x5, x6, x7, x8;
+    uint32_t y0, y1, y2, y3, y4, y5, y6, y7;
+    // ---- iteration 0: plain products (T = 0)
+    {
+        const uint32_t bi = b.v[0];
+        asm("mul.lo.u32 %0, %9, %13;\n\t"  "mul.hi.u32 %1, %9, %13;\n\t"
+            "mul.lo.u32 %2, %10, %13;\n\t" "mul.hi.u32 %3, %10, %13;\n\t"
+            "mul.lo.u32 %4, %11, %13;\n\t" "mul.hi.u32 %5, %11, %13;\n\t"
+            "mul.lo.u32 %6, %12, %13;\n\t" "mul.hi.u32 %7, %12, %13;\n\t"
+            "mov.u32 %8, 0;"
+            : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3), "=r"(x4), "=r"(x5), "=r"(x6), "=r"(x7), "=r"(x8)
+            : "r"(a.v[0]), "r"(a.v[2]), "r"(a.v[4]), "r"(a.v[6]), "r"(bi));
+        asm("mul.lo.u32 %0, %8, %12;\n\t"  "mul.hi.u32 %1, %8, %12;\n\t"
+            "mul.lo.u32 %2, %9, %12;\n\t"  "mul.hi.u32 %3, %9, %12;\n\t"
+            "mul.lo.u32 %4, %10, %12;\n\t" "mul.hi.u32 %5, %10, %12;\n\t"
+            "mul.lo.u32 %6, %11, %12;\n\t" "mul.hi.u32 %7, %11, %12;"
+            : "=r"(y0), "=r"(y1), "=r"(y2), "=r"(y3), "=r"(y4), "=r"(y5), "=r"(y6), "=r"(y7)
+            : "r"(a.v[1]), "r"(a.v[3]), "r"(a.v[5]), "r"(a.v[7]), "r"(bi));
+    }
+#define ZKL_REDUCE_STEP()                                                                        \
+    asm("{\n\t.reg .u32 q;\n\t"                                                                  \
+        "sub.u32 q, 0, %0;\n\t"                                                                  \
+        "add.cc.u32 %0, %0, q;\n\t"                                                              \
+        "addc.cc.u32 %1, %1, 0;\n\t"                                                             \
+        ZKL_MADPAIR("%2", "%3", "q", "%18", "%2", "%3")                                          \
+        ZKL_MADPAIR("%4", "%5", "q", "%20", "%4", "%5")                                          \
+        ZKL_MADPAIR("%6", "%7", "q", "%22", "%6", "%7")                                          \
+        "addc.u32 %8, %8, 0;\n\t"                                                                \
+        "mad.lo.cc.u32  %9,  q, %17, %9;\n\t"                                                    \
+        "madc.hi.cc.u32 %10, q, %17, %10;\n\t"                                                   \
+        ZKL_MADPAIR("%11", "%12", "q", "%19", "%11", "%12")                                      \
+        ZKL_MADPAIR("%13", "%14", "q", "%21", "%13", "%14")                                      \
+        "madc.lo.cc.u32 %15, q, %23, %15;\n\t"                                                   \
+        "madc.hi.u32    %16, q, %23, %16;\n\t}"                                                  \
+        : "+r"(x0), "+r"(x1), "+r"(x2), "+r"(x3), "+r"(x4), "+r"(x5), "+r"(x6), "+r"(x7),          \
+          "+r"(x8), "+r"(y0), "+r"(y1), "+r"(y2), "+r"(y3), "+r"(y4), "+r"(y5), "+r"(y6), "+r"(y7) \
+        : "n"(ZKL_R1), "n"(ZKL_R2), "n"(ZKL_R3), "n"(ZKL_R4), "n"(ZKL_R5), "n"(ZKL_R6),           \
+          "n"(ZKL_R7))
+    ZKL_REDUCE_STEP();
+#pragma unroll
+    for (int i = 1; i < 8; ++i) {
+        const uint32_t bi = b.v[i];
+        uint32_t X0, X1, X2, X3, X4, X5, X6, X7, X8, Y0, Y1, Y2, Y3, Y4, Y5, Y6, Y7, M0;
+        // merge x1 into word 0 of the new X (= old Y); odd products into the new Y, whose
+        // addends are x2..x8 (the old X shifted down one word); the carry of the merge enters
+        // the chain at word 1.
+        //   outputs: %0 M0, %1..%8 Y0..Y7
+        //   inputs : %9 y0, %10 x1, %11..%17 x2..x8, %18..%21 a1 a3 a5 a7, %22 bi
+        asm("add.cc.u32 %0, %9, %10;\n\t"
+            ZKL_MADPAIR("%1", "%2", "%18", "%22", "%11", "%12")
+            ZKL_MADPAIR("%3", "%4", "%19", "%22", "%13", "%14")
+            ZKL_MADPAIR("%5", "%6", "%20", "%22", "%15", "%16")
+            "madc.lo.cc.u32 %7, %21, %22, %17;\n\t"
+            "madc.hi.u32    %8, %21, %22, 0;"
+            : "=r"(M0), "=r"(Y0), "=r"(Y1), "=r"(Y2), "=r"(Y3), "=r"(Y4), "=r"(Y5), "=r"(Y6), "=r"(Y7)
+            : "r"(y0), "r"(x1), "r"(x2), "r"(x3), "r"(x4), "r"(x5), "r"(x6), "r"(x7), "r"(x8),
+              "r"(a.v[1]), "r"(a.v[3]), "r"(a.v[5]), "r"(a.v[7]), "r"(bi));
+        // even products into the new X = (M0, y1..y7)
+        //   outputs: %0..%8 X0..X8
+        //   inputs : %9 M0, %10..%16 y1..y7, %17..%20 a0 a2 a4 a6, %21 bi
+        asm("mad.lo.cc.u32  %0, %17, %21, %9;\n\t"
+            "madc.hi.cc.u32 %1, %17, %21, %10;\n\t"
+            ZKL_MADPAIR("%2", "%3", "%18", "%21", "%11", "%12")
+            ZKL_MADPAIR("%4", "%5", "%19", "%21", "%13", "%14")
+            ZKL_MADPAIR("%6", "%7", "%20", "%21", "%15", "%16")
+            "addc.u32 %8, 0, 0;"
+            : "=r"(X0), "=r"(X1), "=r"(X2), "=r"(X3), "=r"(X4), "=r"(X5), "=r"(X6), "=r"(X7), "=r"(X8)
+            : "r"(M0), "r"(y1), "r"(y2), "r"(y3), "r"(y4), "r"(y5), "r"(y6), "r"(y7),
+              "r"(a.v[0]), "r"(a.v[2]), "r"(a.v[4]), "r"(a.v[6]), "r"(bi));
+        x0 = X0; x1 = X1; x2 = X2; x3 = X3; x4 = X4; x5 = X5; x6 = X6; x7 = X7; x8 = X8;
+        y0 = Y0; y1 = Y1; y2 = Y2; y3 = Y3; y4 = Y4; y5 = Y5; y6 = Y6; y7 = Y7;
+        ZKL_REDUCE_STEP();
+    }
+#undef ZKL_REDUCE_STEP
+    // T = (x1..x8) + (y0..y7), both aligned at word 0; T < 2r.
+    fr res;
+    asm("add.cc.u32  %0, %8,  %16;\n\t"
+        "addc.cc.u32 %1, %9,  %17;\n\t"
+        "addc.cc.u32 %2, %10, %18;\n\t"
+        "addc.cc.u32 %3, %11, %19;\n\t"
+        "addc.cc.u32 %4, %12, %20;\n\t"
+        "addc.cc.u32 %5, %13, %21;\n\t"
+        "addc.cc.u32 %6, %14, %22;\n\t"
+        "addc.u32    %7, %15, %23;"
+        : "=r"(res.v[0]), "=r"(res.v[1]), "=r"(res.v[2]), "=r"(res.v[3]), "=r"(res.v[4]), "=r"(res.v[5]),
+          "=r"(res.v[6]), "=r"(res.v[7])
+        : "r"(x1), "r"(x2), "r"(x3), "r"(x4), "r"(x5), "r"(x6), "r"(x7), "r"(x8),
+          "r"(y0), "r"(y1), "r"(y2), "r"(y3), "r"(y4), "r"(y5), "r"(y6), "r"(y7));
+    fr_reduce_once(res);
+    return res;
+}
+
+__device__ __forceinline__ fr fr_sqr(const fr& a) { return fr_mul(a, a); }
+
+__device__ __forceinline__ fr fr_to_mont(const fr& a) { return fr_mul(a, fr_r2()); }
+
+__device__ __forceinline__ fr fr_from_mont(const fr& a) {
+    fr one = fr_zero();
+    one.v[0] = 1;
+    return fr_mul(a, one);
+}
+
+// a^(r-2) = a^{-1} (Fermat), left-to-right with a 4-bit fixed window (252 squarings +
+// at most 63 + 14 multiplications).  a = 0 gives 0.  Montgomery in, Montgomery out.
+static __device__ __noinline__ fr fr_inv(const fr a) {
+    // r - 2, little-endian 32-bit limbs
+    const uint32_t e[8] = {0xffffffffu, 0xfffffffeu, 0xfffe5bfeu, 0x53bda402u,
+                           0x09a1d805u, 0x3339d808u, 0x299d7d48u, 0x73eda753u};
+    fr tab[16];
+    tab[0] = fr_one();
+    tab[1] = a;
+#pragma unroll 1
+    for (int i = 2; i < 16; ++i) tab[i] = fr_mul(tab[i - 1], a);
+    fr acc = fr_one();
+    bool started = false;
+#pragma unroll 1
+    for (int nib = 63; nib >= 0; --nib) {
+        uint32_t w = (e[nib >> 3] >> ((nib & 7) * 4)) & 0xfu;
+        if (started) {
+            acc = fr_sqr(acc);
+            acc = fr_sqr(acc);
+            acc = fr_sqr(acc);
+            acc = fr_sqr(acc);
+        }
+        if (w) {
+            acc = started ? fr_mul(acc, tab[w]) : tab[w];
+            started = true;
+        }
+    }
+    return acc;
+}
+
+// Canonical (non-Montgomery) a >= r ?
+__device__ __forceinline__ bool fr_geq_modulus(const fr& x) {
+    uint32_t borrow;
+    asm("{\n\t.reg .u32 d;\n\t"
+        "sub.cc.u32  d, %1, %9;\n\t"
+        "subc.cc.u32 d, %2, %10;\n\t"
+        "subc.cc.u32 d, %3, %11;\n\t"
+        "subc.cc.u32 d, %4, %12;\n\t"
+        "subc.cc.u32 d, %5, %13;\n\t"
+        "subc.cc.u32 d, %6, %14;\n\t"
+        "subc.cc.u32 d, %7, %15;\n\t"
+        "subc.cc.u32 d, %8, %16;\n\t"
+        "subc.u32    %0, 0, 0;\n\t}"
+        : "=r"(borrow)
+        : "r"(x.v[0]), "r"(x.v[1]), "r"(x.v[2]), "r"(x.v[3]), "r"(x.v[4]), "r"(x.v[5]), "r"(x.v[6]),
+          "r"(x.v[7]), "n"(ZKL_R0), "n"(ZKL_R1), "n"(ZKL_R2), "n"(ZKL_R3), "n"(ZKL_R4), "n"(ZKL_R5),
+          "n"(ZKL_R6), "n"(ZKL_R7));
+    return borrow == 0;
+}
+
+}  // namespace zkl

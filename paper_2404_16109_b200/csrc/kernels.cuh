@@ -1,0 +1,820 @@
+// Device kernels of the tlookup hot path.  Included once, by api.cu.
+#pragma once
+#include <cub/block/block_radix_sort.cuh>
+
+#include "common.cuh"
+
+namespace zkl {
+
+// ====================================================================== a1: boundary encode
+// canonical AoS (8 LE words per element) -> SoA Montgomery.  One Fr mul (x * R^2) per element.
+__global__ void k_import_canon(const uint32_t* __restrict__ src, uint64_t n, uint32_t* __restrict__ dst,
+                               unsigned long long* err) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint4* p = reinterpret_cast<const uint4*>(src + 8 * i);
+        uint4 a = p[0], b = p[1];
+        fr x;
+        x.v[0] = a.x; x.v[1] = a.y; x.v[2] = a.z; x.v[3] = a.w;
+        x.v[4] = b.x; x.v[5] = b.y; x.v[6] = b.z; x.v[7] = b.w;
+        if (fr_geq_modulus(x)) {
+            if (err) atomic_min_i64(err, i);
+            x = fr_zero();
+        }
+        st_fr(dst, n, i, fr_to_mont(x));
+    }
+}
+
+// signed integer -> canonical Fr (x < 0 -> r - |x|)
+__device__ __forceinline__ fr fr_from_i64(int64_t v) {
+    fr x = fr_zero();
+    uint64_t mag = v < 0 ? (uint64_t)0 - (uint64_t)v : (uint64_t)v;
+    x.v[0] = (uint32_t)mag;
+    x.v[1] = (uint32_t)(mag >> 32);
+    return v < 0 ? fr_sub(fr_zero(), x) : x;
+}
+
+__global__ void k_import_i64(const int64_t* __restrict__ src, uint64_t n, uint32_t* __restrict__ dst) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        st_fr(dst, n, i, fr_to_mont(fr_from_i64(src[i])));
+}
+
+// S_i = x_i + alpha_f y_i.  *af = alpha_f in Montgomery form:
+// mont(af, y) = alpha_f * y (canonical), then one to-Montgomery multiplication.
+__global__ void k_import_pair_dev(const int32_t* __restrict__ x, const int32_t* __restrict__ y, uint64_t n,
+                                  const fr* __restrict__ af, uint32_t* __restrict__ dst) {
+    const fr af_m = *af;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        fr s = fr_add(fr_from_i64(x[i]), fr_mul(af_m, fr_from_i64(y[i])));
+        st_fr(dst, n, i, fr_to_mont(s));
+    }
+}
+
+__global__ void k_export(const uint32_t* __restrict__ src, uint64_t n, uint32_t* __restrict__ dst) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        fr x = fr_from_mont(ld_fr(src, n, i));
+        uint4* p = reinterpret_cast<uint4*>(dst + 8 * i);
+        p[0] = make_uint4(x.v[0], x.v[1], x.v[2], x.v[3]);
+        p[1] = make_uint4(x.v[4], x.v[5], x.v[6], x.v[7]);
+    }
+}
+
+// ====================================================================== a2: table handle
+// Open addressing over the Montgomery representation; slot holds index+1 (0 = empty).
+__device__ __forceinline__ uint32_t hash_fr(const fr& x) {
+    uint32_t h = x.v[0] * 0x9E3779B1u;
+    h ^= x.v[1] + 0x7F4A7C15u + (h << 6) + (h >> 2);
+    h ^= x.v[6] * 0x85EBCA6Bu;
+    h ^= x.v[7];
+    h ^= h >> 16;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 13;
+    return h;
+}
+
+struct TableView {
+    const uint32_t* T;
+    const uint32_t* slots;
+    uint64_t N;
+    uint32_t mask;
+};
+
+// index of x in T, or -1
+__device__ __forceinline__ int64_t table_find(const TableView& tv, const fr& x) {
+    uint32_t h = hash_fr(x) & tv.mask;
+    for (;;) {
+        uint32_t s = __ldg(tv.slots + h);
+        if (s == 0) return -1;
+        uint64_t j = s - 1;
+        if (fr_eq(ld_fr(tv.T, tv.N, j), x)) return (int64_t)j;
+        h = (h + 1) & tv.mask;
+    }
+}
+
+__global__ void k_table_copy(const uint32_t* __restrict__ src, uint64_t n, uint32_t* __restrict__ dst) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        st_fr(dst, n, i, ld_fr(src, n, i));
+}
+
+__global__ void k_table_insert(const uint32_t* __restrict__ T, uint64_t N, uint32_t* slots, uint32_t mask) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < N; j += (uint64_t)gridDim.x * blockDim.x) {
+        fr x = ld_fr(T, N, j);
+        uint32_t h = hash_fr(x) & mask;
+        for (;;) {
+            uint32_t old = atomicCAS(slots + h, 0u, (uint32_t)(j + 1));
+            if (old == 0) break;
+            if (fr_eq(ld_fr(T, N, old - 1), x)) {   // equal key: the slot keeps the smallest index
+                atomicMin(slots + h, (uint32_t)(j + 1));
+                break;
+            }
+            h = (h + 1) & mask;
+        }
+    }
+}
+
+// j is a duplicate iff its key's slot holds a smaller index; report the smallest such j.
+__global__ void k_table_dups(const uint32_t* __restrict__ T, uint64_t N, const uint32_t* slots, uint32_t mask,
+                             unsigned long long* err) {
+    TableView tv{T, slots, N, mask};
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < N; j += (uint64_t)gridDim.x * blockDim.x) {
+        int64_t f = table_find(tv, ld_fr(T, N, j));
+        if (f != (int64_t)j) atomic_min_i64(err, j);
+    }
+}
+
+// ====================================================================== a3: multiplicities
+// Atomic-free histogram: per tile of 4096 lookups, index map (hash probe), block radix sort of the
+// indices, then per distinct index one read-modify-write of the CTA-private row:
+// heads subtract their sorted position, tails add theirs + 1 (two barrier-separated phases, each
+// touching one address per distinct key).  A column sum over the rows gives m.
+constexpr int kHistThreads = 512;
+constexpr int kHistItems = 8;
+constexpr int kHistTile = kHistThreads * kHistItems;   // 4096
+
+__global__ void __launch_bounds__(kHistThreads)
+k_hist_rows(const uint32_t* __restrict__ S, uint64_t n, uint64_t global_offset, TableView tv, uint32_t* rows,
+            int key_bits, unsigned long long* err) {
+    typedef cub::BlockRadixSort<uint32_t, kHistThreads, kHistItems> Sort;
+    __shared__ union {
+        typename Sort::TempStorage sort;
+        uint32_t keys[kHistTile];
+    } sm;
+    const uint32_t N = (uint32_t)tv.N;
+    uint32_t* row = rows + (uint64_t)blockIdx.x * N;
+    for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) row[j] = 0;
+    __syncthreads();
+    const uint64_t ntiles = (n + kHistTile - 1) / kHistTile;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t base = tile * kHistTile;
+        uint32_t keys[kHistItems];
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+            const uint64_t i0 = base + 2048 * g + 4 * threadIdx.x;
+            fr x[4];
+            if (i0 + 3 < n && (n & 3) == 0) {
+                ld_fr4(S, n, i0, x);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) x[q] = i0 + q < n ? ld_fr(S, n, i0 + q) : fr_zero();
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                uint32_t key = N;  // sentinel: not counted
+                if (i0 + q < n) {
+                    int64_t f = table_find(tv, x[q]);
+                    if (f < 0) atomic_min_i64(err, global_offset + i0 + q);
+                    else key = (uint32_t)f;
+                }
+                keys[4 * g + q] = key;
+            }
+        }
+        __syncthreads();   // smem union reuse across tiles
+        Sort(sm.sort).Sort(keys, 0, key_bits);
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kHistItems; ++q) sm.keys[threadIdx.x * kHistItems + q] = keys[q];
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kHistItems; ++q) {
+            const int p = threadIdx.x * kHistItems + q;
+            const uint32_t k = sm.keys[p];
+            if (k < N && (p == 0 || sm.keys[p - 1] != k)) row[k] -= (uint32_t)p;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kHistItems; ++q) {
+            const int p = threadIdx.x * kHistItems + q;
+            const uint32_t k = sm.keys[p];
+            if (k < N && (p == kHistTile - 1 || sm.keys[p + 1] != k)) row[k] += (uint32_t)(p + 1);
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_hist_colsum(const uint32_t* __restrict__ rows, int nrows, uint64_t N, uint32_t* __restrict__ m) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < N; j += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t s = 0;
+        for (int b = 0; b < nrows; ++b) s += rows[(uint64_t)b * N + j];
+        m[j] = s;
+    }
+}
+
+// ====================================================================== a4: batched inversion
+// Block product tree over one value per thread (heap layout in smem: leaves at [nt, 2nt)).
+// Given the inverse of the root, returns the inverse of this thread's value.
+// tree, inv: 2*nt fr each.  All threads must call.  Thread 0 supplies root_inv via *root_inv_src
+// (global) or, if root_inv_src == nullptr, computes it by Fermat.
+__device__ void block_tree_up(fr* tree, const fr& v) {
+    const int nt = blockDim.x, t = threadIdx.x;
+    tree[nt + t] = v;
+    __syncthreads();
+    for (int width = nt >> 1; width >= 1; width >>= 1) {
+        if (t < width) tree[width + t] = fr_mul(tree[2 * (width + t)], tree[2 * (width + t) + 1]);
+        __syncthreads();
+    }
+}
+
+// after block_tree_up; inv[1] must be set (and synced) by the caller
+__device__ fr block_tree_down(const fr* tree, fr* inv) {
+    const int nt = blockDim.x, t = threadIdx.x;
+    for (int width = 1; width < nt; width <<= 1) {
+        if (t < width) {
+            const int node = width + t;
+            const fr iv = inv[node];
+            inv[2 * node] = fr_mul(iv, tree[2 * node + 1]);
+            inv[2 * node + 1] = fr_mul(iv, tree[2 * node]);
+        }
+        __syncthreads();
+    }
+    return inv[nt + t];
+}
+
+constexpr int kInvThreads = 256;
+constexpr int kInvPer = 16;                         // elements per thread
+constexpr int kInvTile = kInvThreads * kInvPer;     // 4096 elements
+// thread t's chain: element e = 4g + j (g, j in 0..3) at tile offset 1024 g + 4 t + j
+
+// Forward pass: x = beta + S; per-thread prefix products stored in Abuf (slot of element e >= 1 holds
+// p_{e-1}, slot of e = 0 holds the thread's total); tile total -> totals[tile] (SoA, ntiles).
+__global__ void __launch_bounds__(kInvThreads)
+k_inv_fwd(const uint32_t* __restrict__ S, uint64_t n, const ProofScalars* __restrict__ sc, uint32_t* Abuf,
+          uint32_t* totals, uint64_t ntiles, uint64_t err_offset, unsigned long long* err) {
+    __shared__ fr tree[2 * kInvThreads];
+    const fr beta = sc->beta;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t base = tile * kInvTile;
+        fr p = fr_zero(), g0[4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            const uint64_t i0 = base + 1024 * g + 4 * threadIdx.x;
+            fr x[4], slot[4];
+            ld_fr4(S, n, i0, x);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                x[j] = fr_add(x[j], beta);
+                if (fr_is_zero(x[j])) atomic_min_i64(err, err_offset + i0 + j);
+                slot[j] = p;                        // p_{e-1} (garbage for e = 0, replaced below)
+                p = (g == 0 && j == 0) ? x[j] : fr_mul(p, x[j]);
+            }
+            if (g == 0) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) g0[j] = slot[j];
+            } else {
+                st_fr4(Abuf, n, i0, slot);
+            }
+        }
+        g0[0] = p;   // thread total in the slot of element 0
+        st_fr4(Abuf, n, base + 4 * threadIdx.x, g0);
+        block_tree_up(tree, p);
+        if (threadIdx.x == 0) st_fr(totals, ntiles, tile, tree[1]);
+        __syncthreads();
+    }
+}
+
+// Inverts `count` values (SoA `vals`, stride `count`) into `out`: one block, chains of length
+// ceil(count / blockDim) per thread, one Fermat for the whole batch.
+__global__ void __launch_bounds__(1024)
+k_batch_invert(const uint32_t* __restrict__ vals, uint64_t count, uint32_t* out) {
+    extern __shared__ fr smem_fr[];
+    fr* tree = smem_fr;
+    fr* inv = smem_fr + 2 * blockDim.x;
+    const uint64_t per = (count + blockDim.x - 1) / blockDim.x;
+    const uint64_t lo = threadIdx.x * per, hi = min(lo + per, count);
+    fr p = fr_one();
+    for (uint64_t i = lo; i < hi; ++i) {
+        st_fr(out, count, i, p);                    // exclusive prefix
+        p = fr_mul(p, ld_fr(vals, count, i));
+    }
+    block_tree_up(tree, p);
+    if (threadIdx.x == 0) inv[1] = fr_inv(tree[1]);
+    __syncthreads();
+    fr iv = block_tree_down(tree, inv);
+    for (uint64_t i = hi; i-- > lo;) {
+        st_fr(out, count, i, fr_mul(ld_fr(out, count, i), iv));
+        iv = fr_mul(iv, ld_fr(vals, count, i));
+    }
+}
+
+// Backward pass: A = 1/(beta + S) over the tile, fused with the round-1 evaluation (a5):
+//   Hinf += W[y] (A_1 - A_0)(S_1 - S_0),  a0 += A_0,  a1 += A_1   per pair y = (2y, 2y+1).
+// H0 = H1 = sum_y W[y] A_t (S_t + beta) = sum W = 1 globally (A (S + beta) = 1), no work.
+// W[y] = E_hi[tile] * E_lo[y mod 2048] (a tile is one group of 2048 pairs).
+__global__ void __launch_bounds__(kInvThreads)
+k_inv_bwd(const uint32_t* __restrict__ S, uint64_t n, const ProofScalars* __restrict__ sc, uint32_t* Abuf,
+          const uint32_t* __restrict__ totals_inv, uint64_t ntiles, const fr* __restrict__ elo,
+          const fr* __restrict__ ehi, int eval, fr* partials) {
+    __shared__ fr tree[2 * kInvThreads];
+    __shared__ fr inv[2 * kInvThreads];
+    const fr beta = sc->beta;
+    fr hinf = fr_zero(), a0 = fr_zero(), a1 = fr_zero();
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t base = tile * kInvTile;
+        fr g0[4];
+        ld_fr4(Abuf, n, base + 4 * threadIdx.x, g0);
+        block_tree_up(tree, g0[0]);
+        if (threadIdx.x == 0) inv[1] = ld_fr(totals_inv, ntiles, tile);
+        __syncthreads();
+        fr iv = block_tree_down(tree, inv);
+        fr acc = fr_zero();
+#pragma unroll
+        for (int g = 3; g >= 0; --g) {
+            const uint64_t i0 = base + 1024 * g + 4 * threadIdx.x;
+            fr slot[4], x[4], A[4];
+            if (g == 0) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) slot[j] = g0[j];
+            } else {
+                ld_fr4(Abuf, n, i0, slot);
+            }
+            ld_fr4(S, n, i0, x);
+#pragma unroll
+            for (int j = 3; j >= 0; --j) {
+                if (g == 0 && j == 0) {
+                    A[0] = iv;
+                } else {
+                    A[j] = fr_mul(iv, slot[j]);
+                    iv = fr_mul(iv, fr_add(x[j], beta));
+                }
+            }
+            st_fr4(Abuf, n, i0, A);
+            if (eval) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const fr dA = fr_sub(A[2 * h + 1], A[2 * h]);
+                    const fr dS = fr_sub(x[2 * h + 1], x[2 * h]);
+                    const uint32_t ylo = 512 * g + 2 * threadIdx.x + h;
+                    acc = fr_add(acc, fr_mul(elo[ylo], fr_mul(dA, dS)));
+                    a0 = fr_add(a0, A[2 * h]);
+                    a1 = fr_add(a1, A[2 * h + 1]);
+                }
+            }
+        }
+        if (eval) hinf = fr_add(hinf, fr_mul(ehi[tile], acc));
+        __syncthreads();
+    }
+    if (eval) {
+        __shared__ fr scratch[3 * (kInvThreads / 32)];
+        fr v[3] = {hinf, a0, a1};
+        block_sum_fr<3>(v, scratch);
+        if (threadIdx.x == 0) {
+            partials[SLOT_HINF * kMaxBlocks + blockIdx.x] = v[0];
+            partials[SLOT_A0 * kMaxBlocks + blockIdx.x] = v[1];
+            partials[SLOT_A1 * kMaxBlocks + blockIdx.x] = v[2];
+        }
+    }
+}
+
+// ====================================================================== a6/a7: sumcheck rounds
+// Round k >= 2 fused with the fold of round k-1 (FOLD = true), or round 1 on given vectors
+// (FOLD = false, sumcheck_prove).  Pairs y of the round are split y = (y_hi, y_lo), y_lo the low
+// gbits bits; W[y] = E_hi[y_hi] E_lo[y_lo]; a block processes whole groups of G = 2^gbits pairs,
+// each thread G/256 of them, accumulating E_lo-weighted sums that are scaled by E_hi once per group.
+constexpr int kRoundThreads = 256;
+
+template <bool FOLD>
+__global__ void __launch_bounds__(kRoundThreads)
+k_round(const uint32_t* __restrict__ Aold, const uint32_t* __restrict__ Sold, uint64_t nold,
+        uint32_t* __restrict__ Anew, uint32_t* __restrict__ Snew, const ProofScalars* __restrict__ sc, int k,
+        const fr* __restrict__ elo, const fr* __restrict__ ehi, int gbits, int direct_h1, fr* partials) {
+    const fr beta = sc->beta;
+    const fr rk = FOLD ? sc->r[k - 2] : fr_zero();
+    const uint64_t npairs = FOLD ? nold / 4 : nold / 2;   // pairs of the round being evaluated
+    const uint64_t nnew = nold / 2;
+    const uint32_t G = 1u << gbits;
+    const uint64_t ngroups = npairs >> gbits;
+    fr H0 = fr_zero(), H1 = fr_zero(), Hinf = fr_zero(), a0 = fr_zero(), a1 = fr_zero();
+    for (uint64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+        fr c0 = fr_zero(), c1 = fr_zero(), cinf = fr_zero();
+        for (uint32_t yl = threadIdx.x; yl < G; yl += blockDim.x) {
+            const uint64_t y = (grp << gbits) + yl;
+            fr A0, A1, S0, S1;
+            if (FOLD) {
+                fr a[4], s[4];
+                ld_fr4(Aold, nold, 4 * y, a);
+                ld_fr4(Sold, nold, 4 * y, s);
+                A0 = fr_add(a[0], fr_mul(rk, fr_sub(a[1], a[0])));
+                A1 = fr_add(a[2], fr_mul(rk, fr_sub(a[3], a[2])));
+                S0 = fr_add(s[0], fr_mul(rk, fr_sub(s[1], s[0])));
+                S1 = fr_add(s[2], fr_mul(rk, fr_sub(s[3], s[2])));
+                st_fr2(Anew, nnew, 2 * y, A0, A1);
+                st_fr2(Snew, nnew, 2 * y, S0, S1);
+            } else {
+                fr a[2], s[2];
+                ld_fr2(Aold, nold, 2 * y, a);
+                ld_fr2(Sold, nold, 2 * y, s);
+                A0 = a[0]; A1 = a[1]; S0 = s[0]; S1 = s[1];
+            }
+            const fr e = elo[yl];
+            c0 = fr_add(c0, fr_mul(e, fr_mul(A0, fr_add(S0, beta))));
+            cinf = fr_add(cinf, fr_mul(e, fr_mul(fr_sub(A1, A0), fr_sub(S1, S0))));
+            if (direct_h1) c1 = fr_add(c1, fr_mul(e, fr_mul(A1, fr_add(S1, beta))));
+            a0 = fr_add(a0, A0);
+            a1 = fr_add(a1, A1);
+        }
+        const fr eh = ehi[grp];
+        H0 = fr_add(H0, fr_mul(eh, c0));
+        Hinf = fr_add(Hinf, fr_mul(eh, cinf));
+        if (direct_h1) H1 = fr_add(H1, fr_mul(eh, c1));
+    }
+    __shared__ fr scratch[5 * (kRoundThreads / 32)];
+    fr v[5] = {H0, H1, Hinf, a0, a1};
+    block_sum_fr<5>(v, scratch);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int s = 0; s < 5; ++s) partials[s * kMaxBlocks + blockIdx.x] = v[s];
+    }
+}
+
+// ====================================================================== a9: tail rounds (one CTA)
+// Rounds k0..kend on <= kTailMax elements held in shared memory.  Input: either the round-(k0-1)
+// vectors (2n elements, folded with r_{k0-1} on load), or the round-k0 vectors (n elements).
+// mode_invert: S only is given; A = 1/(beta + S) is computed here (block batch inversion) and
+// written to Aout (the whole prove for D_local < 4096).  All partial sums are direct (H0, H1, Hinf).
+// After round kend the vectors are folded with r_kend; A(v), S(v) go to fin[0], fin[1].
+constexpr int kTailThreads = 512;
+
+__global__ void __launch_bounds__(kTailThreads)
+k_tail(const uint32_t* __restrict__ Ain, const uint32_t* __restrict__ Sin, uint64_t nin, int fold_in,
+       int mode_invert, uint32_t* Aout, uint64_t err_offset, unsigned long long* err,
+       const ProofScalars* __restrict__ sc, int k0, int kend, const RoundDesc* __restrict__ rounds,
+       const fr* __restrict__ arena, fr* partials_base, fr* fin) {
+    extern __shared__ fr smem_fr[];
+    const int nt = blockDim.x, t = threadIdx.x;
+    const uint64_t n = fold_in ? nin / 2 : nin;
+    fr* As = smem_fr;              // n
+    fr* Ss = smem_fr + kTailMax;   // n
+    fr* tree = smem_fr + 2 * kTailMax;        // 2 nt
+    fr* inv = tree + 2 * nt;                  // 2 nt
+    fr* scratch = inv + 2 * nt;               // 5 * nt/32
+    const fr beta = sc->beta;
+    if (fold_in) {
+        const fr r = sc->r[k0 - 2];
+        for (uint64_t i = t; i < n; i += nt) {
+            fr a0 = ld_fr(Ain, nin, 2 * i), a1 = ld_fr(Ain, nin, 2 * i + 1);
+            fr s0 = ld_fr(Sin, nin, 2 * i), s1 = ld_fr(Sin, nin, 2 * i + 1);
+            As[i] = fr_add(a0, fr_mul(r, fr_sub(a1, a0)));
+            Ss[i] = fr_add(s0, fr_mul(r, fr_sub(s1, s0)));
+        }
+    } else {
+        for (uint64_t i = t; i < n; i += nt) {
+            Ss[i] = ld_fr(Sin, nin, i);
+            if (!mode_invert) As[i] = ld_fr(Ain, nin, i);
+        }
+    }
+    __syncthreads();
+    if (mode_invert) {
+        // chain of ceil(n / nt) consecutive elements per thread
+        const uint64_t per = (n + nt - 1) / nt, lo = t * per, hi = min(lo + per, n);
+        fr p = fr_one();
+        for (uint64_t i = lo; i < hi; ++i) {
+            fr x = fr_add(Ss[i], beta);
+            if (fr_is_zero(x)) atomic_min_i64(err, err_offset + i);
+            As[i] = p;
+            p = fr_mul(p, x);
+        }
+        block_tree_up(tree, p);
+        if (t == 0) inv[1] = fr_inv(tree[1]);
+        __syncthreads();
+        fr iv = block_tree_down(tree, inv);
+        for (uint64_t i = hi; i-- > lo;) {
+            fr x = fr_add(Ss[i], beta);
+            As[i] = fr_mul(As[i], iv);
+            iv = fr_mul(iv, x);
+        }
+        __syncthreads();
+        for (uint64_t i = t; i < n; i += nt) st_fr(Aout, n, i, As[i]);
+    }
+    uint64_t len = n;
+    for (int k = k0; k <= kend; ++k) {
+        const RoundDesc rd = rounds[k - 1];
+        const fr* elo = arena + rd.elo_off;
+        const fr eh = arena[rd.ehi_off];
+        fr v[5] = {fr_zero(), fr_zero(), fr_zero(), fr_zero(), fr_zero()};
+        for (uint64_t y = t; y < len / 2; y += nt) {
+            const fr A0 = As[2 * y], A1 = As[2 * y + 1], S0 = Ss[2 * y], S1 = Ss[2 * y + 1];
+            const fr e = fr_mul(eh, elo[y]);
+            v[0] = fr_add(v[0], fr_mul(e, fr_mul(A0, fr_add(S0, beta))));
+            v[1] = fr_add(v[1], fr_mul(e, fr_mul(A1, fr_add(S1, beta))));
+            v[2] = fr_add(v[2], fr_mul(e, fr_mul(fr_sub(A1, A0), fr_sub(S1, S0))));
+            v[3] = fr_add(v[3], A0);
+            v[4] = fr_add(v[4], A1);
+        }
+        block_sum_fr<5>(v, scratch);
+        if (t == 0) {
+            fr* part = partials_base + (uint64_t)(k - 1) * kSlots * kMaxBlocks;
+#pragma unroll
+            for (int s = 0; s < 5; ++s) part[s * kMaxBlocks] = v[s];
+        }
+        // fold with r_k
+        const fr r = sc->r[k - 1];
+        fr na[4], ns[4];
+        int cnt = 0;
+        for (uint64_t y = t; y < len / 2; y += nt, ++cnt) {
+            na[cnt] = fr_add(As[2 * y], fr_mul(r, fr_sub(As[2 * y + 1], As[2 * y])));
+            ns[cnt] = fr_add(Ss[2 * y], fr_mul(r, fr_sub(Ss[2 * y + 1], Ss[2 * y])));
+        }
+        __syncthreads();
+        cnt = 0;
+        for (uint64_t y = t; y < len / 2; y += nt, ++cnt) {
+            As[y] = na[cnt];
+            Ss[y] = ns[cnt];
+        }
+        __syncthreads();
+        len /= 2;
+    }
+    if (t == 0) {
+        fin[0] = As[0];
+        fin[1] = Ss[0];
+    }
+}
+
+// ====================================================================== a8: table side
+// B = 1/(beta + T) (or m/(beta+T), LOGUP) is produced by the inversion kernels; here:
+// Mf = m as field elements, E2 = e~(u[d-n:], .), and the rounds k <= n evaluated directly at
+// t = 0..3 (16 Fr muls per pair), folded with r_k.
+__global__ void k_tab_init(const uint32_t* __restrict__ m, uint64_t N, uint32_t* Mf, uint32_t* B,
+                           const ProofScalars* __restrict__ sc, int d, int nbits, int variant,
+                           uint32_t* E2) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < N; j += (uint64_t)gridDim.x * blockDim.x) {
+        if (m) {   // prove mode: m (u32) -> Fr; LOGUP: B <- m B
+            fr mv = fr_zero();
+            mv.v[0] = m[j];
+            mv = fr_to_mont(mv);
+            st_fr(Mf, N, j, mv);
+            if (variant == ZKL_VARIANT_LOGUP) st_fr(B, N, j, fr_mul(ld_fr(B, N, j), mv));
+        }
+        fr e = fr_one();
+        for (int b = 0; b < nbits; ++b) {
+            const fr u = sc->u[d - nbits + b];
+            const bool bit = (j >> (nbits - 1 - b)) & 1;
+            e = fr_mul(e, bit ? u : fr_sub(fr_one(), u));
+        }
+        st_fr(E2, N, j, e);
+    }
+}
+
+__device__ __forceinline__ fr tab_term(const fr& b, const fr& t, const fr& m, const fr& e, const fr& beta,
+                                       const fr& alpha2, int variant) {
+    // PAPER: B (alpha2 e2 (T + beta) - m);  LOGUP: -B + alpha2 e2 (B (T + beta) - m)
+    if (variant == ZKL_VARIANT_PAPER) return fr_mul(b, fr_sub(fr_mul(fr_mul(alpha2, e), fr_add(t, beta)), m));
+    return fr_sub(fr_mul(fr_mul(alpha2, e), fr_sub(fr_mul(b, fr_add(t, beta)), m)), b);
+}
+
+__global__ void __launch_bounds__(256)
+k_tab_round(const uint32_t* __restrict__ Bo, const uint32_t* __restrict__ To, const uint32_t* __restrict__ Mo,
+            const uint32_t* __restrict__ Eo, uint64_t nold, uint32_t* Bn, uint32_t* Tn, uint32_t* Mn,
+            uint32_t* En, const ProofScalars* __restrict__ sc, int k, int variant, fr* partials, fr* fin) {
+    const fr beta = sc->beta, alpha2 = sc->alpha2, r = sc->r[k - 1];
+    const uint64_t np = nold / 2;
+    fr g[4] = {fr_zero(), fr_zero(), fr_zero(), fr_zero()};
+    for (uint64_t y = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; y < np; y += (uint64_t)gridDim.x * blockDim.x) {
+        fr b0 = ld_fr(Bo, nold, 2 * y), b1 = ld_fr(Bo, nold, 2 * y + 1);
+        fr t0 = ld_fr(To, nold, 2 * y), t1 = ld_fr(To, nold, 2 * y + 1);
+        fr m0 = ld_fr(Mo, nold, 2 * y), m1 = ld_fr(Mo, nold, 2 * y + 1);
+        fr e0 = ld_fr(Eo, nold, 2 * y), e1 = ld_fr(Eo, nold, 2 * y + 1);
+        const fr db = fr_sub(b1, b0), dt = fr_sub(t1, t0), dm = fr_sub(m1, m0), de = fr_sub(e1, e0);
+        fr bt = b0, tt = t0, mt = m0, et = e0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (q > 0) { bt = fr_add(bt, db); tt = fr_add(tt, dt); mt = fr_add(mt, dm); et = fr_add(et, de); }
+            g[q] = fr_add(g[q], tab_term(bt, tt, mt, et, beta, alpha2, variant));
+        }
+        const fr nb = fr_add(b0, fr_mul(r, db)), ntt = fr_add(t0, fr_mul(r, dt));
+        const fr nm = fr_add(m0, fr_mul(r, dm)), ne = fr_add(e0, fr_mul(r, de));
+        st_fr(Bn, np, y, nb); st_fr(Tn, np, y, ntt); st_fr(Mn, np, y, nm); st_fr(En, np, y, ne);
+        if (np == 1) { fin[0] = nb; fin[1] = ntt; fin[2] = nm; fin[3] = ne; }
+    }
+    __shared__ fr scratch[4 * 8];
+    block_sum_fr<4>(g, scratch);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) partials[q * kMaxBlocks + blockIdx.x] = g[q];
+    }
+}
+
+// ====================================================================== setup / derivation
+// eq tables for every round: job list (offset, ncoords, first coordinate, times rank_eq)
+struct EqJob {
+    uint64_t off;
+    uint32_t nbits;
+    uint32_t c0;
+    uint32_t scale;
+    uint32_t pad;
+};
+
+__global__ void k_eq_fill(const EqJob* __restrict__ jobs, int njobs, uint64_t total, const ProofScalars* __restrict__ sc,
+                          fr* arena) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+        int jb = 0;
+        while (jb + 1 < njobs && jobs[jb + 1].off <= i) ++jb;
+        const EqJob J = jobs[jb];
+        const uint64_t y = i - J.off;
+        fr e = J.scale ? sc->rank_eq : fr_one();
+        for (uint32_t b = 0; b < J.nbits; ++b) {
+            const fr u = sc->u[J.c0 + b];
+            const bool bit = (y >> (J.nbits - 1 - b)) & 1;
+            e = fr_mul(e, bit ? u : fr_sub(fr_one(), u));
+        }
+        arena[i] = e;
+    }
+}
+
+// Canonical challenges -> Montgomery scalars; rank factor eq(u[0:p], rank); w = N / D.
+__global__ void k_setup(const zkl_fr* __restrict__ host_chal, int d, int pbits, int rank, uint64_t N, uint64_t D,
+                        ProofScalars* sc) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    auto conv = [](const zkl_fr& z) {
+        fr x;
+        for (int l = 0; l < 8; ++l) x.v[l] = z.w[l];
+        return fr_to_mont(x);
+    };
+    sc->beta = conv(host_chal[0]);
+    sc->alpha1 = conv(host_chal[1]);
+    sc->alpha2 = conv(host_chal[2]);
+    for (int c = 0; c < d; ++c) sc->u[c] = conv(host_chal[3 + c]);
+    for (int k = 0; k < d; ++k) sc->r[k] = conv(host_chal[3 + d + k]);
+    fr re = fr_one();
+    for (int b = 0; b < pbits; ++b) {
+        const bool bit = (rank >> (pbits - 1 - b)) & 1;
+        re = fr_mul(re, bit ? sc->u[b] : fr_sub(fr_one(), sc->u[b]));
+    }
+    sc->rank_eq = re;
+    (void)N; (void)D;
+}
+
+// Sum of each round's per-block partial rows -> rank_sums[k][slot] (this rank's contribution).
+__global__ void k_reduce_rounds(const fr* __restrict__ partials, const RoundDesc* __restrict__ rounds, int nrounds,
+                                fr* rank_sums) {
+    __shared__ fr scratch[5 * 8];
+    const int k = blockIdx.x;   // 0-based round
+    if (k >= nrounds) return;
+    const uint32_t nb = rounds[k].nblocks;
+    fr v[5];
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+        v[s] = fr_zero();
+        for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x)
+            v[s] = fr_add(v[s], partials[((uint64_t)k * kSlots + s) * kMaxBlocks + b]);
+    }
+    block_sum_fr<5>(v, scratch);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int s = 0; s < 5; ++s) rank_sums[k * kSlots + s] = v[s];
+    }
+}
+
+__global__ void k_reduce_tab(const fr* __restrict__ tpart, const uint32_t* __restrict__ tnb, int nrounds, fr* tab_sums) {
+    __shared__ fr scratch[4 * 8];
+    const int k = blockIdx.x;
+    if (k >= nrounds) return;
+    const uint32_t nb = tnb[k];
+    fr v[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        v[s] = fr_zero();
+        for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x)
+            v[s] = fr_add(v[s], tpart[((uint64_t)k * 4 + s) * kMaxBlocks + b]);
+    }
+    block_sum_fr<4>(v, scratch);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int s = 0; s < 4; ++s) tab_sums[k * 4 + s] = v[s];
+    }
+}
+
+__device__ __forceinline__ fr fr_small(uint32_t v) {
+    fr x = fr_zero();
+    x.v[0] = v;
+    return fr_to_mont(x);
+}
+
+__device__ __forceinline__ zkl_fr to_canon(const fr& m) {
+    fr c = fr_from_mont(m);
+    zkl_fr z;
+    for (int l = 0; l < 8; ++l) z.w[l] = c.v[l];
+    return z;
+}
+
+// Round derivation (a7): g_k(t) = alpha1 C_k l_c(t) H(t) + a(t) + tab_k(t), c = d - k,
+// C_k = prod_{j<k} l_{d-j}(r_j);  H(1) derived from g_k(0) + g_k(1) = g_{k-1}(r_{k-1}) when the
+// round did not sum it directly;  H(2) = -H0 + 2 H1 + 2 Hinf, H(3) = -2 H0 + 3 H1 + 6 Hinf.
+// ranks: D-side sums of local rounds are summed over `nranks` rows of `gathered`; rounds > dl use
+// `repl_sums` (replicated, already global).  fin_loc: A(v), S(v); tfin: B, T, M, E2 at v'.
+__global__ void k_derive(const fr* __restrict__ gathered, int nranks, int dl, const fr* __restrict__ repl_sums,
+                         const RoundDesc* __restrict__ rounds, const fr* __restrict__ tab_sums,
+                         const ProofScalars* __restrict__ sc, int d, int n, int variant, int prove_mode,
+                         const fr* __restrict__ fin_loc, const fr* __restrict__ tfin, ProofOut* out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const fr one = fr_one(), two = fr_small(2), three = fr_small(3), five = fr_small(5), six = fr_small(6);
+    // ---- the divisors: 2, 6 and coef_k * u_c (k where H(1) is derived); one Fermat for all
+    fr C[kMaxRounds + 1], dv[kMaxRounds + 2], pre[kMaxRounds + 2];
+    C[0] = one;
+    for (int k = 1; k <= d; ++k) {
+        const fr u = sc->u[d - k];
+        const fr l0 = fr_sub(one, u);
+        C[k] = fr_mul(C[k - 1], fr_add(l0, fr_mul(sc->r[k - 1], fr_sub(u, l0))));   // C_{k+1} at C[k]
+    }
+    dv[0] = two;
+    dv[1] = six;
+    for (int k = 1; k <= d; ++k) {
+        const fr q = fr_mul(fr_mul(sc->alpha1, C[k - 1]), sc->u[d - k]);
+        dv[k + 1] = fr_is_zero(q) ? one : q;
+    }
+    const int nd = d + 2;
+    fr acc = one;
+    for (int i = 0; i < nd; ++i) { pre[i] = acc; acc = fr_mul(acc, dv[i]); }
+    fr iv = fr_inv(acc);
+    for (int i = nd - 1; i >= 0; --i) { const fr t = fr_mul(iv, pre[i]); iv = fr_mul(iv, dv[i]); dv[i] = t; }
+    const fr inv2 = dv[0], inv6 = dv[1];
+    // ---- table constant tau once all table coordinates are bound
+    const fr tb = tfin[0], tt = tfin[1], tm = tfin[2], te = tfin[3];
+    fr tau = (variant == ZKL_VARIANT_PAPER)
+                 ? fr_mul(tb, fr_sub(fr_mul(fr_mul(sc->alpha2, te), fr_add(tt, sc->beta)), tm))
+                 : fr_sub(fr_mul(fr_mul(sc->alpha2, te), fr_sub(fr_mul(tb, fr_add(tt, sc->beta)), tm)), tb);
+    fr claim = (variant == ZKL_VARIANT_PAPER) ? fr_add(sc->alpha1, sc->alpha2) : sc->alpha1;
+    fr tscale = one;
+    for (int k = 1; k <= d; ++k) {
+        fr s[5];
+        for (int q = 0; q < 5; ++q) {
+            s[q] = fr_zero();
+            if (k <= dl) {
+                for (int p = 0; p < nranks; ++p)
+                    s[q] = fr_add(s[q], gathered[((uint64_t)p * dl + (k - 1)) * kSlots + q]);
+            } else {
+                s[q] = repl_sums[(k - dl - 1) * kSlots + q];
+            }
+        }
+        fr tab[4];
+        if (k <= n) {
+            for (int q = 0; q < 4; ++q) tab[q] = tab_sums[(k - 1) * 4 + q];
+        } else {
+            tscale = fr_mul(tscale, inv2);
+            const fr c = fr_mul(tau, tscale);
+            for (int q = 0; q < 4; ++q) tab[q] = c;
+        }
+        const fr u = sc->u[d - k];
+        const fr l0 = fr_sub(one, u), l1 = u;
+        const fr l2 = fr_sub(fr_mul(three, u), one);
+        const fr l3 = fr_sub(fr_mul(five, u), two);
+        const fr coef = fr_mul(sc->alpha1, C[k - 1]);
+        fr H0 = s[SLOT_H0], H1 = s[SLOT_H1];
+        const fr Hinf = s[SLOT_HINF], a0 = s[SLOT_A0], a1 = s[SLOT_A1];
+        if (k == 1 && prove_mode) { H0 = one; H1 = one; }
+        const fr g0 = fr_add(fr_add(fr_mul(fr_mul(coef, l0), H0), a0), tab[0]);
+        fr g1;
+        const bool direct = (k == 1) || rounds[k - 1].direct_h1 || fr_is_zero(fr_mul(coef, l1));
+        if (direct) {
+            g1 = fr_add(fr_add(fr_mul(fr_mul(coef, l1), H1), a1), tab[1]);
+        } else {
+            g1 = fr_sub(claim, g0);
+            H1 = fr_mul(fr_sub(fr_sub(g1, a1), tab[1]), dv[k + 1]);   // / (coef u_c)
+        }
+        const fr H2 = fr_add(fr_sub(fr_add(H1, H1), H0), fr_add(Hinf, Hinf));
+        const fr H3 = fr_add(fr_sub(fr_mul(three, H1), fr_add(H0, H0)), fr_mul(six, Hinf));
+        const fr da = fr_sub(a1, a0);
+        const fr g2 = fr_add(fr_add(fr_mul(fr_mul(coef, l2), H2), fr_add(a0, fr_add(da, da))), tab[2]);
+        const fr g3 = fr_add(fr_add(fr_mul(fr_mul(coef, l3), H3), fr_add(a0, fr_mul(three, da))), tab[3]);
+        out->evals[k - 1][0] = to_canon(g0);
+        out->evals[k - 1][1] = to_canon(g1);
+        out->evals[k - 1][2] = to_canon(g2);
+        out->evals[k - 1][3] = to_canon(g3);
+        // claim_k = g_k(r_k), Lagrange on {0,1,2,3}:
+        //  L0 = -(x-1)(x-2)(x-3)/6, L1 = x(x-2)(x-3)/2, L2 = -x(x-1)(x-3)/2, L3 = x(x-1)(x-2)/6
+        const fr x = sc->r[k - 1];
+        const fr xm1 = fr_sub(x, one), xm2 = fr_sub(x, two), xm3 = fr_sub(x, three);
+        const fr L0 = fr_neg(fr_mul(fr_mul(fr_mul(xm1, xm2), xm3), inv6));
+        const fr L1 = fr_mul(fr_mul(fr_mul(x, xm2), xm3), inv2);
+        const fr L2 = fr_neg(fr_mul(fr_mul(fr_mul(x, xm1), xm3), inv2));
+        const fr L3 = fr_mul(fr_mul(fr_mul(x, xm1), xm2), inv6);
+        claim = fr_add(fr_add(fr_mul(g0, L0), fr_mul(g1, L1)), fr_add(fr_mul(g2, L2), fr_mul(g3, L3)));
+    }
+    out->finals[0] = to_canon(fin_loc[0]);
+    out->finals[1] = to_canon(fin_loc[1]);
+    out->finals[2] = to_canon(tb);
+    out->finals[3] = to_canon(tt);
+    out->finals[4] = to_canon(tm);
+}
+
+// beta + T_j (zero check: DIV_ZERO_T) -> x (SoA), for the table-side batch inversion
+__global__ void k_add_beta(const uint32_t* __restrict__ T, uint64_t N, const ProofScalars* __restrict__ sc,
+                           uint32_t* x, unsigned long long* err) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < N; j += (uint64_t)gridDim.x * blockDim.x) {
+        const fr v = fr_add(ld_fr(T, N, j), sc->beta);
+        if (fr_is_zero(v)) atomic_min_i64(err, j);
+        st_fr(x, N, j, v);
+    }
+}
+
+// N = 1: the table vectors are already fully bound
+__global__ void k_tab_fin0(const uint32_t* B, const uint32_t* T, const uint32_t* M, const uint32_t* E, fr* fin) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        fin[0] = ld_fr(B, 1, 0); fin[1] = ld_fr(T, 1, 0); fin[2] = ld_fr(M, 1, 0); fin[3] = ld_fr(E, 1, 0);
+    }
+}
+
+// copy SoA vector (same n)
+__global__ void k_copy_vec(const uint32_t* __restrict__ src, uint64_t n, uint32_t* __restrict__ dst) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < 8 * n; i += (uint64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+}  // namespace zkl

@@ -1,0 +1,338 @@
+"""Thin Python binding of the zkl C ABI (include/zkl.h) — argument marshalling only.
+
+Every step of the tlookup path runs in libzkl.so (hand-written sm_100a CUDA).  PyTorch provides the
+device memory (field vectors, the workspace, table memory) and the CUDA stream.  There is no CPU
+fallback: if libzkl.so is missing or no GPU is present, calls fail loudly.
+
+C names are exposed unchanged (`zkl_tlookup_prepare`, ...); `Context` bundles the common calls.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libzkl.so")
+R_MODULUS = 0x73EDA753299D7D483339D80809A1D80553BDA402FFFE5BFEFFFFFFFF00000001
+
+STATUS = ["ZKL_OK", "ZKL_E_ARG", "ZKL_E_SHAPE", "ZKL_E_NONCANONICAL", "ZKL_E_DUP_TABLE", "ZKL_E_NOT_IN_TABLE",
+          "ZKL_E_DIV_ZERO_T", "ZKL_E_DIV_ZERO_S", "ZKL_E_CUDA", "ZKL_E_NCCL", "ZKL_E_OOM", "ZKL_E_STATE"]
+PAPER, LOGUP = 0, 1
+
+
+class zkl_fr(ctypes.Structure):
+    _fields_ = [("w", ctypes.c_uint32 * 8)]
+
+
+class zkl_vec(ctypes.Structure):
+    _fields_ = [("limbs", ctypes.c_void_p), ("n", ctypes.c_uint64)]
+
+
+class zkl_challenges(ctypes.Structure):
+    _fields_ = [("beta", zkl_fr), ("alpha1", zkl_fr), ("alpha2", zkl_fr),
+                ("u", ctypes.POINTER(zkl_fr)), ("r", ctypes.POINTER(zkl_fr))]
+
+
+class zkl_final_evals(ctypes.Structure):
+    _fields_ = [("A", zkl_fr), ("S", zkl_fr), ("B", zkl_fr), ("T", zkl_fr), ("m", zkl_fr)]
+
+
+class ZklError(RuntimeError):
+    def __init__(self, status: int, index: int = -1, msg: str = ""):
+        name = STATUS[status] if 0 <= status < len(STATUS) else str(status)
+        super().__init__(f"{name}({index}): {msg}")
+        self.status, self.name, self.index = status, name, index
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libzkl.so (built in-tree by paper_2404_16109_b200.build / __graft_entry__.build)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2404_16109_b200.build` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        P, U64, I32, I64P = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)
+        sig = {
+            "zkl_strerror": ([I32], ctypes.c_char_p),
+            "zkl_ctx_create": ([I32, P, ctypes.POINTER(P)], I32),
+            "zkl_nccl_unique_id": ([ctypes.c_char_p], I32),
+            "zkl_ctx_create_dist": ([I32, P, ctypes.c_char_p, I32, I32, ctypes.POINTER(P)], I32),
+            "zkl_ctx_destroy": ([P], None),
+            "zkl_last_error": ([P], ctypes.c_char_p),
+            "zkl_workspace_bytes": ([U64, U64, I32], ctypes.c_size_t),
+            "zkl_ctx_set_workspace": ([P, P, ctypes.c_size_t], I32),
+            "zkl_ctx_launch_count": ([P], U64),
+            "zkl_vec_import": ([P, P, I32, zkl_vec, I64P], I32),
+            "zkl_vec_import_i64": ([P, P, zkl_vec], I32),
+            "zkl_vec_import_pair": ([P, P, P, ctypes.POINTER(zkl_fr), zkl_vec], I32),
+            "zkl_vec_export": ([P, zkl_vec, P, I32], I32),
+            "zkl_table_bytes": ([U64], ctypes.c_size_t),
+            "zkl_table_create": ([P, zkl_vec, P, ctypes.c_size_t, ctypes.POINTER(P), I64P], I32),
+            "zkl_table_destroy": ([P], None),
+            "zkl_tlookup_prepare": ([P, zkl_vec, U64, P, P, I64P], I32),
+            "zkl_tlookup_prove": ([P, zkl_vec, U64, P, P, ctypes.POINTER(zkl_challenges), I32, zkl_vec, zkl_vec,
+                                   ctypes.POINTER(zkl_fr), ctypes.POINTER(zkl_final_evals), I64P], I32),
+            "zkl_sumcheck_prove": ([P, zkl_vec, zkl_vec, U64, zkl_vec, zkl_vec, zkl_vec,
+                                    ctypes.POINTER(zkl_challenges), I32, ctypes.POINTER(zkl_fr),
+                                    ctypes.POINTER(zkl_final_evals)], I32),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+EXPORTED = ["zkl_strerror", "zkl_ctx_create", "zkl_nccl_unique_id", "zkl_ctx_create_dist", "zkl_ctx_destroy",
+            "zkl_last_error", "zkl_workspace_bytes", "zkl_ctx_set_workspace", "zkl_ctx_launch_count",
+            "zkl_vec_import", "zkl_vec_import_i64", "zkl_vec_import_pair", "zkl_vec_export", "zkl_table_bytes",
+            "zkl_table_create", "zkl_table_destroy", "zkl_tlookup_prepare", "zkl_tlookup_prove",
+            "zkl_sumcheck_prove"]
+
+
+def __getattr__(name):   # C names exposed unchanged: zkl.zkl_tlookup_prove(...)
+    if name in EXPORTED:
+        return getattr(lib(), name)
+    raise AttributeError(name)
+
+
+# ---------------------------------------------------------------- marshalling helpers
+def fr_from_int(x: int) -> zkl_fr:
+    if not 0 <= x < R_MODULUS:
+        raise ValueError("field element out of range")
+    f = zkl_fr()
+    for i in range(8):
+        f.w[i] = (x >> (32 * i)) & 0xFFFFFFFF
+    return f
+
+
+def fr_to_int(f: zkl_fr) -> int:
+    return sum(int(f.w[i]) << (32 * i) for i in range(8))
+
+
+def ints_to_canon(xs: Sequence[int]) -> np.ndarray:
+    """Python ints -> (n, 8) uint32 canonical little-endian words."""
+    out = np.zeros((len(xs), 8), dtype=np.uint32)
+    for i, x in enumerate(xs):
+        for k in range(8):
+            out[i, k] = (x >> (32 * k)) & 0xFFFFFFFF
+    return out
+
+
+def canon_to_ints(a: np.ndarray) -> List[int]:
+    a = np.asarray(a, dtype=np.uint32).reshape(-1, 8).astype(object)
+    return [int(sum(int(r[k]) << (32 * k) for k in range(8))) for r in a]
+
+
+@dataclass
+class Vec:
+    """A device field vector: torch int32 storage of 8*n words (SoA Montgomery)."""
+    data: "object"        # torch.Tensor
+    n: int
+
+    @property
+    def c(self) -> zkl_vec:
+        return zkl_vec(self.data.data_ptr() if self.data is not None else None, self.n)
+
+
+@dataclass
+class Proof:
+    evals: List[List[int]]
+    finals: Dict[str, int]
+    A: Optional[Vec] = None
+    B: Optional[Vec] = None
+
+
+class Context:
+    """One device context: stream, workspace and the zkl_ctx handle."""
+
+    def __init__(self, device: int = 0, stream=None, rank: int = 0, nranks: int = 1, nccl_id: bytes = None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("zkl needs a CUDA device (no CPU fallback)")
+        self.torch = torch
+        self.device = torch.device("cuda", device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        h = ctypes.c_void_p()
+        if nranks > 1:
+            st = lib().zkl_ctx_create_dist(device, ctypes.c_void_p(self.stream.cuda_stream), nccl_id, rank, nranks,
+                                           ctypes.byref(h))
+        else:
+            st = lib().zkl_ctx_create(device, ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h))
+        if st:
+            raise ZklError(st, -1, "context creation")
+        self.h = h
+        self.rank, self.nranks = rank, nranks
+        self.ws = None
+        self._tables = []
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().zkl_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- plumbing
+    def _check(self, st: int, idx: int = -1):
+        if st:
+            raise ZklError(st, idx, lib().zkl_last_error(self.h).decode(errors="replace"))
+
+    @property
+    def launches(self) -> int:
+        return int(lib().zkl_ctx_launch_count(self.h))
+
+    def reserve(self, D_local: int, N: int):
+        need = int(lib().zkl_workspace_bytes(D_local, N, self.nranks))
+        if need == 0:
+            raise ZklError(2, -1, f"bad shape D_local={D_local} N={N}")
+        if self.ws is None or self.ws.numel() < need:
+            self.ws = None
+            self.torch.cuda.synchronize(self.device)
+            self.ws = self.torch.empty(need + 256, dtype=self.torch.uint8, device=self.device)
+        ptr = self.ws.data_ptr()
+        pad = (-ptr) % 256
+        self._check(lib().zkl_ctx_set_workspace(self.h, ctypes.c_void_p(ptr + pad), need))
+
+    def vec(self, n: int) -> Vec:
+        return Vec(self.torch.empty(max(8 * n, 32), dtype=self.torch.int32, device=self.device), n)
+
+    # -- a1
+    def import_canon(self, canon: np.ndarray, dst: Optional[Vec] = None) -> Vec:
+        canon = np.ascontiguousarray(canon, dtype=np.uint32).reshape(-1, 8)
+        n = canon.shape[0]
+        dst = dst or self.vec(n)
+        err = ctypes.c_int64(-1)
+        st = lib().zkl_vec_import(self.h, canon.ctypes.data, 0, dst.c, ctypes.byref(err))
+        self._check(st, err.value)
+        return dst
+
+    def import_canon_device(self, canon_dev, n: int, dst: Optional[Vec] = None) -> Vec:
+        dst = dst or self.vec(n)
+        err = ctypes.c_int64(-1)
+        st = lib().zkl_vec_import(self.h, ctypes.c_void_p(canon_dev.data_ptr()), 1, dst.c, ctypes.byref(err))
+        self._check(st, err.value)
+        return dst
+
+    def import_ints(self, x, dst: Optional[Vec] = None) -> Vec:
+        t = self.torch.as_tensor(np.asarray(x, dtype=np.int64)).to(self.device) if not hasattr(x, "data_ptr") else x
+        n = t.numel()
+        dst = dst or self.vec(n)
+        self._check(lib().zkl_vec_import_i64(self.h, ctypes.c_void_p(t.data_ptr()), dst.c))
+        return dst
+
+    def import_pair(self, x, y, alpha_f: int, dst: Optional[Vec] = None) -> Vec:
+        tx = x if hasattr(x, "data_ptr") else self.torch.as_tensor(np.asarray(x, np.int32)).to(self.device)
+        ty = y if hasattr(y, "data_ptr") else self.torch.as_tensor(np.asarray(y, np.int32)).to(self.device)
+        n = tx.numel()
+        dst = dst or self.vec(n)
+        af = fr_from_int(alpha_f % R_MODULUS)
+        self._check(lib().zkl_vec_import_pair(self.h, ctypes.c_void_p(tx.data_ptr()), ctypes.c_void_p(ty.data_ptr()),
+                                              ctypes.byref(af), dst.c))
+        return dst
+
+    def export(self, v: Vec) -> np.ndarray:
+        out = np.zeros((v.n, 8), dtype=np.uint32)
+        self._check(lib().zkl_vec_export(self.h, v.c, out.ctypes.data, 0))
+        return out
+
+    def export_ints(self, v: Vec) -> List[int]:
+        return canon_to_ints(self.export(v))
+
+    # -- a2
+    def table(self, T: Vec):
+        nbytes = int(lib().zkl_table_bytes(T.n))
+        mem = self.torch.empty(nbytes + 256, dtype=self.torch.uint8, device=self.device)
+        ptr = mem.data_ptr()
+        pad = (-ptr) % 256
+        h = ctypes.c_void_p()
+        err = ctypes.c_int64(-1)
+        st = lib().zkl_table_create(self.h, T.c, ctypes.c_void_p(ptr + pad), nbytes, ctypes.byref(h),
+                                    ctypes.byref(err))
+        self._check(st, err.value)
+        tab = Table(h, T.n, mem, self)
+        return tab
+
+    # -- a3
+    def prepare(self, S: Vec, D: int, tab: "Table", m=None):
+        m = m if m is not None else self.torch.empty(tab.N, dtype=self.torch.int32, device=self.device)
+        err = ctypes.c_int64(-1)
+        st = lib().zkl_tlookup_prepare(self.h, S.c, D, tab.h, ctypes.c_void_p(m.data_ptr()), ctypes.byref(err))
+        self._check(st, err.value)
+        return m
+
+    # -- a4..a9
+    @staticmethod
+    def challenges(beta: int, alpha1: int, alpha2: int, u: Sequence[int], r: Sequence[int]):
+        U = (zkl_fr * max(len(u), 1))(*[fr_from_int(x % R_MODULUS) for x in u])
+        Rr = (zkl_fr * max(len(r), 1))(*[fr_from_int(x % R_MODULUS) for x in r])
+        ch = zkl_challenges(fr_from_int(beta % R_MODULUS), fr_from_int(alpha1 % R_MODULUS),
+                            fr_from_int(alpha2 % R_MODULUS), ctypes.cast(U, ctypes.POINTER(zkl_fr)),
+                            ctypes.cast(Rr, ctypes.POINTER(zkl_fr)))
+        ch._keep = (U, Rr)
+        return ch
+
+    def prove(self, S: Vec, D: int, tab: "Table", m, ch, variant: int = PAPER, want_A: bool = False,
+              want_B: bool = False) -> Proof:
+        d = D.bit_length() - 1
+        A = self.vec(S.n) if want_A else Vec(None, S.n)
+        B = self.vec(tab.N) if want_B else Vec(None, tab.N)
+        evals = (zkl_fr * (4 * max(d, 1)))()
+        fin = zkl_final_evals()
+        err = ctypes.c_int64(-1)
+        st = lib().zkl_tlookup_prove(self.h, S.c, D, tab.h, ctypes.c_void_p(m.data_ptr()), ctypes.byref(ch), variant,
+                                     A.c, B.c, evals, ctypes.byref(fin), ctypes.byref(err))
+        self._check(st, err.value)
+        return Proof(_evals(evals, d), _finals(fin), A if want_A else None, B if want_B else None)
+
+    def sumcheck(self, A: Vec, S: Vec, D: int, B: Vec, T: Vec, mfr: Vec, ch, variant: int = PAPER) -> Proof:
+        d = D.bit_length() - 1
+        evals = (zkl_fr * (4 * max(d, 1)))()
+        fin = zkl_final_evals()
+        st = lib().zkl_sumcheck_prove(self.h, A.c, S.c, D, B.c, T.c, mfr.c, ctypes.byref(ch), variant, evals,
+                                      ctypes.byref(fin))
+        self._check(st)
+        return Proof(_evals(evals, d), _finals(fin))
+
+
+class Table:
+    def __init__(self, h, N, mem, ctx):
+        self.h, self.N, self.mem, self.ctx = h, N, mem, ctx
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().zkl_table_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+def _evals(arr, d) -> List[List[int]]:
+    return [[fr_to_int(arr[4 * k + t]) for t in range(4)] for k in range(d)]
+
+
+def _finals(f: zkl_final_evals) -> Dict[str, int]:
+    return {"A": fr_to_int(f.A), "S": fr_to_int(f.S), "B": fr_to_int(f.B), "T": fr_to_int(f.T),
+            "m": fr_to_int(f.m)}
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    st = lib().zkl_nccl_unique_id(buf)
+    if st:
+        raise ZklError(st, -1, "ncclGetUniqueId")
+    return buf.raw
