@@ -237,17 +237,19 @@ static void batch_inverse(fe *out, const fe *in, uint64_t n) {
 /* e~(u, .) on {0,1}^k, coordinate 0 = MSB: built by expanding the product formula one
  * coordinate at a time (new[2i] = old[i](1-u_c), new[2i+1] = old[i] u_c).  Montgomery in/out. */
 static void eq_table(fe *out, const fe *u, int k) {
+    fe *prev = (fe *)malloc(((size_t)1 << (k > 0 ? k - 1 : 0)) * sizeof(fe));
     out[0] = ONE_M;
     for (int c = 0; c < k; ++c) {
         uint64_t sz = 1ULL << c;
+        memcpy(prev, out, sz * sizeof(fe));
         fe one_minus = fsub(ONE_M, u[c]);
         #pragma omp parallel for schedule(static) if (sz > 4096)
-        for (int64_t i = (int64_t)sz - 1; i >= 0; --i) {
-            fe o = out[i];
-            out[2 * i + 1] = fmul(o, u[c]);
-            out[2 * i] = fmul(o, one_minus);
+        for (int64_t i = 0; i < (int64_t)sz; ++i) {
+            out[2 * i + 1] = fmul(prev[i], u[c]);
+            out[2 * i] = fmul(prev[i], one_minus);
         }
     }
+    free(prev);
 }
 
 /*

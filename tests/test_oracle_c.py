@@ -29,7 +29,8 @@ def _chal(ch):
 
 
 @pytest.mark.parametrize("variant", [TL.PAPER, TL.LOGUP])
-@pytest.mark.parametrize("d,n", [(1, 0), (1, 1), (2, 0), (3, 3), (4, 1), (5, 3), (6, 6), (7, 2), (8, 4)])
+@pytest.mark.parametrize("d,n", [(1, 0), (1, 1), (2, 0), (3, 3), (4, 1), (5, 3), (6, 6), (7, 2), (8, 4), (14, 3),
+                                 (15, 9)])
 def test_c_equals_python(d, n, variant):
     rng = random.Random(d * 31 + n + variant)
     D, N = 1 << d, 1 << n
