@@ -44,12 +44,25 @@ int set_err(zkl_ctx* ctx, int st, const char* fmt, ...) {
         }                                                                                           \
     } while (0)
 
+// Every kernel launch goes through LAUNCH: counted, and (when profiling) bracketed by events on
+// the launching stream.
 #define LAUNCH(ctx, kern, grid, block, smem, stream, ...)                                           \
     do {                                                                                            \
+        zkl_ctx::ProfRec* pr_ = prof_begin((ctx), #kern, (stream));                                 \
         kern<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                                   \
         (ctx)->launches++;                                                                          \
+        if (pr_) cudaEventRecord(pr_->b, (stream));                                                 \
         CUDA_TRY(ctx, cudaGetLastError());                                                          \
     } while (0)
+
+zkl_ctx::ProfRec* prof_begin(zkl_ctx* ctx, const char* name, cudaStream_t st) {
+    if (!ctx->profiling || ctx->nprof >= 256) return nullptr;
+    zkl_ctx::ProfRec* r = &ctx->prof[ctx->nprof++];
+    r->name = name;
+    r->stream = st;
+    cudaEventRecord(r->a, st);
+    return r;
+}
 
 bool is_pow2(uint64_t x) { return x && !(x & (x - 1)); }
 int ilog2(uint64_t x) { int k = 0; while ((1ull << k) < x) ++k; return k; }
@@ -521,6 +534,8 @@ int zkl_ctx_create_dist(int device, void* cuda_stream, const uint8_t nccl_id[128
 void zkl_ctx_destroy(zkl_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
+    if (c->prof[0].a)
+        for (int i = 0; i < 256; ++i) { cudaEventDestroy(c->prof[i].a); cudaEventDestroy(c->prof[i].b); }
     if (c->nccl_comm) zkl_nccl_destroy(c);
     cudaStreamSynchronize(c->side);
     cudaStreamDestroy(c->side);
@@ -551,6 +566,33 @@ int zkl_ctx_set_workspace(zkl_ctx* c, void* ptr, size_t bytes) {
 }
 
 uint64_t zkl_ctx_launch_count(const zkl_ctx* c) { return c ? c->launches : 0; }
+
+int zkl_ctx_set_profiling(zkl_ctx* c, int on) {
+    if (!c) return ZKL_E_ARG;
+    if (on && !c->prof[0].a) {
+        for (int i = 0; i < 256; ++i) {
+            if (cudaEventCreate(&c->prof[i].a) != cudaSuccess || cudaEventCreate(&c->prof[i].b) != cudaSuccess)
+                return ZKL_E_CUDA;
+        }
+    }
+    c->profiling = on;
+    c->nprof = 0;
+    return ZKL_OK;
+}
+
+int zkl_ctx_profile_read(zkl_ctx* c, char* names, int name_len, float* ms, int cap) {
+    if (!c) return -ZKL_E_ARG;
+    int n = 0;
+    for (int i = 0; i < c->nprof && n < cap; ++i, ++n) {
+        float t = 0;
+        cudaEventSynchronize(c->prof[i].b);
+        cudaEventElapsedTime(&t, c->prof[i].a, c->prof[i].b);
+        ms[n] = t;
+        snprintf(names + (size_t)n * name_len, name_len, "%s", c->prof[i].name);
+    }
+    c->nprof = 0;
+    return n;
+}
 
 // ---------------------------------------------------------------- a1
 int zkl_vec_import(zkl_ctx* ctx, const void* canon, int src_on_device, zkl_vec dst, int64_t* err_index) {
@@ -661,10 +703,15 @@ int zkl_table_create(zkl_ctx* ctx, zkl_vec T, void* mem, size_t mem_bytes, zkl_t
     if (cudaMallocAsync((void**)&derr, sizeof(unsigned long long), ctx->stream) != cudaSuccess) return fail(ZKL_E_CUDA);
     cudaMemsetAsync(derr, 0xff, sizeof(unsigned long long), ctx->stream);
     cudaMemsetAsync(t->slots, 0, 4 * nslots, ctx->stream);
-    k_table_copy<<<grid_for(N, 256), 256, 0, ctx->stream>>>(T.limbs, N, t->T);
-    k_table_insert<<<grid_for(N, 256), 256, 0, ctx->stream>>>(t->T, N, t->slots, t->slot_mask);
-    k_table_dups<<<grid_for(N, 256), 256, 0, ctx->stream>>>(t->T, N, t->slots, t->slot_mask, derr);
-    ctx->launches += 3;
+    {
+        auto launch_all = [&]() -> int {
+            LAUNCH(ctx, k_table_copy, grid_for(N, 256), 256, 0, ctx->stream, T.limbs, N, t->T);
+            LAUNCH(ctx, k_table_insert, grid_for(N, 256), 256, 0, ctx->stream, t->T, N, t->slots, t->slot_mask);
+            LAUNCH(ctx, k_table_dups, grid_for(N, 256), 256, 0, ctx->stream, t->T, N, t->slots, t->slot_mask, derr);
+            return ZKL_OK;
+        };
+        if ((st = launch_all())) return fail(st);
+    }
     unsigned long long* herr = reinterpret_cast<unsigned long long*>((uint8_t*)ctx->host_out + 60000);
     cudaMemcpyAsync(herr, derr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream);
     cudaFreeAsync(derr, ctx->stream);

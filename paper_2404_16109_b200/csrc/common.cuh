@@ -147,6 +147,14 @@ struct zkl_ctx {
     int poisoned;
     uint64_t launches;
     char last_error[512];
+    // optional per-kernel timing (zkl_ctx_set_profiling): events around every launch
+    int profiling;
+    int nprof;
+    struct ProfRec {
+        const char* name;
+        cudaEvent_t a, b;
+        cudaStream_t stream;
+    } prof[256];
 };
 
 struct zkl_table {

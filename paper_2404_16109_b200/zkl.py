@@ -70,6 +70,8 @@ def lib() -> ctypes.CDLL:
             "zkl_workspace_bytes": ([U64, U64, I32], ctypes.c_size_t),
             "zkl_ctx_set_workspace": ([P, P, ctypes.c_size_t], I32),
             "zkl_ctx_launch_count": ([P], U64),
+            "zkl_ctx_set_profiling": ([P, I32], I32),
+            "zkl_ctx_profile_read": ([P, ctypes.c_char_p, I32, ctypes.POINTER(ctypes.c_float), I32], I32),
             "zkl_vec_import": ([P, P, I32, zkl_vec, I64P], I32),
             "zkl_vec_import_i64": ([P, P, zkl_vec], I32),
             "zkl_vec_import_pair": ([P, P, P, ctypes.POINTER(zkl_fr), zkl_vec], I32),
@@ -94,6 +96,7 @@ def lib() -> ctypes.CDLL:
 
 EXPORTED = ["zkl_strerror", "zkl_ctx_create", "zkl_nccl_unique_id", "zkl_ctx_create_dist", "zkl_ctx_destroy",
             "zkl_last_error", "zkl_workspace_bytes", "zkl_ctx_set_workspace", "zkl_ctx_launch_count",
+            "zkl_ctx_set_profiling", "zkl_ctx_profile_read",
             "zkl_vec_import", "zkl_vec_import_i64", "zkl_vec_import_pair", "zkl_vec_export", "zkl_table_bytes",
             "zkl_table_create", "zkl_table_destroy", "zkl_tlookup_prepare", "zkl_tlookup_prove",
             "zkl_sumcheck_prove"]
@@ -195,6 +198,20 @@ class Context:
     def launches(self) -> int:
         return int(lib().zkl_ctx_launch_count(self.h))
 
+    def set_profiling(self, on: bool):
+        self._check(lib().zkl_ctx_set_profiling(self.h, 1 if on else 0))
+
+    def profile_read(self):
+        """[(kernel name, ms)] of the launches recorded since profiling was (re)enabled or last read."""
+        cap, nl = 256, 64
+        names = ctypes.create_string_buffer(cap * nl)
+        ms = (ctypes.c_float * cap)()
+        n = lib().zkl_ctx_profile_read(self.h, names, nl, ms, cap)
+        if n < 0:
+            raise ZklError(-n, -1, "profile_read")
+        raw = names.raw
+        return [(raw[i * nl:(i + 1) * nl].split(b"\0", 1)[0].decode(), float(ms[i])) for i in range(n)]
+
     def reserve(self, D_local: int, N: int):
         need = int(lib().zkl_workspace_bytes(D_local, N, self.nranks))
         if need == 0:
@@ -253,9 +270,12 @@ class Context:
         return canon_to_ints(self.export(v))
 
     # -- a2
-    def table(self, T: Vec):
+    def table_mem(self, N: int):
+        return self.torch.empty(int(lib().zkl_table_bytes(N)) + 256, dtype=self.torch.uint8, device=self.device)
+
+    def table(self, T: Vec, mem=None):
         nbytes = int(lib().zkl_table_bytes(T.n))
-        mem = self.torch.empty(nbytes + 256, dtype=self.torch.uint8, device=self.device)
+        mem = mem if mem is not None else self.table_mem(T.n)
         ptr = mem.data_ptr()
         pad = (-ptr) % 256
         h = ctypes.c_void_p()
