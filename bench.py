@@ -262,7 +262,10 @@ def main():
     d2h = 32 * (4 * d + 5)
 
     # ---------------- roofline of the dominant kernel (largest share of the step)
-    tot = {k: sum(v) / args.steps for k, v in kern.items()}
+    tot = {}
+    for k, v in kern.items():
+        k = k.strip("()").split("<")[0] if k.startswith("(") else k
+        tot[k] = tot.get(k, 0.0) + sum(v) / args.steps
     dom = max(tot, key=tot.get)
     per_step_work = 0.0
     if dom == "k_inv_fwd" or dom == "k_inv_bwd":

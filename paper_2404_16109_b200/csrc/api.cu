@@ -69,20 +69,34 @@ int ilog2(uint64_t x) { int k = 0; while ((1ull << k) < x) ++k; return k; }
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 size_t soa_bytes(uint64_t n) { return align_up(8 * 4 * std::max<uint64_t>(n, 4)); }
 
-unsigned grid_for(uint64_t work, unsigned threads, unsigned cap = kSMs * 8) {
+unsigned grid_for(uint64_t work, unsigned threads, unsigned cap) {
     uint64_t g = (work + threads - 1) / threads;
     if (g < 1) g = 1;
     if (g > cap) g = cap;
     return (unsigned)g;
 }
 
+unsigned grid_for(uint64_t work, unsigned threads) { return grid_for(work, threads, kSMs * 8); }
+
 int hist_rows_for(uint64_t Dp, uint64_t N) {
     uint64_t ntiles = (Dp + kHistTile - 1) / kHistTile;
     uint64_t cap = std::max<uint64_t>(1, (256ull << 20) / (4 * N));
-    return (int)std::min<uint64_t>(std::min<uint64_t>(kSMs, ntiles), cap);
+    return (int)std::min<uint64_t>(std::min<uint64_t>(2 * kSMs, ntiles), cap);
 }
 
 // ------------------------------------------------------------------ plan + workspace layout
+constexpr uint64_t kInvTop = 8192;   // the top level of the inversion hierarchy: one block
+
+// One hierarchical batched inversion over level-0 tiles [t0, t1) (a4).
+struct InvPlan {
+    uint64_t t0, t1;
+    int nlev;              // tiled levels above level 0
+    uint64_t n[12];        // n[0]: level-0 elements of the range; n[L], L >= 1: level sizes; n[nlev+1]: top
+    size_t o_val[12], o_slot[12], o_topinv;
+};
+
+unsigned grid_for(uint64_t work, unsigned threads, unsigned cap);
+
 struct Plan {
     uint64_t D, Dp, N;
     int d, dl, n, pbits, P, rank;
@@ -95,11 +109,14 @@ struct Plan {
     int njobs;
     uint64_t arena;
     uint64_t ntiles;     // inversion tiles (Dp / 4096)
+    int nhalves;
+    InvPlan inv[2];      // D side, one hierarchy per half
+    InvPlan tinv;        // table side (N >= 4096)
     int inv_blocks;
     int hist_rows;
     // workspace offsets
     size_t o_out, o_sc, o_err, o_rounds, o_jobs, o_chal, o_part, o_tpart, o_tnb, o_rank, o_gath, o_repl, o_tsum,
-        o_fin, o_tfin, o_gfin, o_arena, o_hist, o_tot, o_totinv, o_A, o_A1, o_S1, o_A2, o_S2, o_tB, o_tX, o_tM,
+        o_fin, o_tfin, o_gfin, o_rc, o_arena, o_hist, o_tot, o_totinv, o_A, o_A1, o_S1, o_A2, o_S2, o_tB, o_tX, o_tM,
         o_tE, o_tp[2][4], total;
 };
 
@@ -118,7 +135,14 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
     p.Dp = D / P;
     p.small = p.Dp < (uint64_t)kInvTile;
     p.ntiles = p.small ? 0 : p.Dp / kInvTile;
-    p.inv_blocks = p.small ? 0 : (int)std::min<uint64_t>(p.ntiles, kSMs * 4);
+    p.nhalves = p.small ? 0 : (p.ntiles >= 2 ? 2 : 1);
+    p.inv_blocks = 0;
+    for (int h = 0; h < p.nhalves; ++h) {
+        InvPlan& ip = p.inv[h];
+        ip.t0 = h == 0 ? 0 : p.ntiles / 2;
+        ip.t1 = (h == 0 && p.nhalves == 2) ? p.ntiles / 2 : p.ntiles;
+        p.inv_blocks += (int)std::min<uint64_t>(ip.t1 - ip.t0, kSMs * 2);
+    }
     p.hist_rows = hist_rows_for(p.Dp, N);
     // ---- D-side local rounds
     if (p.small) {
@@ -199,6 +223,7 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
     p.o_fin = take(sizeof(fr) * 4);
     p.o_tfin = take(sizeof(fr) * 4);
     p.o_gfin = take(sizeof(fr) * 2 * (size_t)P);
+    p.o_rc = take(sizeof(RoundConst) * kMaxRounds);
     p.o_arena = take(sizeof(fr) * p.arena);
     p.o_hist = take(sizeof(uint32_t) * (size_t)p.hist_rows * N);
     p.o_tot = take(soa_bytes(p.ntiles));
@@ -214,6 +239,28 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
     p.o_tE = take(soa_bytes(N));
     for (int q = 0; q < 4; ++q) p.o_tp[0][q] = take(soa_bytes(N / 2));
     for (int q = 0; q < 4; ++q) p.o_tp[1][q] = take(soa_bytes(N / 4));
+    auto inv_levels = [&](InvPlan& ip, uint64_t n0) {
+        ip.n[0] = n0;
+        int L = 0;
+        uint64_t nl = n0 / kInvPer;
+        while (nl > kInvTop) {
+            ++L;
+            ip.n[L] = nl;
+            ip.o_val[L] = take(soa_bytes(nl));
+            ip.o_slot[L] = take(soa_bytes(nl));
+            nl /= kInvPer;
+        }
+        ip.nlev = L;
+        ip.n[L + 1] = nl;
+        ip.o_val[L + 1] = take(soa_bytes(nl));
+        ip.o_topinv = take(soa_bytes(nl));
+    };
+    for (int h = 0; h < p.nhalves; ++h) inv_levels(p.inv[h], (p.inv[h].t1 - p.inv[h].t0) * kInvTile);
+    if (N >= (uint64_t)kInvTile) {
+        p.tinv.t0 = 0;
+        p.tinv.t1 = N / kInvTile;
+        inv_levels(p.tinv, N);
+    }
     p.total = o;
 }
 
@@ -259,6 +306,48 @@ int sync_stream(zkl_ctx* ctx) {
         ctx->poisoned = 1;
         return set_err(ctx, ZKL_E_CUDA, "asynchronous CUDA error: %s", cudaGetErrorString(e));
     }
+    return ZKL_OK;
+}
+
+// ------------------------------------------------------------------ hierarchical batched inversion (a4)
+// Forward passes: level 0 on `s0` (the caller's stream), the levels above and the one-block top on `s1`.
+int inv_forward(zkl_ctx* ctx, const InvPlan& ip, const uint32_t* X0, uint64_t n0total, uint32_t* slots0,
+                const ProofScalars* sc, uint64_t err_off, unsigned long long* err, cudaStream_t s0, cudaStream_t s1,
+                cudaEvent_t ev) {
+    const unsigned nb0 = (unsigned)std::min<uint64_t>(ip.t1 - ip.t0, kSMs * 2);
+    LAUNCH(ctx, k_inv_fwd<true>, nb0, kInvThreads, 0, s0, X0, n0total, sc, slots0, at<uint32_t>(ctx, ip.o_val[1]),
+           ip.n[1], ip.t0, ip.t1, err_off, err);
+    if (s1 != s0) {
+        CUDA_TRY(ctx, cudaEventRecord(ev, s0));
+        CUDA_TRY(ctx, cudaStreamWaitEvent(s1, ev, 0));
+    }
+    for (int L = 1; L <= ip.nlev; ++L) {
+        const uint64_t tiles = ip.n[L] / kInvTile;
+        LAUNCH(ctx, k_inv_fwd<false>, (unsigned)std::min<uint64_t>(tiles, kSMs * 2), kInvThreads, 0, s1,
+               at<uint32_t>(ctx, ip.o_val[L]), ip.n[L], sc, at<uint32_t>(ctx, ip.o_slot[L]),
+               at<uint32_t>(ctx, ip.o_val[L + 1]), ip.n[L + 1], (uint64_t)0, tiles, (uint64_t)0, err);
+    }
+    const uint64_t ntop = ip.n[ip.nlev + 1];
+    const unsigned bt = (unsigned)std::min<uint64_t>(1024, std::max<uint64_t>(32, ntop / 8));
+    LAUNCH(ctx, k_batch_invert, 1, bt, 4 * bt * sizeof(fr), s1, at<uint32_t>(ctx, ip.o_val[ip.nlev + 1]), ntop,
+           (uint64_t)0, ntop, at<uint32_t>(ctx, ip.o_topinv));
+    for (int L = ip.nlev; L >= 1; --L) {
+        const uint64_t tiles = ip.n[L] / kInvTile;
+        const uint32_t* ninv = L == ip.nlev ? at<uint32_t>(ctx, ip.o_topinv) : at<uint32_t>(ctx, ip.o_slot[L + 1]);
+        LAUNCH(ctx, k_inv_bwd<false>, (unsigned)std::min<uint64_t>(tiles, kSMs * 2), kInvThreads, 0, s1,
+               at<uint32_t>(ctx, ip.o_val[L]), ip.n[L], sc, at<uint32_t>(ctx, ip.o_slot[L]), ninv, ip.n[L + 1],
+               (uint64_t)0, tiles, (const fr*)nullptr, (const fr*)nullptr, (fr*)nullptr, 0);
+    }
+    return ZKL_OK;
+}
+
+// Level-0 backward pass on s0 (after the upper levels on s1 completed: caller orders via events).
+int inv_backward0(zkl_ctx* ctx, const InvPlan& ip, const uint32_t* X0, uint64_t n0total, uint32_t* slots0,
+                  const ProofScalars* sc, const fr* elo, const fr* ehi, fr* partials, int row0, cudaStream_t s0) {
+    const unsigned nb0 = (unsigned)std::min<uint64_t>(ip.t1 - ip.t0, kSMs * 2);
+    const uint32_t* ninv = ip.nlev >= 1 ? at<uint32_t>(ctx, ip.o_slot[1]) : at<uint32_t>(ctx, ip.o_topinv);
+    LAUNCH(ctx, k_inv_bwd<true>, nb0, kInvThreads, 0, s0, X0, n0total, sc, slots0, ninv, ip.n[1], ip.t0, ip.t1, elo,
+           ehi, partials, row0);
     return ZKL_OK;
 }
 
@@ -337,6 +426,8 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
     LAUNCH(ctx, k_eq_fill, grid_for(p.arena, 256), 256, 0, s, jobs, p.njobs, p.arena, sc, arena);
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, s));
     CUDA_TRY(ctx, cudaStreamWaitEvent(s2, ctx->ev_fork, 0));
+    RoundConst* rc = at<RoundConst>(ctx, p.o_rc);
+    LAUNCH(ctx, k_round_consts, 1, 64, 0, s2, sc, p.d, p.n, rc);
 
     // ================= table side (side stream)
     uint32_t* tB = at<uint32_t>(ctx, p.o_tB);
@@ -345,9 +436,14 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
     uint32_t* tE = at<uint32_t>(ctx, p.o_tE);
     const uint32_t* Tsrc = a.prove_mode ? a.table->T : a.T_in.limbs;
     if (a.prove_mode) {
-        LAUNCH(ctx, k_add_beta, grid_for(N, 256), 256, 0, s2, Tsrc, N, sc, tX, err + 1);
-        const unsigned bt = (unsigned)std::min<uint64_t>(1024, std::max<uint64_t>(32, N));
-        LAUNCH(ctx, k_batch_invert, 1, bt, 4 * bt * sizeof(fr), s2, tX, N, tB);
+        if (N >= (uint64_t)kInvTile) {
+            if ((st = inv_forward(ctx, p.tinv, Tsrc, N, tB, sc, 0, err + 1, s2, s2, nullptr))) return st;
+            if ((st = inv_backward0(ctx, p.tinv, Tsrc, N, tB, sc, nullptr, nullptr, nullptr, 0, s2))) return st;
+        } else {
+            LAUNCH(ctx, k_add_beta, grid_for(N, 256), 256, 0, s2, Tsrc, N, sc, tX, err + 1);
+            const unsigned bt = (unsigned)std::min<uint64_t>(1024, std::max<uint64_t>(32, N));
+            LAUNCH(ctx, k_batch_invert, 1, bt, 4 * bt * sizeof(fr), s2, tX, N, (uint64_t)0, N, tB);
+        }
         LAUNCH(ctx, k_tab_init, grid_for(N, 256), 256, 0, s2, a.m_dev, N, tM, tB, sc, p.d, p.n, a.variant, tE);
         if (a.B_out.limbs) LAUNCH(ctx, k_copy_vec, grid_for(8 * N, 256), 256, 0, s2, tB, N, a.B_out.limbs);
     } else {
@@ -382,19 +478,32 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
     const uint32_t* S1in = a.S.limbs;
     const uint64_t errS_off = (uint64_t)p.rank * p.Dp;
     const size_t tail_smem = (2 * kTailMax + 4 * kTailThreads) * sizeof(fr) + 5 * (kTailThreads / 32) * sizeof(fr);
+    int rounds_nb0 = -1;   // round-1 partial rows written by the inversion (prove mode)
     if (p.small) {
         LAUNCH(ctx, k_tail, 1, kTailThreads, tail_smem, s, A1in, S1in, p.Dp, 0, a.prove_mode ? 1 : 0, Abuf,
                errS_off, err, sc, 1, p.dl, rounds, arena, partials, fin);
     } else {
         if (a.prove_mode) {
-            uint32_t* tot = at<uint32_t>(ctx, p.o_tot);
-            uint32_t* totinv = at<uint32_t>(ctx, p.o_totinv);
-            LAUNCH(ctx, k_inv_fwd, p.inv_blocks, kInvThreads, 0, s, a.S.limbs, p.Dp, sc, Abuf, tot, p.ntiles, errS_off,
-                   err);
-            const unsigned bt = (unsigned)std::min<uint64_t>(1024, std::max<uint64_t>(32, p.ntiles));
-            LAUNCH(ctx, k_batch_invert, 1, bt, 4 * bt * sizeof(fr), s, tot, p.ntiles, totinv);
-            LAUNCH(ctx, k_inv_bwd, p.inv_blocks, kInvThreads, 0, s, a.S.limbs, p.Dp, sc, Abuf, totinv, p.ntiles,
-                   arena + p.rd[0].elo_off, arena + p.rd[0].ehi_off, 1, partials);
+            // hierarchical batched inversion in two halves: the upper levels + one-block top (one Fermat) of
+            // half h run on the aux stream while the main stream does the level-0 forward pass of the other
+            // half (h = 0) or the level-0 backward pass of half 0 (h = 1), hiding their latency.
+            const int halves = p.nhalves;
+            int nb[2] = {0, 0}, row0[2] = {0, 0};
+            for (int h = 0; h < halves; ++h) {
+                nb[h] = (int)std::min<uint64_t>(p.inv[h].t1 - p.inv[h].t0, kSMs * 2);
+                if ((st = inv_forward(ctx, p.inv[h], a.S.limbs, p.Dp, Abuf, sc, errS_off, err, s, ctx->aux,
+                                      ctx->ev_fwd[h])))
+                    return st;
+                CUDA_TRY(ctx, cudaEventRecord(ctx->ev_mid[h], ctx->aux));
+            }
+            if (halves == 2) row0[1] = nb[0];
+            for (int h = 0; h < halves; ++h) {
+                CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_mid[h], 0));
+                if ((st = inv_backward0(ctx, p.inv[h], a.S.limbs, p.Dp, Abuf, sc, arena + p.rd[0].elo_off,
+                                        arena + p.rd[0].ehi_off, partials, row0[h], s)))
+                    return st;
+            }
+            rounds_nb0 = halves == 2 ? nb[0] + nb[1] : nb[0];
         }
         const uint32_t *cA = A1in, *cS = S1in;
         uint64_t len = p.Dp;
@@ -402,14 +511,18 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
             const RoundDesc& r = p.rd[k - 1];
             fr* part = partials + (size_t)(k - 1) * kSlots * kMaxBlocks;
             if (k == 1) {
-                LAUNCH(ctx, k_round<false>, r.nblocks, kRoundThreads, 0, s, cA, cS, len, nullptr, nullptr, sc, k,
-                       arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, (int)r.direct_h1, part);
+                LAUNCH(ctx, (k_round<false, true>), r.nblocks, kRoundThreads, 0, s, cA, cS, len, nullptr, nullptr, sc,
+                       k, arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, part);
             } else {
                 const bool odd = (k & 1) == 0;   // k = 2 -> buffers 1
                 uint32_t* nA = at<uint32_t>(ctx, odd ? p.o_A1 : p.o_A2);
                 uint32_t* nS = at<uint32_t>(ctx, odd ? p.o_S1 : p.o_S2);
-                LAUNCH(ctx, k_round<true>, r.nblocks, kRoundThreads, 0, s, cA, cS, len, nA, nS, sc, k,
-                       arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, (int)r.direct_h1, part);
+                if (r.direct_h1)
+                    LAUNCH(ctx, (k_round<true, true>), r.nblocks, kRoundThreads, 0, s, cA, cS, len, nA, nS, sc, k,
+                           arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, part);
+                else
+                    LAUNCH(ctx, (k_round<true, false>), r.nblocks, kRoundThreads, 0, s, cA, cS, len, nA, nS, sc, k,
+                           arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, part);
                 cA = nA; cS = nS;
                 len /= 2;
             }
@@ -417,6 +530,10 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
         // tail input: the vectors of round k0-1 (len elements), folded with r_{k0-1} on load
         LAUNCH(ctx, k_tail, 1, kTailThreads, tail_smem, s, cA, cS, len, 1, 0, (uint32_t*)nullptr, errS_off, err, sc,
                p.k0, p.dl, rounds, arena, partials, fin);
+    }
+    if (rounds_nb0 >= 0 && (uint32_t)rounds_nb0 != p.rd[0].nblocks) {
+        // the plan's round-1 row count must match what the inversion wrote
+        return set_err(ctx, ZKL_E_STATE, "internal: round-1 rows %d != plan %u", rounds_nb0, p.rd[0].nblocks);
     }
     if (p.dl > 0) LAUNCH(ctx, k_reduce_rounds, p.dl, 256, 0, s, partials, rounds, p.dl, rank_sums);
     const fr* gathered = rank_sums;
@@ -433,8 +550,8 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
                rounds + p.dl, p.d - p.dl, repl);
     }
     CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
-    LAUNCH(ctx, k_derive, 1, 32, 0, s, gathered, ctx->nranks, p.dl, repl, rounds, tsum, sc, p.d, p.n, a.variant,
-           a.prove_mode ? 1 : 0, fin, tfin, out);
+    LAUNCH(ctx, k_derive, 1, 64, 0, s, gathered, ctx->nranks, p.dl, repl, rounds, tsum, sc, rc, p.d, p.n,
+           a.variant, a.prove_mode ? 1 : 0, fin, tfin, out);
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->host_out, out, sizeof(ProofOut), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(ctx, cudaMemcpyAsync((uint8_t*)ctx->host_out + offsetof(ProofOut, err_index), err,
                                   2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
@@ -496,12 +613,23 @@ static int ctx_create_common(int device, void* stream, zkl_ctx** out) {
     c->nranks = 1;
     if (cudaSetDevice(device) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_fwd[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_fwd[1], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_mid[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_mid[1], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
-        cudaMallocHost(&c->host_out, 1 << 16) != cudaSuccess) {
+        cudaMallocHost(&c->host_out, 1 << 16) != cudaSuccess || cudaMalloc(&c->dscratch, 4096) != cudaSuccess) {
         cudaGetLastError();
         free(c);
         return ZKL_E_CUDA;
+    }
+    // stream-ordered allocations (host-sourced import/export only) must not be trimmed at every sync
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     const size_t tail_smem = (2 * kTailMax + 4 * kTailThreads) * sizeof(fr) + 5 * (kTailThreads / 32) * sizeof(fr);
     cudaFuncSetAttribute(k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tail_smem);
@@ -538,10 +666,14 @@ void zkl_ctx_destroy(zkl_ctx* c) {
         for (int i = 0; i < 256; ++i) { cudaEventDestroy(c->prof[i].a); cudaEventDestroy(c->prof[i].b); }
     if (c->nccl_comm) zkl_nccl_destroy(c);
     cudaStreamSynchronize(c->side);
+    cudaStreamSynchronize(c->aux);
     cudaStreamDestroy(c->side);
+    cudaStreamDestroy(c->aux);
+    for (int i = 0; i < 2; ++i) { cudaEventDestroy(c->ev_fwd[i]); cudaEventDestroy(c->ev_mid[i]); }
     cudaEventDestroy(c->ev_fork);
     cudaEventDestroy(c->ev_join);
     cudaFreeHost(c->host_out);
+    cudaFree(c->dscratch);
     free(c);
 }
 
@@ -580,14 +712,16 @@ int zkl_ctx_set_profiling(zkl_ctx* c, int on) {
     return ZKL_OK;
 }
 
-int zkl_ctx_profile_read(zkl_ctx* c, char* names, int name_len, float* ms, int cap) {
+int zkl_ctx_profile_read(zkl_ctx* c, char* names, int name_len, float* ms, float* start_ms, int cap) {
     if (!c) return -ZKL_E_ARG;
     int n = 0;
     for (int i = 0; i < c->nprof && n < cap; ++i, ++n) {
-        float t = 0;
+        float t = 0, t0 = 0;
         cudaEventSynchronize(c->prof[i].b);
         cudaEventElapsedTime(&t, c->prof[i].a, c->prof[i].b);
+        cudaEventElapsedTime(&t0, c->prof[0].a, c->prof[i].a);
         ms[n] = t;
+        if (start_ms) start_ms[n] = t0;
         snprintf(names + (size_t)n * name_len, name_len, "%s", c->prof[i].name);
     }
     c->nprof = 0;
@@ -610,12 +744,10 @@ int zkl_vec_import(zkl_ctx* ctx, const void* canon, int src_on_device, zkl_vec d
         src = (const uint32_t*)tmp;
     }
     unsigned long long* err = reinterpret_cast<unsigned long long*>((uint8_t*)ctx->host_out + 60000);
-    unsigned long long* derr = nullptr;
-    CUDA_TRY(ctx, cudaMallocAsync((void**)&derr, sizeof(unsigned long long), ctx->stream));
+    unsigned long long* derr = reinterpret_cast<unsigned long long*>(ctx->dscratch);
     CUDA_TRY(ctx, cudaMemsetAsync(derr, 0xff, sizeof(unsigned long long), ctx->stream));
     LAUNCH(ctx, k_import_canon, grid_for(dst.n, 256), 256, 0, ctx->stream, src, dst.n, dst.limbs, derr);
     CUDA_TRY(ctx, cudaMemcpyAsync(err, derr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(ctx, cudaFreeAsync(derr, ctx->stream));
     if (tmp) CUDA_TRY(ctx, cudaFreeAsync(tmp, ctx->stream));
     if ((st = sync_stream(ctx))) return st;
     if (*err != ~0ull) {
@@ -642,13 +774,13 @@ int zkl_vec_import_pair(zkl_ctx* ctx, const int32_t* x, const int32_t* y, const 
     if ((st = check_vec(ctx, dst, dst.n, "dst"))) return st;
     if (dst.n == 0) return ZKL_OK;
     // alpha_f -> Montgomery on the device (one launch, no host arithmetic)
-    fr* af = nullptr;
-    CUDA_TRY(ctx, cudaMallocAsync((void**)&af, sizeof(fr), ctx->stream));
-    CUDA_TRY(ctx, cudaMemcpyAsync(af, alpha_f, sizeof(fr), cudaMemcpyHostToDevice, ctx->stream));
+    fr* af = reinterpret_cast<fr*>(ctx->dscratch + 64);
+    zkl_fr* staged = reinterpret_cast<zkl_fr*>((uint8_t*)ctx->host_out + 62000);
+    *staged = *alpha_f;
+    CUDA_TRY(ctx, cudaMemcpyAsync(af, staged, sizeof(fr), cudaMemcpyHostToDevice, ctx->stream));
     LAUNCH(ctx, k_import_canon, 1, 32, 0, ctx->stream, (const uint32_t*)af, 1, (uint32_t*)af,
            (unsigned long long*)nullptr);
     LAUNCH(ctx, k_import_pair_dev, grid_for(dst.n, 256), 256, 0, ctx->stream, x, y, dst.n, af, dst.limbs);
-    CUDA_TRY(ctx, cudaFreeAsync(af, ctx->stream));
     return sync_stream(ctx);
 }
 
@@ -675,8 +807,8 @@ int zkl_vec_export(zkl_ctx* ctx, zkl_vec src, void* canon, int dst_on_device) {
 // ---------------------------------------------------------------- a2
 size_t zkl_table_bytes(uint64_t N) {
     if (!is_pow2(N)) return 0;
-    uint64_t slots = std::max<uint64_t>(64, 2 * N);
-    return soa_bytes(N) + align_up(4 * slots);
+    uint64_t slots = std::max<uint64_t>(64, 4 * N);   // load factor <= 1/4
+    return soa_bytes(N) + align_up(32 * N) + align_up(4 * slots);
 }
 
 int zkl_table_create(zkl_ctx* ctx, zkl_vec T, void* mem, size_t mem_bytes, zkl_table** out, int64_t* err_index) {
@@ -692,29 +824,29 @@ int zkl_table_create(zkl_ctx* ctx, zkl_vec T, void* mem, size_t mem_bytes, zkl_t
         return set_err(ctx, ZKL_E_OOM, "table memory: need %zu bytes, 256-byte aligned", zkl_table_bytes(N));
     zkl_table* t = (zkl_table*)calloc(1, sizeof(zkl_table));
     if (!t) return ZKL_E_OOM;
-    const uint64_t nslots = std::max<uint64_t>(64, 2 * N);
+    const uint64_t nslots = std::max<uint64_t>(64, 4 * N);
     t->N = N;
     t->T = (uint32_t*)mem;
-    t->slots = (uint32_t*)((uint8_t*)mem + soa_bytes(N));
+    t->Taos = (uint4*)((uint8_t*)mem + soa_bytes(N));
+    t->slots = (uint32_t*)((uint8_t*)mem + soa_bytes(N) + align_up(32 * N));
     t->slot_mask = (uint32_t)(nslots - 1);
     t->device = ctx->device;
-    unsigned long long* derr = nullptr;
+    unsigned long long* derr = reinterpret_cast<unsigned long long*>(ctx->dscratch + 8);
     auto fail = [&](int code) { free(t); return code; };
-    if (cudaMallocAsync((void**)&derr, sizeof(unsigned long long), ctx->stream) != cudaSuccess) return fail(ZKL_E_CUDA);
     cudaMemsetAsync(derr, 0xff, sizeof(unsigned long long), ctx->stream);
     cudaMemsetAsync(t->slots, 0, 4 * nslots, ctx->stream);
     {
         auto launch_all = [&]() -> int {
-            LAUNCH(ctx, k_table_copy, grid_for(N, 256), 256, 0, ctx->stream, T.limbs, N, t->T);
+            LAUNCH(ctx, k_table_copy, grid_for(N, 256), 256, 0, ctx->stream, T.limbs, N, t->T, t->Taos);
             LAUNCH(ctx, k_table_insert, grid_for(N, 256), 256, 0, ctx->stream, t->T, N, t->slots, t->slot_mask);
-            LAUNCH(ctx, k_table_dups, grid_for(N, 256), 256, 0, ctx->stream, t->T, N, t->slots, t->slot_mask, derr);
+            LAUNCH(ctx, k_table_dups, grid_for(N, 256), 256, 0, ctx->stream, t->T, t->Taos, N, t->slots, t->slot_mask,
+                   derr);
             return ZKL_OK;
         };
         if ((st = launch_all())) return fail(st);
     }
     unsigned long long* herr = reinterpret_cast<unsigned long long*>((uint8_t*)ctx->host_out + 60000);
     cudaMemcpyAsync(herr, derr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream);
-    cudaFreeAsync(derr, ctx->stream);
     if ((st = sync_stream(ctx))) return fail(st);
     if (*herr != ~0ull) {
         if (err_index) *err_index = (int64_t)*herr;
@@ -743,9 +875,11 @@ int zkl_tlookup_prepare(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T,
     unsigned long long* err = at<unsigned long long>(ctx, p.o_err);
     uint32_t* rows = at<uint32_t>(ctx, p.o_hist);
     CUDA_TRY(ctx, cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), ctx->stream));
-    TableView tv{T->T, T->slots, T->N, T->slot_mask};
+    TableView tv{T->T, T->Taos, T->slots, T->N, T->slot_mask};
+    // key bits: n (+1 for the sentinel of a partial tile when D_local < 4096)
+    const int key_bits = std::max(1, p.n + (p.Dp < (uint64_t)kHistTile ? 1 : 0));
     LAUNCH(ctx, k_hist_rows, p.hist_rows, kHistThreads, 0, ctx->stream, S.limbs, p.Dp, (uint64_t)ctx->rank * p.Dp,
-           tv, rows, p.n + 1, err);
+           tv, rows, key_bits, err);
     LAUNCH(ctx, k_hist_colsum, grid_for(T->N, 256), 256, 0, ctx->stream, rows, p.hist_rows, T->N, m_dev);
     if (ctx->nranks > 1) {
         int rc = zkl_dist_allreduce_u32(ctx, m_dev, T->N);

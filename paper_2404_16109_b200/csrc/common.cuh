@@ -138,12 +138,15 @@ struct zkl_ctx {
     int device;
     cudaStream_t stream;
     cudaStream_t side;             // table-side work overlapping the D side
+    cudaStream_t aux;              // batch inversions of the tile totals (latency hidden behind the D side)
     cudaEvent_t ev_fork, ev_join;
+    cudaEvent_t ev_fwd[2], ev_mid[2];
     int rank, nranks;
     void* nccl_comm;               // ncclComm_t (loaded at run time) when nranks > 1
     uint8_t* ws;
     size_t ws_bytes;
-    void* host_out;                // pinned host copy of ProofOut
+    void* host_out;                // pinned host copy of ProofOut + staging
+    uint8_t* dscratch;             // 4 KiB device scratch (scalars, error words) owned by the ctx
     int poisoned;
     uint64_t launches;
     char last_error[512];
@@ -160,6 +163,7 @@ struct zkl_ctx {
 struct zkl_table {
     uint64_t N;
     uint32_t* T;        // SoA Montgomery copy, N entries
+    uint4* Taos;        // AoS copy (32 B per entry) for key compares
     uint32_t* slots;    // open-addressing hash: slot -> index+1 (0 = empty)
     uint32_t slot_mask;
     int device;

@@ -54,6 +54,21 @@ __device__ __forceinline__ fr fr_r2() {
     return o;
 }
 
+#define ZKL_FR_CONST(name, a0, a1, a2, a3, a4, a5, a6, a7)                                          \
+    __device__ __forceinline__ fr name() {                                                          \
+        fr o;                                                                                       \
+        o.v[0] = a0; o.v[1] = a1; o.v[2] = a2; o.v[3] = a3; o.v[4] = a4; o.v[5] = a5; o.v[6] = a6;   \
+        o.v[7] = a7;                                                                                \
+        return o;                                                                                   \
+    }
+// Montgomery forms of small constants (x * 2^256 mod r)
+ZKL_FR_CONST(fr_inv2_m, 0xffffffffu, 0x00000000u, 0x0001a401u, 0xac425bfdu, 0xf65e27fau, 0xccc627f7u, 0xd66282b7u, 0x0c1258acu)
+ZKL_FR_CONST(fr_inv6_m, 0xaaaaaaabu, 0xffffffffu, 0x5554c954u, 0x1be9e156u, 0xade09d57u, 0x11134802u, 0x63347f18u, 0x514f37c6u)
+ZKL_FR_CONST(fr_two_m, 0xfffffffcu, 0x00000003u, 0x00069004u, 0xb1096ff4u, 0xd9789feau, 0x33189fdfu, 0x598a0adfu, 0x304962b3u)
+ZKL_FR_CONST(fr_three_m, 0xfffffffau, 0x00000005u, 0x0009d806u, 0x098e27eeu, 0xc634efe0u, 0xcca4efcfu, 0x064f104eu, 0x486e140du)
+ZKL_FR_CONST(fr_five_m, 0xfffffff5u, 0x0000000au, 0x00120c0bu, 0x66d9f3dfu, 0x960bb7c5u, 0xcc83b7a7u, 0x363b9de5u, 0x04c9cf6du)
+ZKL_FR_CONST(fr_six_m, 0xfffffff3u, 0x0000000cu, 0x0015540du, 0xbf5eabd9u, 0x82c807bau, 0x66100797u, 0xe300a355u, 0x1cee80c6u)
+
 __device__ __forceinline__ bool fr_is_zero(const fr& a) {
     uint32_t x = a.v[0] | a.v[1] | a.v[2] | a.v[3] | a.v[4] | a.v[5] | a.v[6] | a.v[7];
     return x == 0;

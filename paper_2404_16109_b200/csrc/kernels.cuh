@@ -72,27 +72,38 @@ __device__ __forceinline__ uint32_t hash_fr(const fr& x) {
 }
 
 struct TableView {
-    const uint32_t* T;
-    const uint32_t* slots;
+    const uint32_t* T;       // SoA Montgomery
+    const uint4* Taos;       // AoS copy (2 x uint4 per entry) for one-sector key compares
+    const uint32_t* slots;   // index + 1, 0 = empty
     uint64_t N;
     uint32_t mask;
 };
 
-// index of x in T, or -1
+__device__ __forceinline__ bool aos_eq(const uint4* p, const fr& x) {
+    const uint4 a = __ldg(p), b = __ldg(p + 1);
+    return ((a.x ^ x.v[0]) | (a.y ^ x.v[1]) | (a.z ^ x.v[2]) | (a.w ^ x.v[3]) | (b.x ^ x.v[4]) | (b.y ^ x.v[5]) |
+            (b.z ^ x.v[6]) | (b.w ^ x.v[7])) == 0;
+}
+
+// index of x in T, or -1 (linear probing)
 __device__ __forceinline__ int64_t table_find(const TableView& tv, const fr& x) {
     uint32_t h = hash_fr(x) & tv.mask;
     for (;;) {
         uint32_t s = __ldg(tv.slots + h);
         if (s == 0) return -1;
-        uint64_t j = s - 1;
-        if (fr_eq(ld_fr(tv.T, tv.N, j), x)) return (int64_t)j;
+        if (aos_eq(tv.Taos + 2 * (uint64_t)(s - 1), x)) return (int64_t)(s - 1);
         h = (h + 1) & tv.mask;
     }
 }
 
-__global__ void k_table_copy(const uint32_t* __restrict__ src, uint64_t n, uint32_t* __restrict__ dst) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        st_fr(dst, n, i, ld_fr(src, n, i));
+__global__ void k_table_copy(const uint32_t* __restrict__ src, uint64_t n, uint32_t* __restrict__ dst,
+                             uint4* __restrict__ aos) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const fr x = ld_fr(src, n, i);
+        st_fr(dst, n, i, x);
+        aos[2 * i] = make_uint4(x.v[0], x.v[1], x.v[2], x.v[3]);
+        aos[2 * i + 1] = make_uint4(x.v[4], x.v[5], x.v[6], x.v[7]);
+    }
 }
 
 __global__ void k_table_insert(const uint32_t* __restrict__ T, uint64_t N, uint32_t* slots, uint32_t mask) {
@@ -112,9 +123,9 @@ __global__ void k_table_insert(const uint32_t* __restrict__ T, uint64_t N, uint3
 }
 
 // j is a duplicate iff its key's slot holds a smaller index; report the smallest such j.
-__global__ void k_table_dups(const uint32_t* __restrict__ T, uint64_t N, const uint32_t* slots, uint32_t mask,
-                             unsigned long long* err) {
-    TableView tv{T, slots, N, mask};
+__global__ void k_table_dups(const uint32_t* __restrict__ T, const uint4* __restrict__ aos, uint64_t N,
+                             const uint32_t* slots, uint32_t mask, unsigned long long* err) {
+    TableView tv{T, aos, slots, N, mask};
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < N; j += (uint64_t)gridDim.x * blockDim.x) {
         int64_t f = table_find(tv, ld_fr(T, N, j));
         if (f != (int64_t)j) atomic_min_i64(err, j);
@@ -122,15 +133,18 @@ __global__ void k_table_dups(const uint32_t* __restrict__ T, uint64_t N, const u
 }
 
 // ====================================================================== a3: multiplicities
-// Atomic-free histogram: per tile of 4096 lookups, index map (hash probe), block radix sort of the
-// indices, then per distinct index one read-modify-write of the CTA-private row:
-// heads subtract their sorted position, tails add theirs + 1 (two barrier-separated phases, each
-// touching one address per distinct key).  A column sum over the rows gives m.
+// Atomic-free histogram: per tile of 4096 lookups, index map (hash probe, 8 independent probes per thread
+// in flight), block radix sort of the indices (8-bit digits), then per distinct index one read-modify-
+// write of the CTA-private row: heads subtract their sorted position, tails add theirs + 1 (two
+// barrier-separated phases, each touching one address per distinct key).  A column sum gives m.
+// A lookup not in T reports its index (atomicMin on the error word, the error path only) and is
+// counted under key 0 — m is discarded on error.  Keys beyond n (a partial tile, n < 4096) take the
+// sentinel N, which sorts last and is not counted.
 constexpr int kHistThreads = 512;
 constexpr int kHistItems = 8;
 constexpr int kHistTile = kHistThreads * kHistItems;   // 4096
 
-__global__ void __launch_bounds__(kHistThreads)
+__global__ void __launch_bounds__(kHistThreads, 2)
 k_hist_rows(const uint32_t* __restrict__ S, uint64_t n, uint64_t global_offset, TableView tv, uint32_t* rows,
             int key_bits, unsigned long long* err) {
     typedef cub::BlockRadixSort<uint32_t, kHistThreads, kHistItems> Sort;
@@ -143,29 +157,46 @@ k_hist_rows(const uint32_t* __restrict__ S, uint64_t n, uint64_t global_offset, 
     for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) row[j] = 0;
     __syncthreads();
     const uint64_t ntiles = (n + kHistTile - 1) / kHistTile;
+    const bool vec_ok = (n & 3) == 0;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const uint64_t base = tile * kHistTile;
-        uint32_t keys[kHistItems];
+        fr x[kHistItems];
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
             const uint64_t i0 = base + 2048 * g + 4 * threadIdx.x;
-            fr x[4];
-            if (i0 + 3 < n && (n & 3) == 0) {
-                ld_fr4(S, n, i0, x);
+            if (vec_ok && i0 + 3 < n) {
+                fr q[4];
+                ld_fr4(S, n, i0, q);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) x[4 * g + j] = q[j];
             } else {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) x[q] = i0 + q < n ? ld_fr(S, n, i0 + q) : fr_zero();
+                for (int j = 0; j < 4; ++j) x[4 * g + j] = i0 + j < n ? ld_fr(S, n, i0 + j) : fr_zero();
             }
+        }
+        // first probe of all 8 keys in flight together
+        uint32_t h[kHistItems], slot[kHistItems], keys[kHistItems];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                uint32_t key = N;  // sentinel: not counted
-                if (i0 + q < n) {
-                    int64_t f = table_find(tv, x[q]);
-                    if (f < 0) atomic_min_i64(err, global_offset + i0 + q);
-                    else key = (uint32_t)f;
-                }
-                keys[4 * g + q] = key;
+        for (int q = 0; q < kHistItems; ++q) h[q] = hash_fr(x[q]) & tv.mask;
+#pragma unroll
+        for (int q = 0; q < kHistItems; ++q) slot[q] = __ldg(tv.slots + h[q]);
+#pragma unroll
+        for (int q = 0; q < kHistItems; ++q) {
+            const uint64_t i = base + 2048 * (q >> 2) + 4 * threadIdx.x + (q & 3);
+            bool ok = slot[q] != 0 && aos_eq(tv.Taos + 2 * (uint64_t)(slot[q] - 1), x[q]);
+            uint32_t key = slot[q] - 1;
+            if (!ok && slot[q] != 0) {                 // collision: keep probing
+                const int64_t f = table_find(tv, x[q]);
+                ok = f >= 0;
+                key = (uint32_t)f;
             }
+            if (i >= n) {
+                key = N;
+            } else if (!ok) {
+                atomic_min_i64(err, global_offset + i);
+                key = 0;
+            }
+            keys[q] = key;
         }
         __syncthreads();   // smem union reuse across tiles
         Sort(sm.sort).Sort(keys, 0, key_bits);
@@ -231,54 +262,52 @@ __device__ fr block_tree_down(const fr* tree, fr* inv) {
 constexpr int kInvThreads = 256;
 constexpr int kInvPer = 16;                         // elements per thread
 constexpr int kInvTile = kInvThreads * kInvPer;     // 4096 elements
-// thread t's chain: element e = 4g + j (g, j in 0..3) at tile offset 1024 g + 4 t + j
-
-// Forward pass: x = beta + S; per-thread prefix products stored in Abuf (slot of element e >= 1 holds
-// p_{e-1}, slot of e = 0 holds the thread's total); tile total -> totals[tile] (SoA, ntiles).
-__global__ void __launch_bounds__(kInvThreads)
-k_inv_fwd(const uint32_t* __restrict__ S, uint64_t n, const ProofScalars* __restrict__ sc, uint32_t* Abuf,
-          uint32_t* totals, uint64_t ntiles, uint64_t err_offset, unsigned long long* err) {
-    __shared__ fr tree[2 * kInvThreads];
-    const fr beta = sc->beta;
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint64_t base = tile * kInvTile;
-        fr p = fr_zero(), g0[4];
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-            const uint64_t i0 = base + 1024 * g + 4 * threadIdx.x;
-            fr x[4], slot[4];
-            ld_fr4(S, n, i0, x);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                x[j] = fr_add(x[j], beta);
-                if (fr_is_zero(x[j])) atomic_min_i64(err, err_offset + i0 + j);
-                slot[j] = p;                        // p_{e-1} (garbage for e = 0, replaced below)
-                p = (g == 0 && j == 0) ? x[j] : fr_mul(p, x[j]);
+// Hierarchical (barrier-free) batched inversion.  Level 0 holds the D_local values x = beta + S; level L+1
+// holds the per-thread chain products of level L (one per 16 elements).  Thread t of tile b owns the
+// chain of elements e = 2g + j (g in 0..7, j in 0..1) at tile offset 512 g + 2 t + j: each step is one
+// coalesced 64-bit access per limb plane, and both elements of a round-1 pair (2y, 2y+1), y = 256 g + t
+// within the tile, sit in the same thread.  Its chain product goes to next[256 b + t].
+//   forward : slot(e) = p_{e-1} = x_0 ... x_{e-1} for e >= 1 (slot(0) unused), next = p_15
+//   backward: given I = 1/p_15 (inverse of the next-level element), A_e = I p_{e-1}; I <- I x_e
+// The top level (<= 8192 values) is inverted by one block (k_batch_invert, one Fermat).
+template <bool LEVEL0>
+__global__ void __launch_bounds__(kInvThreads, 2)
+k_inv_fwd(const uint32_t* __restrict__ X, uint64_t n, const ProofScalars* __restrict__ sc, uint32_t* slots,
+          uint32_t* next, uint64_t nnext, uint64_t t0, uint64_t t1, uint64_t err_offset, unsigned long long* err) {
+    const fr beta = LEVEL0 ? sc->beta : fr_zero();
+    for (uint64_t tile = t0 + blockIdx.x; tile < t1; tile += gridDim.x) {
+        const uint64_t base = tile * kInvTile + 2 * threadIdx.x;
+        fr p = fr_zero();
+#pragma unroll 1
+        for (int g = 0; g < 8; ++g) {
+            const uint64_t i0 = base + 512 * g;
+            fr x[2];
+            ld_fr2(X, n, i0, x);
+            if (LEVEL0) {
+                x[0] = fr_add(x[0], beta);
+                x[1] = fr_add(x[1], beta);
+                if (fr_is_zero(x[0])) atomic_min_i64(err, err_offset + i0);
+                if (fr_is_zero(x[1])) atomic_min_i64(err, err_offset + i0 + 1);
             }
-            if (g == 0) {
-#pragma unroll
-                for (int j = 0; j < 4; ++j) g0[j] = slot[j];
-            } else {
-                st_fr4(Abuf, n, i0, slot);
-            }
+            const fr prev = p;                       // p_{2g-1}
+            p = (g == 0) ? x[0] : fr_mul(p, x[0]);   // p_{2g}
+            st_fr2(slots, n, i0, g == 0 ? p : prev, p);
+            p = fr_mul(p, x[1]);                     // p_{2g+1}
         }
-        g0[0] = p;   // thread total in the slot of element 0
-        st_fr4(Abuf, n, base + 4 * threadIdx.x, g0);
-        block_tree_up(tree, p);
-        if (threadIdx.x == 0) st_fr(totals, ntiles, tile, tree[1]);
-        __syncthreads();
+        st_fr(next, nnext, (tile - t0) * kInvThreads + threadIdx.x, p);
     }
 }
 
-// Inverts `count` values (SoA `vals`, stride `count`) into `out`: one block, chains of length
-// ceil(count / blockDim) per thread, one Fermat for the whole batch.
+// Inverts elements [i0, i1) of the SoA vector `vals` (stride `count`) into `out` (same layout): one
+// block, chains of ceil((i1 - i0) / blockDim) per thread, one Fermat for the whole batch.
 __global__ void __launch_bounds__(1024)
-k_batch_invert(const uint32_t* __restrict__ vals, uint64_t count, uint32_t* out) {
+k_batch_invert(const uint32_t* __restrict__ vals, uint64_t count, uint64_t i0, uint64_t i1, uint32_t* out) {
     extern __shared__ fr smem_fr[];
     fr* tree = smem_fr;
     fr* inv = smem_fr + 2 * blockDim.x;
-    const uint64_t per = (count + blockDim.x - 1) / blockDim.x;
-    const uint64_t lo = threadIdx.x * per, hi = min(lo + per, count);
+    const uint64_t len = i1 - i0;
+    const uint64_t per = (len + blockDim.x - 1) / blockDim.x;
+    const uint64_t lo = i0 + threadIdx.x * per, hi = min(lo + per, i1);
     fr p = fr_one();
     for (uint64_t i = lo; i < hi; ++i) {
         st_fr(out, count, i, p);                    // exclusive prefix
@@ -294,71 +323,57 @@ k_batch_invert(const uint32_t* __restrict__ vals, uint64_t count, uint32_t* out)
     }
 }
 
-// Backward pass: A = 1/(beta + S) over the tile, fused with the round-1 evaluation (a5):
-//   Hinf += W[y] (A_1 - A_0)(S_1 - S_0),  a0 += A_0,  a1 += A_1   per pair y = (2y, 2y+1).
+// Backward pass over tiles [t0, t1): slots (prefixes) -> inverses, in place.  Level 0 writes A = 1/(beta+S)
+// and fuses the round-1 evaluation (a5):
+//   Hinf += W[y] (A_1 - A_0)(S_1 - S_0),  a0 += A_0,  a1 += A_1   per pair y = (2y, 2y+1);
 // H0 = H1 = sum_y W[y] A_t (S_t + beta) = sum W = 1 globally (A (S + beta) = 1), no work.
-// W[y] = E_hi[tile] * E_lo[y mod 2048] (a tile is one group of 2048 pairs).
-__global__ void __launch_bounds__(kInvThreads)
-k_inv_bwd(const uint32_t* __restrict__ S, uint64_t n, const ProofScalars* __restrict__ sc, uint32_t* Abuf,
-          const uint32_t* __restrict__ totals_inv, uint64_t ntiles, const fr* __restrict__ elo,
-          const fr* __restrict__ ehi, int eval, fr* partials) {
-    __shared__ fr tree[2 * kInvThreads];
-    __shared__ fr inv[2 * kInvThreads];
-    const fr beta = sc->beta;
+// W[y] = E_hi[tile] * E_lo[y mod 2048] (a tile is one group of 2048 pairs).  Partial rows go to
+// row0 + blockIdx.x.
+template <bool LEVEL0>
+__global__ void __launch_bounds__(kInvThreads, 2)
+k_inv_bwd(const uint32_t* __restrict__ X, uint64_t n, const ProofScalars* __restrict__ sc, uint32_t* slots,
+          const uint32_t* __restrict__ next_inv, uint64_t nnext, uint64_t t0, uint64_t t1,
+          const fr* __restrict__ elo, const fr* __restrict__ ehi, fr* partials, int row0) {
+    const fr beta = LEVEL0 ? sc->beta : fr_zero();
+    const bool eval = LEVEL0 && partials != nullptr;
     fr hinf = fr_zero(), a0 = fr_zero(), a1 = fr_zero();
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint64_t base = tile * kInvTile;
-        fr g0[4];
-        ld_fr4(Abuf, n, base + 4 * threadIdx.x, g0);
-        block_tree_up(tree, g0[0]);
-        if (threadIdx.x == 0) inv[1] = ld_fr(totals_inv, ntiles, tile);
-        __syncthreads();
-        fr iv = block_tree_down(tree, inv);
+    for (uint64_t tile = t0 + blockIdx.x; tile < t1; tile += gridDim.x) {
+        const uint64_t base = tile * kInvTile + 2 * threadIdx.x;
+        fr iv = ld_fr(next_inv, nnext, (tile - t0) * kInvThreads + threadIdx.x);
         fr acc = fr_zero();
-#pragma unroll
-        for (int g = 3; g >= 0; --g) {
-            const uint64_t i0 = base + 1024 * g + 4 * threadIdx.x;
-            fr slot[4], x[4], A[4];
+#pragma unroll 1
+        for (int g = 7; g >= 0; --g) {
+            const uint64_t i0 = base + 512 * g;
+            fr slot[2], x[2], A0, A1;
+            ld_fr2(slots, n, i0, slot);
+            ld_fr2(X, n, i0, x);
+            A1 = fr_mul(iv, slot[1]);
+            iv = fr_mul(iv, LEVEL0 ? fr_add(x[1], beta) : x[1]);
             if (g == 0) {
-#pragma unroll
-                for (int j = 0; j < 4; ++j) slot[j] = g0[j];
+                A0 = iv;
             } else {
-                ld_fr4(Abuf, n, i0, slot);
+                A0 = fr_mul(iv, slot[0]);
+                iv = fr_mul(iv, LEVEL0 ? fr_add(x[0], beta) : x[0]);
             }
-            ld_fr4(S, n, i0, x);
-#pragma unroll
-            for (int j = 3; j >= 0; --j) {
-                if (g == 0 && j == 0) {
-                    A[0] = iv;
-                } else {
-                    A[j] = fr_mul(iv, slot[j]);
-                    iv = fr_mul(iv, fr_add(x[j], beta));
-                }
-            }
-            st_fr4(Abuf, n, i0, A);
+            st_fr2(slots, n, i0, A0, A1);
             if (eval) {
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const fr dA = fr_sub(A[2 * h + 1], A[2 * h]);
-                    const fr dS = fr_sub(x[2 * h + 1], x[2 * h]);
-                    const uint32_t ylo = 512 * g + 2 * threadIdx.x + h;
-                    acc = fr_add(acc, fr_mul(elo[ylo], fr_mul(dA, dS)));
-                    a0 = fr_add(a0, A[2 * h]);
-                    a1 = fr_add(a1, A[2 * h + 1]);
-                }
+                const fr dA = fr_sub(A1, A0), dS = fr_sub(x[1], x[0]);
+                acc = fr_add(acc, fr_mul(elo[256 * g + threadIdx.x], fr_mul(dA, dS)));
+                a0 = fr_add(a0, A0);
+                a1 = fr_add(a1, A1);
             }
         }
         if (eval) hinf = fr_add(hinf, fr_mul(ehi[tile], acc));
-        __syncthreads();
     }
     if (eval) {
         __shared__ fr scratch[3 * (kInvThreads / 32)];
         fr v[3] = {hinf, a0, a1};
         block_sum_fr<3>(v, scratch);
         if (threadIdx.x == 0) {
-            partials[SLOT_HINF * kMaxBlocks + blockIdx.x] = v[0];
-            partials[SLOT_A0 * kMaxBlocks + blockIdx.x] = v[1];
-            partials[SLOT_A1 * kMaxBlocks + blockIdx.x] = v[2];
+            const int row = row0 + blockIdx.x;
+            partials[SLOT_HINF * kMaxBlocks + row] = v[0];
+            partials[SLOT_A0 * kMaxBlocks + row] = v[1];
+            partials[SLOT_A1 * kMaxBlocks + row] = v[2];
         }
     }
 }
@@ -370,11 +385,12 @@ k_inv_bwd(const uint32_t* __restrict__ S, uint64_t n, const ProofScalars* __rest
 // each thread G/256 of them, accumulating E_lo-weighted sums that are scaled by E_hi once per group.
 constexpr int kRoundThreads = 256;
 
-template <bool FOLD>
-__global__ void __launch_bounds__(kRoundThreads)
+template <bool FOLD, bool DIRECT>
+__global__ void __launch_bounds__(kRoundThreads, 2)
 k_round(const uint32_t* __restrict__ Aold, const uint32_t* __restrict__ Sold, uint64_t nold,
         uint32_t* __restrict__ Anew, uint32_t* __restrict__ Snew, const ProofScalars* __restrict__ sc, int k,
-        const fr* __restrict__ elo, const fr* __restrict__ ehi, int gbits, int direct_h1, fr* partials) {
+        const fr* __restrict__ elo, const fr* __restrict__ ehi, int gbits, fr* partials) {
+    constexpr bool direct_h1 = DIRECT;
     const fr beta = sc->beta;
     const fr rk = FOLD ? sc->r[k - 2] : fr_zero();
     const uint64_t npairs = FOLD ? nold / 4 : nold / 2;   // pairs of the round being evaluated
@@ -388,14 +404,19 @@ k_round(const uint32_t* __restrict__ Aold, const uint32_t* __restrict__ Sold, ui
             const uint64_t y = (grp << gbits) + yl;
             fr A0, A1, S0, S1;
             if (FOLD) {
-                fr a[4], s[4];
-                ld_fr4(Aold, nold, 4 * y, a);
-                ld_fr4(Sold, nold, 4 * y, s);
-                A0 = fr_add(a[0], fr_mul(rk, fr_sub(a[1], a[0])));
-                A1 = fr_add(a[2], fr_mul(rk, fr_sub(a[3], a[2])));
-                S0 = fr_add(s[0], fr_mul(rk, fr_sub(s[1], s[0])));
-                S1 = fr_add(s[2], fr_mul(rk, fr_sub(s[3], s[2])));
+                {
+                    fr a[4];
+                    ld_fr4(Aold, nold, 4 * y, a);
+                    A0 = fr_add(a[0], fr_mul(rk, fr_sub(a[1], a[0])));
+                    A1 = fr_add(a[2], fr_mul(rk, fr_sub(a[3], a[2])));
+                }
                 st_fr2(Anew, nnew, 2 * y, A0, A1);
+                {
+                    fr s[4];
+                    ld_fr4(Sold, nold, 4 * y, s);
+                    S0 = fr_add(s[0], fr_mul(rk, fr_sub(s[1], s[0])));
+                    S1 = fr_add(s[2], fr_mul(rk, fr_sub(s[3], s[2])));
+                }
                 st_fr2(Snew, nnew, 2 * y, S0, S1);
             } else {
                 fr a[2], s[2];
@@ -694,48 +715,97 @@ __device__ __forceinline__ zkl_fr to_canon(const fr& m) {
     return z;
 }
 
-// Round derivation (a7): g_k(t) = alpha1 C_k l_c(t) H(t) + a(t) + tab_k(t), c = d - k,
-// C_k = prod_{j<k} l_{d-j}(r_j);  H(1) derived from g_k(0) + g_k(1) = g_{k-1}(r_{k-1}) when the
-// round did not sum it directly;  H(2) = -H0 + 2 H1 + 2 Hinf, H(3) = -2 H0 + 3 H1 + 6 Hinf.
-// ranks: D-side sums of local rounds are summed over `nranks` rows of `gathered`; rounds > dl use
+// Per-round constants that depend only on the challenges (a7), computed on the side stream at the start
+// of a proof: C_k = prod_{j<k} l_{d-j}(r_j), cl_t = alpha1 C_k l_c(t) (c = d - k), the inverse of
+// cl_1 = alpha1 C_k u_c (one batch inversion, one Fermat), the Lagrange basis L_t(r_k) on {0,1,2,3},
+// and 2^{-(k-n)} for the rounds after the table coordinates are bound.
+struct RoundConst {
+    fr cl[4];
+    fr inv_cl1;   // 0 when cl_1 = 0
+    fr L[4];
+    fr tscale;
+};
+
+__global__ void k_round_consts(const ProofScalars* __restrict__ sc, int d, int n, RoundConst* rc) {
+    __shared__ fr C[kMaxRounds + 1];
+    const int k = threadIdx.x + 1;   // one thread per round
+    if (threadIdx.x == 0) {
+        fr c = fr_one();
+        for (int j = 1; j <= d; ++j) {
+            C[j] = c;
+            const fr u = sc->u[d - j];
+            const fr l0 = fr_sub(fr_one(), u);
+            c = fr_mul(c, fr_add(l0, fr_mul(sc->r[j - 1], fr_sub(u, l0))));
+        }
+    }
+    __syncthreads();
+    if (k <= d) {
+        const fr one = fr_one(), two = fr_two_m(), three = fr_three_m();
+        const fr u = sc->u[d - k];
+        const fr coef = fr_mul(sc->alpha1, C[k]);
+        RoundConst& q = rc[k - 1];
+        q.cl[0] = fr_mul(coef, fr_sub(one, u));
+        q.cl[1] = fr_mul(coef, u);
+        q.cl[2] = fr_mul(coef, fr_sub(fr_mul(three, u), one));
+        q.cl[3] = fr_mul(coef, fr_sub(fr_mul(fr_five_m(), u), two));
+        const fr x = sc->r[k - 1];
+        const fr xm1 = fr_sub(x, one), xm2 = fr_sub(x, two), xm3 = fr_sub(x, three);
+        const fr inv2 = fr_inv2_m(), inv6 = fr_inv6_m();
+        q.L[0] = fr_neg(fr_mul(fr_mul(fr_mul(xm1, xm2), xm3), inv6));
+        q.L[1] = fr_mul(fr_mul(fr_mul(x, xm2), xm3), inv2);
+        q.L[2] = fr_neg(fr_mul(fr_mul(fr_mul(x, xm1), xm3), inv2));
+        q.L[3] = fr_mul(fr_mul(fr_mul(x, xm1), xm2), inv6);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // batch inversion of the nonzero cl_1 (one Fermat) and the 2^{-(k-n)} scales
+        fr pre[kMaxRounds], acc = fr_one();
+        for (int j = 0; j < d; ++j) {
+            pre[j] = acc;
+            if (!fr_is_zero(rc[j].cl[1])) acc = fr_mul(acc, rc[j].cl[1]);
+        }
+        fr iv = fr_inv(acc);
+        for (int j = d - 1; j >= 0; --j) {
+            if (fr_is_zero(rc[j].cl[1])) {
+                rc[j].inv_cl1 = fr_zero();
+            } else {
+                rc[j].inv_cl1 = fr_mul(iv, pre[j]);
+                iv = fr_mul(iv, rc[j].cl[1]);
+            }
+        }
+        fr ts = fr_one();
+        for (int j = 1; j <= d; ++j) {
+            if (j > n) ts = fr_mul(ts, fr_inv2_m());
+            rc[j - 1].tscale = ts;
+        }
+    }
+}
+
+// Round derivation (a7): g_k(t) = cl_t H(t) + a(t) + tab_k(t).  H(1) is derived from
+// g_k(0) + g_k(1) = g_{k-1}(r_{k-1}) when the round did not sum it directly, H(2) = -H0 + 2 H1 + 2 Hinf,
+// H(3) = -2 H0 + 3 H1 + 6 Hinf.  Every quantity is affine in the running claim c_{k-1}: each thread
+// builds its round's affine forms in parallel, thread 0 runs the chain c_k = alpha_k c_{k-1} + beta_k
+// (one multiplication per round), then the threads finish their rounds.
+// D-side sums of local rounds are summed over the `nranks` rows of `gathered`; rounds > dl use
 // `repl_sums` (replicated, already global).  fin_loc: A(v), S(v); tfin: B, T, M, E2 at v'.
+struct Affine {
+    fr a, b;   // a * c + b
+};
+
 __global__ void k_derive(const fr* __restrict__ gathered, int nranks, int dl, const fr* __restrict__ repl_sums,
                          const RoundDesc* __restrict__ rounds, const fr* __restrict__ tab_sums,
-                         const ProofScalars* __restrict__ sc, int d, int n, int variant, int prove_mode,
-                         const fr* __restrict__ fin_loc, const fr* __restrict__ tfin, ProofOut* out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    const fr one = fr_one(), two = fr_small(2), three = fr_small(3), five = fr_small(5), six = fr_small(6);
-    // ---- the divisors: 2, 6 and coef_k * u_c (k where H(1) is derived); one Fermat for all
-    fr C[kMaxRounds + 1], dv[kMaxRounds + 2], pre[kMaxRounds + 2];
-    C[0] = one;
-    for (int k = 1; k <= d; ++k) {
-        const fr u = sc->u[d - k];
-        const fr l0 = fr_sub(one, u);
-        C[k] = fr_mul(C[k - 1], fr_add(l0, fr_mul(sc->r[k - 1], fr_sub(u, l0))));   // C_{k+1} at C[k]
-    }
-    dv[0] = two;
-    dv[1] = six;
-    for (int k = 1; k <= d; ++k) {
-        const fr q = fr_mul(fr_mul(sc->alpha1, C[k - 1]), sc->u[d - k]);
-        dv[k + 1] = fr_is_zero(q) ? one : q;
-    }
-    const int nd = d + 2;
-    fr acc = one;
-    for (int i = 0; i < nd; ++i) { pre[i] = acc; acc = fr_mul(acc, dv[i]); }
-    fr iv = fr_inv(acc);
-    for (int i = nd - 1; i >= 0; --i) { const fr t = fr_mul(iv, pre[i]); iv = fr_mul(iv, dv[i]); dv[i] = t; }
-    const fr inv2 = dv[0], inv6 = dv[1];
-    // ---- table constant tau once all table coordinates are bound
-    const fr tb = tfin[0], tt = tfin[1], tm = tfin[2], te = tfin[3];
-    fr tau = (variant == ZKL_VARIANT_PAPER)
-                 ? fr_mul(tb, fr_sub(fr_mul(fr_mul(sc->alpha2, te), fr_add(tt, sc->beta)), tm))
-                 : fr_sub(fr_mul(fr_mul(sc->alpha2, te), fr_sub(fr_mul(tb, fr_add(tt, sc->beta)), tm)), tb);
-    fr claim = (variant == ZKL_VARIANT_PAPER) ? fr_add(sc->alpha1, sc->alpha2) : sc->alpha1;
-    fr tscale = one;
-    for (int k = 1; k <= d; ++k) {
+                         const ProofScalars* __restrict__ sc, const RoundConst* __restrict__ rc, int d, int n,
+                         int variant, int prove_mode, const fr* __restrict__ fin_loc, const fr* __restrict__ tfin,
+                         ProofOut* out) {
+    __shared__ Affine form[kMaxRounds][4];    // g_k(t) as affine functions of c_{k-1}
+    __shared__ Affine step[kMaxRounds];
+    __shared__ fr claim[kMaxRounds + 1];
+    const int k = threadIdx.x + 1;
+    const fr one = fr_one(), zero = fr_zero();
+    if (k <= d) {
         fr s[5];
         for (int q = 0; q < 5; ++q) {
-            s[q] = fr_zero();
+            s[q] = zero;
             if (k <= dl) {
                 for (int p = 0; p < nranks; ++p)
                     s[q] = fr_add(s[q], gathered[((uint64_t)p * dl + (k - 1)) * kSlots + q]);
@@ -743,55 +813,71 @@ __global__ void k_derive(const fr* __restrict__ gathered, int nranks, int dl, co
                 s[q] = repl_sums[(k - dl - 1) * kSlots + q];
             }
         }
+        const RoundConst q = rc[k - 1];
         fr tab[4];
         if (k <= n) {
-            for (int q = 0; q < 4; ++q) tab[q] = tab_sums[(k - 1) * 4 + q];
+            for (int t = 0; t < 4; ++t) tab[t] = tab_sums[(k - 1) * 4 + t];
         } else {
-            tscale = fr_mul(tscale, inv2);
-            const fr c = fr_mul(tau, tscale);
-            for (int q = 0; q < 4; ++q) tab[q] = c;
+            const fr tb = tfin[0], tt = tfin[1], tm = tfin[2], te = tfin[3];
+            const fr tau = (variant == ZKL_VARIANT_PAPER)
+                ? fr_mul(tb, fr_sub(fr_mul(fr_mul(sc->alpha2, te), fr_add(tt, sc->beta)), tm))
+                : fr_sub(fr_mul(fr_mul(sc->alpha2, te), fr_sub(fr_mul(tb, fr_add(tt, sc->beta)), tm)), tb);
+            const fr c = fr_mul(tau, q.tscale);
+            for (int t = 0; t < 4; ++t) tab[t] = c;
         }
-        const fr u = sc->u[d - k];
-        const fr l0 = fr_sub(one, u), l1 = u;
-        const fr l2 = fr_sub(fr_mul(three, u), one);
-        const fr l3 = fr_sub(fr_mul(five, u), two);
-        const fr coef = fr_mul(sc->alpha1, C[k - 1]);
-        fr H0 = s[SLOT_H0], H1 = s[SLOT_H1];
-        const fr Hinf = s[SLOT_HINF], a0 = s[SLOT_A0], a1 = s[SLOT_A1];
-        if (k == 1 && prove_mode) { H0 = one; H1 = one; }
-        const fr g0 = fr_add(fr_add(fr_mul(fr_mul(coef, l0), H0), a0), tab[0]);
-        fr g1;
-        const bool direct = (k == 1) || rounds[k - 1].direct_h1 || fr_is_zero(fr_mul(coef, l1));
+        fr H0 = s[SLOT_H0];
+        const fr H1d = s[SLOT_H1], Hinf = s[SLOT_HINF], a0 = s[SLOT_A0], a1 = s[SLOT_A1];
+        fr H1c = H1d;
+        if (k == 1 && prove_mode) { H0 = one; H1c = one; }
+        const fr g0 = fr_add(fr_add(fr_mul(q.cl[0], H0), a0), tab[0]);
+        const bool direct = (k == 1) || rounds[k - 1].direct_h1 || fr_is_zero(q.cl[1]);
+        // H1 = p1 c + q1
+        fr p1 = zero, q1 = H1c;
+        Affine g1;
         if (direct) {
-            g1 = fr_add(fr_add(fr_mul(fr_mul(coef, l1), H1), a1), tab[1]);
+            g1 = Affine{zero, fr_add(fr_add(fr_mul(q.cl[1], H1c), a1), tab[1])};
         } else {
-            g1 = fr_sub(claim, g0);
-            H1 = fr_mul(fr_sub(fr_sub(g1, a1), tab[1]), dv[k + 1]);   // / (coef u_c)
+            p1 = q.inv_cl1;
+            q1 = fr_neg(fr_mul(fr_add(fr_add(g0, a1), tab[1]), q.inv_cl1));
+            g1 = Affine{one, fr_neg(g0)};
         }
-        const fr H2 = fr_add(fr_sub(fr_add(H1, H1), H0), fr_add(Hinf, Hinf));
-        const fr H3 = fr_add(fr_sub(fr_mul(three, H1), fr_add(H0, H0)), fr_mul(six, Hinf));
+        const fr three = fr_three_m(), six = fr_six_m();
         const fr da = fr_sub(a1, a0);
-        const fr g2 = fr_add(fr_add(fr_mul(fr_mul(coef, l2), H2), fr_add(a0, fr_add(da, da))), tab[2]);
-        const fr g3 = fr_add(fr_add(fr_mul(fr_mul(coef, l3), H3), fr_add(a0, fr_mul(three, da))), tab[3]);
-        out->evals[k - 1][0] = to_canon(g0);
-        out->evals[k - 1][1] = to_canon(g1);
-        out->evals[k - 1][2] = to_canon(g2);
-        out->evals[k - 1][3] = to_canon(g3);
-        // claim_k = g_k(r_k), Lagrange on {0,1,2,3}:
-        //  L0 = -(x-1)(x-2)(x-3)/6, L1 = x(x-2)(x-3)/2, L2 = -x(x-1)(x-3)/2, L3 = x(x-1)(x-2)/6
-        const fr x = sc->r[k - 1];
-        const fr xm1 = fr_sub(x, one), xm2 = fr_sub(x, two), xm3 = fr_sub(x, three);
-        const fr L0 = fr_neg(fr_mul(fr_mul(fr_mul(xm1, xm2), xm3), inv6));
-        const fr L1 = fr_mul(fr_mul(fr_mul(x, xm2), xm3), inv2);
-        const fr L2 = fr_neg(fr_mul(fr_mul(fr_mul(x, xm1), xm3), inv2));
-        const fr L3 = fr_mul(fr_mul(fr_mul(x, xm1), xm2), inv6);
-        claim = fr_add(fr_add(fr_mul(g0, L0), fr_mul(g1, L1)), fr_add(fr_mul(g2, L2), fr_mul(g3, L3)));
+        // H2 = -H0 + 2 H1 + 2 Hinf ; H3 = -2 H0 + 3 H1 + 6 Hinf
+        const Affine H2{fr_add(p1, p1), fr_add(fr_sub(fr_add(q1, q1), H0), fr_add(Hinf, Hinf))};
+        const Affine H3{fr_mul(three, p1), fr_add(fr_sub(fr_mul(three, q1), fr_add(H0, H0)), fr_mul(six, Hinf))};
+        const Affine g2{fr_mul(q.cl[2], H2.a), fr_add(fr_add(fr_mul(q.cl[2], H2.b), fr_add(a0, fr_add(da, da))), tab[2])};
+        const Affine g3{fr_mul(q.cl[3], H3.a), fr_add(fr_add(fr_mul(q.cl[3], H3.b), fr_add(a0, fr_mul(three, da))), tab[3])};
+        form[k - 1][0] = Affine{zero, g0};
+        form[k - 1][1] = g1;
+        form[k - 1][2] = g2;
+        form[k - 1][3] = g3;
+        // c_k = sum_t g_t L_t
+        step[k - 1] = Affine{fr_add(fr_add(fr_mul(g1.a, q.L[1]), fr_mul(g2.a, q.L[2])), fr_mul(g3.a, q.L[3])),
+                             fr_add(fr_add(fr_mul(g0, q.L[0]), fr_mul(g1.b, q.L[1])),
+                                    fr_add(fr_mul(g2.b, q.L[2]), fr_mul(g3.b, q.L[3])))};
     }
-    out->finals[0] = to_canon(fin_loc[0]);
-    out->finals[1] = to_canon(fin_loc[1]);
-    out->finals[2] = to_canon(tb);
-    out->finals[3] = to_canon(tt);
-    out->finals[4] = to_canon(tm);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        fr c = (variant == ZKL_VARIANT_PAPER) ? fr_add(sc->alpha1, sc->alpha2) : sc->alpha1;
+        for (int j = 0; j < d; ++j) {
+            claim[j] = c;
+            c = fr_add(fr_mul(step[j].a, c), step[j].b);
+        }
+        claim[d] = c;
+    }
+    __syncthreads();
+    if (k <= d) {
+        const fr c = claim[k - 1];
+        for (int t = 0; t < 4; ++t) out->evals[k - 1][t] = to_canon(fr_add(fr_mul(form[k - 1][t].a, c), form[k - 1][t].b));
+    }
+    if (threadIdx.x == 0) {
+        out->finals[0] = to_canon(fin_loc[0]);
+        out->finals[1] = to_canon(fin_loc[1]);
+        out->finals[2] = to_canon(tfin[0]);
+        out->finals[3] = to_canon(tfin[1]);
+        out->finals[4] = to_canon(tfin[2]);
+    }
 }
 
 // beta + T_j (zero check: DIV_ZERO_T) -> x (SoA), for the table-side batch inversion

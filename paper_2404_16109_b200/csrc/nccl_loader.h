@@ -117,14 +117,12 @@ int zkl_dist_allreduce_u32(zkl_ctx* ctx, uint32_t* buf, uint64_t n) {
 
 // min over ranks of a host u64 (uses the pinned host page + a device word)
 int zkl_dist_min_u64(zkl_ctx* ctx, unsigned long long* v) {
-    unsigned long long* d = nullptr;
-    if (cudaMallocAsync((void**)&d, sizeof(*d), ctx->stream) != cudaSuccess) return ZKL_E_CUDA;
+    unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->dscratch + 16);
     unsigned long long* h = reinterpret_cast<unsigned long long*>((uint8_t*)ctx->host_out + 61000);
     *h = *v;
     cudaMemcpyAsync(d, h, sizeof(*d), cudaMemcpyHostToDevice, ctx->stream);
     NCCL_TRY(ctx, nccl().AllReduce(d, d, 1, ncclUint64, ncclMin, (ncclComm_t)ctx->nccl_comm, ctx->stream));
     cudaMemcpyAsync(h, d, sizeof(*d), cudaMemcpyDeviceToHost, ctx->stream);
-    cudaFreeAsync(d, ctx->stream);
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return ZKL_E_CUDA;
     *v = *h;
     return ZKL_OK;

@@ -86,6 +86,20 @@ __global__ void k_iadd(uint32_t* out, int iters) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// single-thread latency of a dependent chain of fr_mul, and of fr_inv
+__global__ void k_lat(fr* out, int iters, unsigned long long* cyc) {
+    fr x = fr_r2(), y = fr_one();
+    y.v[0] ^= threadIdx.x;
+    unsigned long long c0 = clock64();
+    for (int i = 0; i < iters; ++i) x = fr_mul(x, y);
+    unsigned long long c1 = clock64();
+    fr z = fr_inv(x);
+    unsigned long long c2 = clock64();
+    out[0] = fr_add(x, z);
+    cyc[0] = c1 - c0;
+    cyc[1] = c2 - c1;
+}
+
 static double mhz_from_clk() {
     unsigned long long h[4];
     cudaMemcpyFromSymbol(h, g_clk, sizeof(h));
@@ -126,6 +140,17 @@ int main() {
     timeit("imad_lo", k_imad, (uint32_t*)buf, sms * 8, 256, 20000, 8, false);
     timeit("imad_wide", k_imadwide, (unsigned long long*)buf, sms * 8, 256, 20000, 8, false);
     timeit("iadd", k_iadd, (uint32_t*)buf, sms * 8, 256, 20000, 16, false);
+    {
+        unsigned long long* cyc;
+        CK(cudaMalloc(&cyc, 16));
+        k_lat<<<1, 1>>>((fr*)buf, 1000, cyc);
+        CK(cudaDeviceSynchronize());
+        k_lat<<<1, 1>>>((fr*)buf, 1000, cyc);
+        CK(cudaDeviceSynchronize());
+        unsigned long long h[2];
+        CK(cudaMemcpy(h, cyc, 16, cudaMemcpyDeviceToHost));
+        printf("{\"bench\": \"latency\", \"frmul_cycles\": %.1f, \"frinv_cycles\": %llu}\n", h[0] / 1000.0, h[1]);
+    }
     for (int occ : {2, 4, 8}) {
         timeit("frmul_ilp1", k_frmul<1>, (fr*)buf, sms * occ, 256, 2000, 1, true);
         timeit("frmul_ilp2", k_frmul<2>, (fr*)buf, sms * occ, 256, 1000, 2, true);
