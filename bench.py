@@ -220,8 +220,9 @@ def main():
         e0.record(stream)
         for _ in range(args.steps):
             pf = step(xd, yd, txd, tyd)
-            for name, ms in ctx.profile_read():
-                kern.setdefault(name, []).append(ms)
+            for name, kms, _, tag in ctx.profile_read(with_start=True):
+                if tag == 0:    # kernels on the critical (ctx) stream; side/aux launches overlap it
+                    kern.setdefault(name, []).append(kms)
         e1.record(stream)
         torch.cuda.synchronize(dev)
     barrier()

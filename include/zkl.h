@@ -96,10 +96,12 @@ int zkl_ctx_set_workspace(zkl_ctx* ctx, void* device_ptr, size_t bytes);
 uint64_t zkl_ctx_launch_count(const zkl_ctx* ctx);
 /* Per-launch timing: when on, every launch is bracketed by CUDA events on its stream (<= 256 launches
  * are recorded, then recording stops).  zkl_ctx_profile_read synchronizes, writes up to `cap` kernel names
- * (name_len bytes each, NUL-terminated), durations in ms and (if start_ms != NULL) start times relative to
- * the first recorded launch, returns the count, and clears the record. */
+ * (name_len bytes each, NUL-terminated), durations in ms, (if non-NULL) start times relative to the first
+ * recorded launch and the stream of each launch (0 = the ctx stream, 1 = table-side stream, 2 = aux
+ * stream), returns the count, and clears the record. */
 int zkl_ctx_set_profiling(zkl_ctx* ctx, int on);
-int zkl_ctx_profile_read(zkl_ctx* ctx, char* names, int name_len, float* ms, float* start_ms, int cap);
+int zkl_ctx_profile_read(zkl_ctx* ctx, char* names, int name_len, float* ms, float* start_ms, int* stream_tag,
+                         int cap);
 
 /* ---------------------------------------------------------------- boundary encode (a1) */
 /* canonical 32-byte LE elements (host or device, AoS) -> dst (SoA Montgomery).  E_NONCANONICAL(i). */

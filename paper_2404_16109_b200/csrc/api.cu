@@ -108,6 +108,7 @@ struct Plan {
     EqJob jobs[2 * kMaxRounds];
     int njobs;
     uint64_t arena;
+    uint64_t part_total;
     uint64_t ntiles;     // inversion tiles (Dp / 4096)
     int nhalves;
     InvPlan inv[2];      // D side, one hierarchy per half
@@ -116,7 +117,7 @@ struct Plan {
     int hist_rows;
     // workspace offsets
     size_t o_out, o_sc, o_err, o_rounds, o_jobs, o_chal, o_part, o_tpart, o_tnb, o_rank, o_gath, o_repl, o_tsum,
-        o_fin, o_tfin, o_gfin, o_rc, o_arena, o_hist, o_tot, o_totinv, o_A, o_A1, o_S1, o_A2, o_S2, o_tB, o_tX, o_tM,
+        o_fin, o_tfin, o_gfin, o_rc, o_arena, o_hist, o_keys, o_tot, o_totinv, o_A, o_A1, o_S1, o_A2, o_S2, o_tB, o_tX, o_tM,
         o_tE, o_tp[2][4], total;
 };
 
@@ -152,7 +153,7 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
         int k = 1;
         // round 1: inversion tiles (prove) or k_round<false> (sumcheck)
         if (prove_mode) {
-            choose_round(p, 1, p.Dp / 2, 11, p.inv_blocks);
+            choose_round(p, 1, p.Dp / 2, 11, (int)p.ntiles);   // one partial row per inversion tile
         }
         for (k = 1; k <= p.dl; ++k) {
             const uint64_t nk = p.Dp >> (k - 1);   // elements at round k
@@ -202,6 +203,13 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
     }
     p.njobs = nj;
     p.arena = off;
+    // ---- partial-sum rows per round: [slot][row]
+    uint64_t prow = 0;
+    for (int k = 1; k <= p.d; ++k) {
+        p.rd[k - 1].part_base = prow;
+        prow += (uint64_t)kSlots * std::max<uint32_t>(1, p.rd[k - 1].nblocks);
+    }
+    p.part_total = prow;
     // ---- table rounds
     for (int k = 1; k <= p.n; ++k) p.tnb[k - 1] = grid_for(N >> k, 256, kMaxBlocks);
     // ---- workspace layout
@@ -213,7 +221,7 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
     p.o_rounds = take(sizeof(RoundDesc) * kMaxRounds);
     p.o_jobs = take(sizeof(EqJob) * 2 * kMaxRounds);
     p.o_chal = take(sizeof(zkl_fr) * (3 + 2 * kMaxRounds));
-    p.o_part = take(sizeof(fr) * (size_t)kMaxRounds * kSlots * kMaxBlocks);
+    p.o_part = take(sizeof(fr) * p.part_total);
     p.o_tpart = take(sizeof(fr) * (size_t)kMaxRounds * 4 * kMaxBlocks);
     p.o_tnb = take(sizeof(uint32_t) * kMaxRounds);
     p.o_rank = take(sizeof(fr) * kMaxRounds * kSlots);
@@ -226,6 +234,7 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
     p.o_rc = take(sizeof(RoundConst) * kMaxRounds);
     p.o_arena = take(sizeof(fr) * p.arena);
     p.o_hist = take(sizeof(uint32_t) * (size_t)p.hist_rows * N);
+    p.o_keys = take(sizeof(uint32_t) * std::max<uint64_t>(p.Dp, 4));
     p.o_tot = take(soa_bytes(p.ntiles));
     p.o_totinv = take(soa_bytes(p.ntiles));
     p.o_A = take(soa_bytes(p.Dp));
@@ -314,7 +323,7 @@ int sync_stream(zkl_ctx* ctx) {
 int inv_forward(zkl_ctx* ctx, const InvPlan& ip, const uint32_t* X0, uint64_t n0total, uint32_t* slots0,
                 const ProofScalars* sc, uint64_t err_off, unsigned long long* err, cudaStream_t s0, cudaStream_t s1,
                 cudaEvent_t ev) {
-    const unsigned nb0 = (unsigned)std::min<uint64_t>(ip.t1 - ip.t0, kSMs * 2);
+    const unsigned nb0 = (unsigned)(ip.t1 - ip.t0);   // one block per tile
     LAUNCH(ctx, k_inv_fwd<true>, nb0, kInvThreads, 0, s0, X0, n0total, sc, slots0, at<uint32_t>(ctx, ip.o_val[1]),
            ip.n[1], ip.t0, ip.t1, err_off, err);
     if (s1 != s0) {
@@ -336,18 +345,18 @@ int inv_forward(zkl_ctx* ctx, const InvPlan& ip, const uint32_t* X0, uint64_t n0
         const uint32_t* ninv = L == ip.nlev ? at<uint32_t>(ctx, ip.o_topinv) : at<uint32_t>(ctx, ip.o_slot[L + 1]);
         LAUNCH(ctx, k_inv_bwd<false>, (unsigned)std::min<uint64_t>(tiles, kSMs * 2), kInvThreads, 0, s1,
                at<uint32_t>(ctx, ip.o_val[L]), ip.n[L], sc, at<uint32_t>(ctx, ip.o_slot[L]), ninv, ip.n[L + 1],
-               (uint64_t)0, tiles, (const fr*)nullptr, (const fr*)nullptr, (fr*)nullptr, 0);
+               (uint64_t)0, tiles, (const fr*)nullptr, (const fr*)nullptr, (fr*)nullptr, 0, 0);
     }
     return ZKL_OK;
 }
 
 // Level-0 backward pass on s0 (after the upper levels on s1 completed: caller orders via events).
 int inv_backward0(zkl_ctx* ctx, const InvPlan& ip, const uint32_t* X0, uint64_t n0total, uint32_t* slots0,
-                  const ProofScalars* sc, const fr* elo, const fr* ehi, fr* partials, int row0, cudaStream_t s0) {
-    const unsigned nb0 = (unsigned)std::min<uint64_t>(ip.t1 - ip.t0, kSMs * 2);
+                  const ProofScalars* sc, const fr* elo, const fr* ehi, fr* partials, int rows, cudaStream_t s0) {
+    const unsigned nb0 = (unsigned)(ip.t1 - ip.t0);   // one block per tile; partial row = tile index
     const uint32_t* ninv = ip.nlev >= 1 ? at<uint32_t>(ctx, ip.o_slot[1]) : at<uint32_t>(ctx, ip.o_topinv);
     LAUNCH(ctx, k_inv_bwd<true>, nb0, kInvThreads, 0, s0, X0, n0total, sc, slots0, ninv, ip.n[1], ip.t0, ip.t1, elo,
-           ehi, partials, row0);
+           ehi, partials, (int)ip.t0, rows);
     return ZKL_OK;
 }
 
@@ -479,6 +488,7 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
     const uint64_t errS_off = (uint64_t)p.rank * p.Dp;
     const size_t tail_smem = (2 * kTailMax + 4 * kTailThreads) * sizeof(fr) + 5 * (kTailThreads / 32) * sizeof(fr);
     int rounds_nb0 = -1;   // round-1 partial rows written by the inversion (prove mode)
+    bool r1_reduced = false;
     if (p.small) {
         LAUNCH(ctx, k_tail, 1, kTailThreads, tail_smem, s, A1in, S1in, p.Dp, 0, a.prove_mode ? 1 : 0, Abuf,
                errS_off, err, sc, 1, p.dl, rounds, arena, partials, fin);
@@ -488,28 +498,31 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
             // half h run on the aux stream while the main stream does the level-0 forward pass of the other
             // half (h = 0) or the level-0 backward pass of half 0 (h = 1), hiding their latency.
             const int halves = p.nhalves;
-            int nb[2] = {0, 0}, row0[2] = {0, 0};
             for (int h = 0; h < halves; ++h) {
-                nb[h] = (int)std::min<uint64_t>(p.inv[h].t1 - p.inv[h].t0, kSMs * 2);
                 if ((st = inv_forward(ctx, p.inv[h], a.S.limbs, p.Dp, Abuf, sc, errS_off, err, s, ctx->aux,
                                       ctx->ev_fwd[h])))
                     return st;
                 CUDA_TRY(ctx, cudaEventRecord(ctx->ev_mid[h], ctx->aux));
             }
-            if (halves == 2) row0[1] = nb[0];
             for (int h = 0; h < halves; ++h) {
                 CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_mid[h], 0));
                 if ((st = inv_backward0(ctx, p.inv[h], a.S.limbs, p.Dp, Abuf, sc, arena + p.rd[0].elo_off,
-                                        arena + p.rd[0].ehi_off, partials, row0[h], s)))
+                                        arena + p.rd[0].ehi_off, partials + p.rd[0].part_base, (int)p.ntiles, s)))
                     return st;
             }
-            rounds_nb0 = halves == 2 ? nb[0] + nb[1] : nb[0];
+            rounds_nb0 = (int)p.ntiles;
+            // round 1 has one partial row per tile: reduce it on the aux stream while the rounds run
+            CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fwd[0], s));
+            CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->aux, ctx->ev_fwd[0], 0));
+            LAUNCH(ctx, k_reduce_rounds, 1, 1024, 0, ctx->aux, partials, rounds, 1, rank_sums);
+            CUDA_TRY(ctx, cudaEventRecord(ctx->ev_mid[0], ctx->aux));
+            r1_reduced = true;
         }
         const uint32_t *cA = A1in, *cS = S1in;
         uint64_t len = p.Dp;
         for (int k = a.prove_mode ? 2 : 1; k < p.k0; ++k) {
             const RoundDesc& r = p.rd[k - 1];
-            fr* part = partials + (size_t)(k - 1) * kSlots * kMaxBlocks;
+            fr* part = partials + r.part_base;
             if (k == 1) {
                 LAUNCH(ctx, (k_round<false, true>), r.nblocks, kRoundThreads, 0, s, cA, cS, len, nullptr, nullptr, sc,
                        k, arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, part);
@@ -535,7 +548,12 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
         // the plan's round-1 row count must match what the inversion wrote
         return set_err(ctx, ZKL_E_STATE, "internal: round-1 rows %d != plan %u", rounds_nb0, p.rd[0].nblocks);
     }
-    if (p.dl > 0) LAUNCH(ctx, k_reduce_rounds, p.dl, 256, 0, s, partials, rounds, p.dl, rank_sums);
+    if (r1_reduced) {
+        if (p.dl > 1) LAUNCH(ctx, k_reduce_rounds, p.dl - 1, 256, 0, s, partials, rounds + 1, p.dl - 1, rank_sums + kSlots);
+        CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_mid[0], 0));
+    } else if (p.dl > 0) {
+        LAUNCH(ctx, k_reduce_rounds, p.dl, 256, 0, s, partials, rounds, p.dl, rank_sums);
+    }
     const fr* gathered = rank_sums;
     if (ctx->nranks > 1) {
         int rc = zkl_dist_exchange(ctx, p.dl, rank_sums, gath, fin, at<fr>(ctx, p.o_gfin));
@@ -546,8 +564,7 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
         LAUNCH(ctx, k_tail, 1, kTailThreads, tail_smem, s, (const uint32_t*)at<fr>(ctx, p.o_gfin),
                (const uint32_t*)(at<fr>(ctx, p.o_gfin) + p.P), (uint64_t)p.P, 0, 0, (uint32_t*)nullptr, 0, err, sc,
                p.dl + 1, p.d, rounds, arena, partials, fin);
-        LAUNCH(ctx, k_reduce_rounds, p.d - p.dl, 256, 0, s, partials + (size_t)p.dl * kSlots * kMaxBlocks,
-               rounds + p.dl, p.d - p.dl, repl);
+        LAUNCH(ctx, k_reduce_rounds, p.d - p.dl, 256, 0, s, partials, rounds + p.dl, p.d - p.dl, repl);
     }
     CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
     LAUNCH(ctx, k_derive, 1, 64, 0, s, gathered, ctx->nranks, p.dl, repl, rounds, tsum, sc, rc, p.d, p.n,
@@ -612,8 +629,9 @@ static int ctx_create_common(int device, void* stream, zkl_ctx** out) {
     c->stream = (cudaStream_t)stream;
     c->nranks = 1;
     if (cudaSetDevice(device) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaDeviceGetStreamPriorityRange(&c->prio_lo, &c->prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, c->prio_lo) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, c->prio_hi) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fwd[0], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fwd[1], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_mid[0], cudaEventDisableTiming) != cudaSuccess ||
@@ -712,7 +730,8 @@ int zkl_ctx_set_profiling(zkl_ctx* c, int on) {
     return ZKL_OK;
 }
 
-int zkl_ctx_profile_read(zkl_ctx* c, char* names, int name_len, float* ms, float* start_ms, int cap) {
+int zkl_ctx_profile_read(zkl_ctx* c, char* names, int name_len, float* ms, float* start_ms, int* stream_tag,
+                         int cap) {
     if (!c) return -ZKL_E_ARG;
     int n = 0;
     for (int i = 0; i < c->nprof && n < cap; ++i, ++n) {
@@ -722,6 +741,7 @@ int zkl_ctx_profile_read(zkl_ctx* c, char* names, int name_len, float* ms, float
         cudaEventElapsedTime(&t0, c->prof[0].a, c->prof[i].a);
         ms[n] = t;
         if (start_ms) start_ms[n] = t0;
+        if (stream_tag) stream_tag[n] = c->prof[i].stream == c->side ? 1 : (c->prof[i].stream == c->aux ? 2 : 0);
         snprintf(names + (size_t)n * name_len, name_len, "%s", c->prof[i].name);
     }
     c->nprof = 0;
@@ -780,7 +800,9 @@ int zkl_vec_import_pair(zkl_ctx* ctx, const int32_t* x, const int32_t* y, const 
     CUDA_TRY(ctx, cudaMemcpyAsync(af, staged, sizeof(fr), cudaMemcpyHostToDevice, ctx->stream));
     LAUNCH(ctx, k_import_canon, 1, 32, 0, ctx->stream, (const uint32_t*)af, 1, (uint32_t*)af,
            (unsigned long long*)nullptr);
-    LAUNCH(ctx, k_import_pair_dev, grid_for(dst.n, 256), 256, 0, ctx->stream, x, y, dst.n, af, dst.limbs);
+    fr* consts = af + 1;
+    LAUNCH(ctx, k_pair_consts, 1, 32, 0, ctx->stream, af, consts);
+    LAUNCH(ctx, k_import_pair_dev, grid_for(dst.n, 256), 256, 0, ctx->stream, x, y, dst.n, consts, dst.limbs);
     return sync_stream(ctx);
 }
 
@@ -876,10 +898,12 @@ int zkl_tlookup_prepare(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T,
     uint32_t* rows = at<uint32_t>(ctx, p.o_hist);
     CUDA_TRY(ctx, cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), ctx->stream));
     TableView tv{T->T, T->Taos, T->slots, T->N, T->slot_mask};
+    uint32_t* keys = at<uint32_t>(ctx, p.o_keys);
+    LAUNCH(ctx, k_index_map, grid_for(p.Dp, 256, kSMs * 32), 256, 0, ctx->stream, S.limbs, p.Dp,
+           (uint64_t)ctx->rank * p.Dp, tv, keys, err);
     // key bits: n (+1 for the sentinel of a partial tile when D_local < 4096)
     const int key_bits = std::max(1, p.n + (p.Dp < (uint64_t)kHistTile ? 1 : 0));
-    LAUNCH(ctx, k_hist_rows, p.hist_rows, kHistThreads, 0, ctx->stream, S.limbs, p.Dp, (uint64_t)ctx->rank * p.Dp,
-           tv, rows, key_bits, err);
+    LAUNCH(ctx, k_hist_count, p.hist_rows, kHistThreads, 0, ctx->stream, keys, p.Dp, (uint32_t)T->N, rows, key_bits);
     LAUNCH(ctx, k_hist_colsum, grid_for(T->N, 256), 256, 0, ctx->stream, rows, p.hist_rows, T->N, m_dev);
     if (ctx->nranks > 1) {
         int rc = zkl_dist_allreduce_u32(ctx, m_dev, T->N);

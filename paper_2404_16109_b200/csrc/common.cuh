@@ -109,8 +109,9 @@ __device__ __forceinline__ void atomic_min_i64(unsigned long long* p, uint64_t v
 // Scalars of one proof, Montgomery form, in the workspace.
 struct RoundDesc {
     uint64_t elo_off, ehi_off;   // offsets (in fr) of E_lo / E_hi in the eq arena
+    uint64_t part_base;          // offset (in fr) of this round's partial rows: [slot][row], row stride nblocks
     uint32_t gbits;              // log2 of the group size G (pairs sharing one E_hi entry)
-    uint32_t nblocks;            // blocks that wrote partial rows for this round
+    uint32_t nblocks;            // partial rows (blocks / tiles) written for this round
     uint32_t direct_h1;          // 1: H(1) summed directly (round 1 of sumcheck_prove, u_c = 0)
     uint32_t pad;
 };
@@ -138,7 +139,8 @@ struct zkl_ctx {
     int device;
     cudaStream_t stream;
     cudaStream_t side;             // table-side work overlapping the D side
-    cudaStream_t aux;              // batch inversions of the tile totals (latency hidden behind the D side)
+    cudaStream_t aux;              // upper inversion levels (high priority, latency hidden behind the D side)
+    int prio_lo, prio_hi;
     cudaEvent_t ev_fork, ev_join;
     cudaEvent_t ev_fwd[2], ev_mid[2];
     int rank, nranks;

@@ -69,6 +69,10 @@ ZKL_FR_CONST(fr_three_m, 0xfffffffau, 0x00000005u, 0x0009d806u, 0x098e27eeu, 0xc
 ZKL_FR_CONST(fr_five_m, 0xfffffff5u, 0x0000000au, 0x00120c0bu, 0x66d9f3dfu, 0x960bb7c5u, 0xcc83b7a7u, 0x363b9de5u, 0x04c9cf6du)
 ZKL_FR_CONST(fr_six_m, 0xfffffff3u, 0x0000000cu, 0x0015540du, 0xbf5eabd9u, 0x82c807bau, 0x66100797u, 0xe300a355u, 0x1cee80c6u)
 
+// 2^32 in Montgomery form (2^32 * 2^256 mod r) and its negation
+ZKL_FR_CONST(fr_2p32_m, 0xcaaf6b13u, 0x355094eau, 0x69a568efu, 0xf6b10cb3u, 0x40cc3869u, 0xe2c926a6u, 0xed269aadu, 0x736a6d3bu)
+ZKL_FR_CONST(fr_2p32_m_neg, 0x355094eeu, 0xcaaf6b14u, 0x9658f30fu, 0x5d0c974fu, 0xc8d59f9bu, 0x5070b161u, 0x3c76e29au, 0x00833a17u)
+
 __device__ __forceinline__ bool fr_is_zero(const fr& a) {
     uint32_t x = a.v[0] | a.v[1] | a.v[2] | a.v[3] | a.v[4] | a.v[5] | a.v[6] | a.v[7];
     return x == 0;
@@ -206,7 +210,7 @@ __device__ __forceinline__ fr fr_mul(const fr& a, const fr& b) {
         ZKL_MADPAIR("%11", "%12", "q", "%19", "%11", "%12")                                      \
         ZKL_MADPAIR("%13", "%14", "q", "%21", "%13", "%14")                                      \
         "madc.lo.cc.u32 %15, q, %23, %15;\n\t"                                                   \
-        "madc.hi.u32    %16, q, %23, %16;\n\t}"                                                  \
+        "madc.hi.cc.u32 %16, q, %23, %16;\n\t}"    /* carry out is 0 (see header) */          \
         : "+r"(x0), "+r"(x1), "+r"(x2), "+r"(x3), "+r"(x4), "+r"(x5), "+r"(x6), "+r"(x7),          \
           "+r"(x8), "+r"(y0), "+r"(y1), "+r"(y2), "+r"(y3), "+r"(y4), "+r"(y5), "+r"(y6), "+r"(y7) \
         : "n"(ZKL_R1), "n"(ZKL_R2), "n"(ZKL_R3), "n"(ZKL_R4), "n"(ZKL_R5), "n"(ZKL_R6),           \
@@ -226,7 +230,7 @@ __device__ __forceinline__ fr fr_mul(const fr& a, const fr& b) {
             ZKL_MADPAIR("%3", "%4", "%19", "%22", "%13", "%14")
             ZKL_MADPAIR("%5", "%6", "%20", "%22", "%15", "%16")
             "madc.lo.cc.u32 %7, %21, %22, %17;\n\t"
-            "madc.hi.u32    %8, %21, %22, 0;"
+            "madc.hi.cc.u32 %8, %21, %22, 0;"
             : "=r"(M0), "=r"(Y0), "=r"(Y1), "=r"(Y2), "=r"(Y3), "=r"(Y4), "=r"(Y5), "=r"(Y6), "=r"(Y7)
             : "r"(y0), "r"(x1), "r"(x2), "r"(x3), "r"(x4), "r"(x5), "r"(x6), "r"(x7), "r"(x8),
               "r"(a.v[1]), "r"(a.v[3]), "r"(a.v[5]), "r"(a.v[7]), "r"(bi));

@@ -38,15 +38,55 @@ __global__ void k_import_i64(const int64_t* __restrict__ src, uint64_t n, uint32
         st_fr(dst, n, i, fr_to_mont(fr_from_i64(src[i])));
 }
 
-// S_i = x_i + alpha_f y_i.  *af = alpha_f in Montgomery form:
-// mont(af, y) = alpha_f * y (canonical), then one to-Montgomery multiplication.
-__global__ void k_import_pair_dev(const int32_t* __restrict__ x, const int32_t* __restrict__ y, uint64_t n,
-                                  const fr* __restrict__ af, uint32_t* __restrict__ dst) {
-    const fr af_m = *af;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        fr s = fr_add(fr_from_i64(x[i]), fr_mul(af_m, fr_from_i64(y[i])));
-        st_fr(dst, n, i, fr_to_mont(s));
+// S_i = x_i + alpha_f y_i for 32-bit x, y, straight into Montgomery form without a full
+// field multiplication: with Cx = +-2^32 R, Cy = +-alpha_f 2^32 R (mod r, sign of x / y),
+//   U = |x| Cx + |y| Cy  (< 2^32 r, 9 words),  V = (U + q r) / 2^32 with q = -U mod 2^32 (r' = -1)
+// is congruent to (x + alpha_f y) R and below 2r: one conditional subtraction makes it canonical.
+// consts: [Cx+, Cx-, Cy+, Cy-] (Montgomery-domain words, canonical).
+__device__ __forceinline__ fr fr_from_small_pair(int32_t x, int32_t y, const fr* __restrict__ c) {
+    const uint32_t ax = x < 0 ? 0u - (uint32_t)x : (uint32_t)x;
+    const uint32_t ay = y < 0 ? 0u - (uint32_t)y : (uint32_t)y;
+    const fr& cx = c[x < 0 ? 1 : 0];
+    const fr& cy = c[y < 0 ? 3 : 2];
+    uint32_t u[9];
+    uint64_t t = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        t = (uint64_t)ax * cx.v[j] + (uint64_t)ay * cy.v[j] + (t >> 32);
+        u[j] = (uint32_t)t;
     }
+    u[8] = (uint32_t)(t >> 32);
+    const uint32_t q = 0u - u[0];
+    const uint32_t rl[8] = {ZKL_R0, ZKL_R1, ZKL_R2, ZKL_R3, ZKL_R4, ZKL_R5, ZKL_R6, ZKL_R7};
+    uint64_t cy64 = u[0] != 0;   // u0 + q * r0 = u0 + q = 0 (mod 2^32), carry iff u0 != 0
+    fr v;
+#pragma unroll
+    for (int j = 1; j < 8; ++j) {
+        const uint64_t w = (uint64_t)q * rl[j] + u[j] + cy64;
+        v.v[j - 1] = (uint32_t)w;
+        cy64 = w >> 32;
+    }
+    v.v[7] = (uint32_t)(u[8] + cy64);
+    fr_reduce_once(v);
+    return v;
+}
+
+__global__ void k_pair_consts(const fr* __restrict__ af_m, fr* c) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        c[0] = fr_2p32_m();
+        c[1] = fr_2p32_m_neg();
+        c[2] = fr_mul(*af_m, fr_2p32_m());
+        c[3] = fr_neg(c[2]);
+    }
+}
+
+__global__ void k_import_pair_dev(const int32_t* __restrict__ x, const int32_t* __restrict__ y, uint64_t n,
+                                  const fr* __restrict__ consts, uint32_t* __restrict__ dst) {
+    __shared__ fr c[4];
+    if (threadIdx.x < 4) c[threadIdx.x] = consts[threadIdx.x];
+    __syncthreads();
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        st_fr(dst, n, i, fr_from_small_pair(x[i], y[i], c));
 }
 
 __global__ void k_export(const uint32_t* __restrict__ src, uint64_t n, uint32_t* __restrict__ dst) {
@@ -133,70 +173,56 @@ __global__ void k_table_dups(const uint32_t* __restrict__ T, const uint4* __rest
 }
 
 // ====================================================================== a3: multiplicities
-// Atomic-free histogram: per tile of 4096 lookups, index map (hash probe, 8 independent probes per thread
-// in flight), block radix sort of the indices (8-bit digits), then per distinct index one read-modify-
-// write of the CTA-private row: heads subtract their sorted position, tails add theirs + 1 (two
-// barrier-separated phases, each touching one address per distinct key).  A column sum gives m.
-// A lookup not in T reports its index (atomicMin on the error word, the error path only) and is
-// counted under key 0 — m is discarded on error.  Keys beyond n (a partial tile, n < 4096) take the
-// sentinel N, which sorts last and is not counted.
+// Two passes, atomic-free:
+//  (1) index map: one lookup per thread (high occupancy hides the two dependent L2 round trips of the
+//      hash probe): key_i = j such that S_i = T_j (full 256-bit compare against the AoS key copy).  A
+//      lookup not in T reports its index (atomicMin on the error word — the error path only) and gets
+//      key 0 (m is discarded on error).
+//  (2) count: per tile of 4096 keys, block radix sort, then per distinct key one read-modify-write of
+//      the CTA-private row: heads subtract their sorted position, tails add theirs + 1 (two barrier-
+//      separated phases, each touching one address per distinct key).  Keys beyond n (a partial tile,
+//      n < 4096) take the sentinel N, which sorts last and is not counted.  A column sum gives m.
+__global__ void __launch_bounds__(256)
+k_index_map(const uint32_t* __restrict__ S, uint64_t n, uint64_t global_offset, TableView tv,
+            uint32_t* __restrict__ keys, unsigned long long* err) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const fr x = ld_fr(S, n, i);
+        const int64_t f = table_find(tv, x);
+        uint32_t key = 0;
+        if (f < 0) atomic_min_i64(err, global_offset + i);
+        else key = (uint32_t)f;
+        keys[i] = key;
+    }
+}
+
 constexpr int kHistThreads = 512;
 constexpr int kHistItems = 8;
 constexpr int kHistTile = kHistThreads * kHistItems;   // 4096
 
 __global__ void __launch_bounds__(kHistThreads, 2)
-k_hist_rows(const uint32_t* __restrict__ S, uint64_t n, uint64_t global_offset, TableView tv, uint32_t* rows,
-            int key_bits, unsigned long long* err) {
+k_hist_count(const uint32_t* __restrict__ keys_in, uint64_t n, uint32_t N, uint32_t* rows, int key_bits) {
     typedef cub::BlockRadixSort<uint32_t, kHistThreads, kHistItems> Sort;
     __shared__ union {
         typename Sort::TempStorage sort;
         uint32_t keys[kHistTile];
     } sm;
-    const uint32_t N = (uint32_t)tv.N;
     uint32_t* row = rows + (uint64_t)blockIdx.x * N;
     for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) row[j] = 0;
     __syncthreads();
     const uint64_t ntiles = (n + kHistTile - 1) / kHistTile;
-    const bool vec_ok = (n & 3) == 0;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const uint64_t base = tile * kHistTile;
-        fr x[kHistItems];
+        uint32_t keys[kHistItems];
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
             const uint64_t i0 = base + 2048 * g + 4 * threadIdx.x;
-            if (vec_ok && i0 + 3 < n) {
-                fr q[4];
-                ld_fr4(S, n, i0, q);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) x[4 * g + j] = q[j];
+            if (i0 + 3 < n) {
+                const uint4 q = __ldg(reinterpret_cast<const uint4*>(keys_in + i0));
+                keys[4 * g] = q.x; keys[4 * g + 1] = q.y; keys[4 * g + 2] = q.z; keys[4 * g + 3] = q.w;
             } else {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) x[4 * g + j] = i0 + j < n ? ld_fr(S, n, i0 + j) : fr_zero();
+                for (int j = 0; j < 4; ++j) keys[4 * g + j] = i0 + j < n ? keys_in[i0 + j] : N;
             }
-        }
-        // first probe of all 8 keys in flight together
-        uint32_t h[kHistItems], slot[kHistItems], keys[kHistItems];
-#pragma unroll
-        for (int q = 0; q < kHistItems; ++q) h[q] = hash_fr(x[q]) & tv.mask;
-#pragma unroll
-        for (int q = 0; q < kHistItems; ++q) slot[q] = __ldg(tv.slots + h[q]);
-#pragma unroll
-        for (int q = 0; q < kHistItems; ++q) {
-            const uint64_t i = base + 2048 * (q >> 2) + 4 * threadIdx.x + (q & 3);
-            bool ok = slot[q] != 0 && aos_eq(tv.Taos + 2 * (uint64_t)(slot[q] - 1), x[q]);
-            uint32_t key = slot[q] - 1;
-            if (!ok && slot[q] != 0) {                 // collision: keep probing
-                const int64_t f = table_find(tv, x[q]);
-                ok = f >= 0;
-                key = (uint32_t)f;
-            }
-            if (i >= n) {
-                key = N;
-            } else if (!ok) {
-                atomic_min_i64(err, global_offset + i);
-                key = 0;
-            }
-            keys[q] = key;
         }
         __syncthreads();   // smem union reuse across tiles
         Sort(sm.sort).Sort(keys, 0, key_bits);
@@ -333,7 +359,7 @@ template <bool LEVEL0>
 __global__ void __launch_bounds__(kInvThreads, 2)
 k_inv_bwd(const uint32_t* __restrict__ X, uint64_t n, const ProofScalars* __restrict__ sc, uint32_t* slots,
           const uint32_t* __restrict__ next_inv, uint64_t nnext, uint64_t t0, uint64_t t1,
-          const fr* __restrict__ elo, const fr* __restrict__ ehi, fr* partials, int row0) {
+          const fr* __restrict__ elo, const fr* __restrict__ ehi, fr* partials, int row0, int rows) {
     const fr beta = LEVEL0 ? sc->beta : fr_zero();
     const bool eval = LEVEL0 && partials != nullptr;
     fr hinf = fr_zero(), a0 = fr_zero(), a1 = fr_zero();
@@ -371,9 +397,9 @@ k_inv_bwd(const uint32_t* __restrict__ X, uint64_t n, const ProofScalars* __rest
         block_sum_fr<3>(v, scratch);
         if (threadIdx.x == 0) {
             const int row = row0 + blockIdx.x;
-            partials[SLOT_HINF * kMaxBlocks + row] = v[0];
-            partials[SLOT_A0 * kMaxBlocks + row] = v[1];
-            partials[SLOT_A1 * kMaxBlocks + row] = v[2];
+            partials[SLOT_HINF * rows + row] = v[0];
+            partials[SLOT_A0 * rows + row] = v[1];
+            partials[SLOT_A1 * rows + row] = v[2];
         }
     }
 }
@@ -441,7 +467,7 @@ k_round(const uint32_t* __restrict__ Aold, const uint32_t* __restrict__ Sold, ui
     block_sum_fr<5>(v, scratch);
     if (threadIdx.x == 0) {
 #pragma unroll
-        for (int s = 0; s < 5; ++s) partials[s * kMaxBlocks + blockIdx.x] = v[s];
+        for (int s = 0; s < 5; ++s) partials[s * gridDim.x + blockIdx.x] = v[s];
     }
 }
 
@@ -521,9 +547,9 @@ k_tail(const uint32_t* __restrict__ Ain, const uint32_t* __restrict__ Sin, uint6
         }
         block_sum_fr<5>(v, scratch);
         if (t == 0) {
-            fr* part = partials_base + (uint64_t)(k - 1) * kSlots * kMaxBlocks;
+            fr* part = partials_base + rd.part_base;
 #pragma unroll
-            for (int s = 0; s < 5; ++s) part[s * kMaxBlocks] = v[s];
+            for (int s = 0; s < 5; ++s) part[s] = v[s];   // one row (nblocks = 1)
         }
         // fold with r_k
         const fr r = sc->r[k - 1];
@@ -665,8 +691,8 @@ __global__ void k_setup(const zkl_fr* __restrict__ host_chal, int d, int pbits, 
 // Sum of each round's per-block partial rows -> rank_sums[k][slot] (this rank's contribution).
 __global__ void k_reduce_rounds(const fr* __restrict__ partials, const RoundDesc* __restrict__ rounds, int nrounds,
                                 fr* rank_sums) {
-    __shared__ fr scratch[5 * 8];
-    const int k = blockIdx.x;   // 0-based round
+    __shared__ fr scratch[5 * 32];
+    const int k = blockIdx.x;   // 0-based round (relative to `rounds`)
     if (k >= nrounds) return;
     const uint32_t nb = rounds[k].nblocks;
     fr v[5];
@@ -674,7 +700,7 @@ __global__ void k_reduce_rounds(const fr* __restrict__ partials, const RoundDesc
     for (int s = 0; s < 5; ++s) {
         v[s] = fr_zero();
         for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x)
-            v[s] = fr_add(v[s], partials[((uint64_t)k * kSlots + s) * kMaxBlocks + b]);
+            v[s] = fr_add(v[s], partials[rounds[k].part_base + (uint64_t)s * nb + b]);
     }
     block_sum_fr<5>(v, scratch);
     if (threadIdx.x == 0) {

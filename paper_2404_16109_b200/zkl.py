@@ -72,7 +72,7 @@ def lib() -> ctypes.CDLL:
             "zkl_ctx_launch_count": ([P], U64),
             "zkl_ctx_set_profiling": ([P, I32], I32),
             "zkl_ctx_profile_read": ([P, ctypes.c_char_p, I32, ctypes.POINTER(ctypes.c_float),
-                                      ctypes.POINTER(ctypes.c_float), I32], I32),
+                                      ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int), I32], I32),
             "zkl_vec_import": ([P, P, I32, zkl_vec, I64P], I32),
             "zkl_vec_import_i64": ([P, P, zkl_vec], I32),
             "zkl_vec_import_pair": ([P, P, P, ctypes.POINTER(zkl_fr), zkl_vec], I32),
@@ -203,18 +203,20 @@ class Context:
         self._check(lib().zkl_ctx_set_profiling(self.h, 1 if on else 0))
 
     def profile_read(self, with_start: bool = False):
-        """[(kernel name, ms[, start ms])] of the launches recorded since profiling was (re)enabled or last read."""
+        """[(kernel name, ms[, start ms, stream tag])] of the launches recorded since profiling was (re)enabled
+        or last read.  stream tag: 0 = ctx stream, 1 = table side, 2 = aux."""
         cap, nl = 256, 64
         names = ctypes.create_string_buffer(cap * nl)
         ms = (ctypes.c_float * cap)()
         st = (ctypes.c_float * cap)()
-        n = lib().zkl_ctx_profile_read(self.h, names, nl, ms, st, cap)
+        tag = (ctypes.c_int * cap)()
+        n = lib().zkl_ctx_profile_read(self.h, names, nl, ms, st, tag, cap)
         if n < 0:
             raise ZklError(-n, -1, "profile_read")
         raw = names.raw
         nm = [raw[i * nl:(i + 1) * nl].split(b"\0", 1)[0].decode() for i in range(n)]
         if with_start:
-            return [(nm[i], float(ms[i]), float(st[i])) for i in range(n)]
+            return [(nm[i], float(ms[i]), float(st[i]), int(tag[i])) for i in range(n)]
         return [(nm[i], float(ms[i])) for i in range(n)]
 
     def reserve(self, D_local: int, N: int):

@@ -26,5 +26,5 @@ ctx.set_profiling(True)
 t0 = time.perf_counter(); step(); torch.cuda.synchronize(); wall = time.perf_counter() - t0
 rec = ctx.profile_read(with_start=True)
 print(f"wall {wall*1e3:.2f} ms  launches {len(rec)}")
-for name, ms, st in rec:
-    print(f"{st:9.3f} {ms:8.3f}  {name}")
+for name, ms, st, tag in sorted(rec, key=lambda r: r[2]):
+    print(f"{st:9.3f} {ms:8.3f}  {'main side aux'.split()[tag]:4s} {name}")
