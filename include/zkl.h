@@ -50,6 +50,7 @@ typedef struct { uint32_t w[8]; } zkl_fr;                  /* canonical, little-
 typedef struct { uint32_t* limbs; uint64_t n; } zkl_vec;   /* device, SoA Montgomery */
 typedef struct zkl_ctx zkl_ctx;
 typedef struct zkl_table zkl_table;
+typedef struct zkl_group zkl_group;
 
 typedef enum {
     ZKL_OK = 0,
@@ -87,6 +88,13 @@ int zkl_ctx_create(int device, void* cuda_stream, zkl_ctx** out);
 int zkl_nccl_unique_id(uint8_t id[128]);
 int zkl_ctx_create_dist(int device, void* cuda_stream, const uint8_t nccl_id[128], int rank, int nranks,
                         zkl_ctx** out);
+/* Loopback communicator: P virtual ranks in ONE process on one device, one host thread per rank, each with
+ * its own ctx.  Collectives are host barriers around device copies through the group's staging memory (no
+ * kernel waits on another rank's kernel).  For testing the multi-rank path (partition, exchange, replicated
+ * rounds) without NCCL; max_N bounds the table size.  The group must outlive its contexts. */
+int zkl_group_create(int device, int nranks, uint64_t max_D_local, uint64_t max_N, zkl_group** out);
+void zkl_group_destroy(zkl_group* group);
+int zkl_ctx_create_loopback(int device, void* cuda_stream, zkl_group* group, int rank, zkl_ctx** out);
 void zkl_ctx_destroy(zkl_ctx* ctx);
 const char* zkl_last_error(const zkl_ctx* ctx);
 /* Workspace for prepare/prove/sumcheck with local length D_local and table size N (bytes, 256-B aligned). */

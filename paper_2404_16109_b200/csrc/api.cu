@@ -13,6 +13,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <new>
 #include <vector>
 
 #include "kernels.cuh"
@@ -674,6 +675,41 @@ int zkl_ctx_create_dist(int device, void* cuda_stream, const uint8_t nccl_id[128
     }
     (*out)->rank = rank;
     (*out)->nranks = nranks;
+    return ZKL_OK;
+}
+
+int zkl_group_create(int device, int nranks, uint64_t max_D_local, uint64_t max_N, zkl_group** out) {
+    if (!out || nranks < 1) return ZKL_E_ARG;
+    zkl_group* g = new (std::nothrow) zkl_group();
+    if (!g) return ZKL_E_OOM;
+    g->nranks = nranks;
+    g->device = device;
+    // largest block: m (N u32) or the round sums (kMaxRounds x kSlots fr)
+    g->staging_bytes = (size_t)nranks * std::max<size_t>(4 * max_N, sizeof(fr) * kMaxRounds * kSlots) + 4096;
+    (void)max_D_local;
+    if (cudaSetDevice(device) != cudaSuccess || cudaMalloc(&g->staging, g->staging_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        delete g;
+        return ZKL_E_CUDA;
+    }
+    *out = g;
+    return ZKL_OK;
+}
+
+void zkl_group_destroy(zkl_group* g) {
+    if (!g) return;
+    cudaSetDevice(g->device);
+    cudaFree(g->staging);
+    delete g;
+}
+
+int zkl_ctx_create_loopback(int device, void* cuda_stream, zkl_group* group, int rank, zkl_ctx** out) {
+    if (!group || rank < 0 || rank >= group->nranks) return ZKL_E_ARG;
+    int st = ctx_create_common(device, cuda_stream, out);
+    if (st) return st;
+    (*out)->group = group;
+    (*out)->rank = rank;
+    (*out)->nranks = group->nranks;
     return ZKL_OK;
 }
 

@@ -135,6 +135,23 @@ struct ProofOut {
 }  // namespace zkl
 
 // ------------------------------------------------------------------ opaque ABI objects
+#include <condition_variable>
+#include <mutex>
+
+// loopback group: P virtual ranks (threads) of one process on one device
+struct zkl_group {
+    int nranks;
+    int device;
+    uint8_t* staging;            // device, nranks x max block
+    size_t staging_bytes;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    uint64_t generation = 0;
+    int min_arrived = 0;
+    unsigned long long min_acc = ~0ull;
+};
+
 struct zkl_ctx {
     int device;
     cudaStream_t stream;
@@ -145,6 +162,7 @@ struct zkl_ctx {
     cudaEvent_t ev_fwd[2], ev_mid[2];
     int rank, nranks;
     void* nccl_comm;               // ncclComm_t (loaded at run time) when nranks > 1
+    zkl_group* group;              // loopback communicator (instead of NCCL), or null
     uint8_t* ws;
     size_t ws_bytes;
     void* host_out;                // pinned host copy of ProofOut + staging

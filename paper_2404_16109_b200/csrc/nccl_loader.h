@@ -15,6 +15,10 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <algorithm>
+#include <condition_variable>
+#include <mutex>
+
 #include <nccl.h>
 
 namespace {
@@ -96,8 +100,8 @@ __global__ void k_pairs_to_soa(const zkl::fr* __restrict__ g, int P, uint32_t* s
 
 // All-gather this rank's round sums (dl x 5 fr) into gath[P][dl][5] and the folded (A, S) into the
 // SoA pair buffer gfin (2 x 8 x P words), via a scratch area right after gfin.
-int zkl_dist_exchange(zkl_ctx* ctx, int dl, const zkl::fr* rank_sums, zkl::fr* gath, const zkl::fr* fin,
-                      zkl::fr* gfin) {
+int nccl_exchange(zkl_ctx* ctx, int dl, const zkl::fr* rank_sums, zkl::fr* gath, const zkl::fr* fin,
+                  zkl::fr* gfin) {
     NcclApi& a = nccl();
     ncclComm_t comm = (ncclComm_t)ctx->nccl_comm;
     const size_t words = (size_t)dl * zkl::kSlots * 8;
@@ -110,13 +114,13 @@ int zkl_dist_exchange(zkl_ctx* ctx, int dl, const zkl::fr* rank_sums, zkl::fr* g
     return cudaGetLastError() == cudaSuccess ? ZKL_OK : ZKL_E_CUDA;
 }
 
-int zkl_dist_allreduce_u32(zkl_ctx* ctx, uint32_t* buf, uint64_t n) {
+int nccl_allreduce_u32(zkl_ctx* ctx, uint32_t* buf, uint64_t n) {
     NCCL_TRY(ctx, nccl().AllReduce(buf, buf, n, ncclUint32, ncclSum, (ncclComm_t)ctx->nccl_comm, ctx->stream));
     return ZKL_OK;
 }
 
 // min over ranks of a host u64 (uses the pinned host page + a device word)
-int zkl_dist_min_u64(zkl_ctx* ctx, unsigned long long* v) {
+int nccl_min_u64(zkl_ctx* ctx, unsigned long long* v) {
     unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->dscratch + 16);
     unsigned long long* h = reinterpret_cast<unsigned long long*>((uint8_t*)ctx->host_out + 61000);
     *h = *v;
@@ -126,6 +130,107 @@ int zkl_dist_min_u64(zkl_ctx* ctx, unsigned long long* v) {
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return ZKL_E_CUDA;
     *v = *h;
     return ZKL_OK;
+}
+
+// ---------------------------------------------------------------- loopback communicator
+// P virtual ranks in one process (one host thread each, same device): a collective is a host barrier
+// around device copies through a staging area owned by the group.  No kernel ever waits on another
+// rank's kernel: every wait is a host-side barrier after a stream synchronization.  Used to run the
+// P > 1 code path (partition, exchange, replicated rounds) bit-for-bit on one GPU.
+int lb_barrier(zkl_group* g) {
+    std::unique_lock<std::mutex> lk(g->mu);
+    const uint64_t gen = g->generation;
+    if (++g->arrived == g->nranks) {
+        g->arrived = 0;
+        ++g->generation;
+        g->cv.notify_all();
+    } else {
+        g->cv.wait(lk, [&] { return g->generation != gen; });
+    }
+    return ZKL_OK;
+}
+
+// every rank contributes `bytes` at `src` (device); afterwards `dst` (device) holds all ranks' blocks, rank-major
+int lb_allgather(zkl_ctx* ctx, const void* src, void* dst, size_t bytes) {
+    zkl_group* g = ctx->group;
+    if ((size_t)g->nranks * bytes > g->staging_bytes) return ZKL_E_OOM;
+    if (cudaMemcpyAsync(g->staging + (size_t)ctx->rank * bytes, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+        return ZKL_E_CUDA;
+    lb_barrier(g);
+    if (cudaMemcpyAsync(dst, g->staging, (size_t)g->nranks * bytes, cudaMemcpyDeviceToDevice, ctx->stream) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+        return ZKL_E_CUDA;
+    lb_barrier(g);
+    return ZKL_OK;
+}
+
+__global__ void k_sum_rows_u32(const uint32_t* __restrict__ rows, int nrows, uint64_t n, uint32_t* out) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t s = 0;
+        for (int r = 0; r < nrows; ++r) s += rows[(uint64_t)r * n + j];
+        out[j] = s;
+    }
+}
+
+int lb_allreduce_u32(zkl_ctx* ctx, uint32_t* buf, uint64_t n) {
+    zkl_group* g = ctx->group;
+    const size_t bytes = n * sizeof(uint32_t);
+    if ((size_t)g->nranks * bytes > g->staging_bytes) return ZKL_E_OOM;
+    if (cudaMemcpyAsync(g->staging + (size_t)ctx->rank * bytes, buf, bytes, cudaMemcpyDeviceToDevice, ctx->stream) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+        return ZKL_E_CUDA;
+    lb_barrier(g);
+    k_sum_rows_u32<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 1184), 256, 0, ctx->stream>>>(
+        reinterpret_cast<const uint32_t*>(g->staging), g->nranks, n, buf);
+    ctx->launches++;
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return ZKL_E_CUDA;
+    lb_barrier(g);
+    return ZKL_OK;
+}
+
+int lb_min_u64(zkl_ctx* ctx, unsigned long long* v) {
+    zkl_group* g = ctx->group;
+    {
+        std::lock_guard<std::mutex> lk(g->mu);
+        if (g->min_arrived == 0) g->min_acc = ~0ull;
+        g->min_acc = std::min(g->min_acc, *v);
+        ++g->min_arrived;
+    }
+    lb_barrier(g);
+    *v = g->min_acc;
+    lb_barrier(g);
+    {
+        std::lock_guard<std::mutex> lk(g->mu);
+        g->min_arrived = 0;
+    }
+    lb_barrier(g);
+    return ZKL_OK;
+}
+
+int lb_exchange(zkl_ctx* ctx, int dl, const zkl::fr* rank_sums, zkl::fr* gath, const zkl::fr* fin, zkl::fr* gfin) {
+    int st;
+    if (dl > 0 && (st = lb_allgather(ctx, rank_sums, gath, (size_t)dl * zkl::kSlots * sizeof(zkl::fr)))) return st;
+    zkl::fr* g2 = gath + (size_t)ctx->nranks * dl * zkl::kSlots;
+    if ((st = lb_allgather(ctx, fin, g2, 2 * sizeof(zkl::fr)))) return st;
+    k_pairs_to_soa<<<1, 32, 0, ctx->stream>>>(g2, ctx->nranks, reinterpret_cast<uint32_t*>(gfin));
+    ctx->launches++;
+    return cudaGetLastError() == cudaSuccess ? ZKL_OK : ZKL_E_CUDA;
+}
+
+// ---------------------------------------------------------------- dispatch
+int zkl_dist_exchange(zkl_ctx* ctx, int dl, const zkl::fr* rank_sums, zkl::fr* gath, const zkl::fr* fin,
+                      zkl::fr* gfin) {
+    return ctx->group ? lb_exchange(ctx, dl, rank_sums, gath, fin, gfin) : nccl_exchange(ctx, dl, rank_sums, gath, fin, gfin);
+}
+int zkl_dist_allreduce_u32(zkl_ctx* ctx, uint32_t* buf, uint64_t n) {
+    return ctx->group ? lb_allreduce_u32(ctx, buf, n) : nccl_allreduce_u32(ctx, buf, n);
+}
+int zkl_dist_min_u64(zkl_ctx* ctx, unsigned long long* v) {
+    return ctx->group ? lb_min_u64(ctx, v) : nccl_min_u64(ctx, v);
 }
 
 }  // namespace

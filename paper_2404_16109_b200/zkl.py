@@ -66,6 +66,9 @@ def lib() -> ctypes.CDLL:
             "zkl_nccl_unique_id": ([ctypes.c_char_p], I32),
             "zkl_ctx_create_dist": ([I32, P, ctypes.c_char_p, I32, I32, ctypes.POINTER(P)], I32),
             "zkl_ctx_destroy": ([P], None),
+            "zkl_group_create": ([I32, I32, U64, U64, ctypes.POINTER(P)], I32),
+            "zkl_group_destroy": ([P], None),
+            "zkl_ctx_create_loopback": ([I32, P, P, I32, ctypes.POINTER(P)], I32),
             "zkl_last_error": ([P], ctypes.c_char_p),
             "zkl_workspace_bytes": ([U64, U64, I32], ctypes.c_size_t),
             "zkl_ctx_set_workspace": ([P, P, ctypes.c_size_t], I32),
@@ -96,6 +99,7 @@ def lib() -> ctypes.CDLL:
 
 
 EXPORTED = ["zkl_strerror", "zkl_ctx_create", "zkl_nccl_unique_id", "zkl_ctx_create_dist", "zkl_ctx_destroy",
+            "zkl_group_create", "zkl_group_destroy", "zkl_ctx_create_loopback",
             "zkl_last_error", "zkl_workspace_bytes", "zkl_ctx_set_workspace", "zkl_ctx_launch_count",
             "zkl_ctx_set_profiling", "zkl_ctx_profile_read",
             "zkl_vec_import", "zkl_vec_import_i64", "zkl_vec_import_pair", "zkl_vec_export", "zkl_table_bytes",
@@ -159,7 +163,8 @@ class Proof:
 class Context:
     """One device context: stream, workspace and the zkl_ctx handle."""
 
-    def __init__(self, device: int = 0, stream=None, rank: int = 0, nranks: int = 1, nccl_id: bytes = None):
+    def __init__(self, device: int = 0, stream=None, rank: int = 0, nranks: int = 1, nccl_id: bytes = None,
+                 group: "LoopbackGroup" = None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("zkl needs a CUDA device (no CPU fallback)")
@@ -167,7 +172,11 @@ class Context:
         self.device = torch.device("cuda", device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         h = ctypes.c_void_p()
-        if nranks > 1:
+        if group is not None:
+            nranks = group.nranks
+            st = lib().zkl_ctx_create_loopback(device, ctypes.c_void_p(self.stream.cuda_stream), group.h, rank,
+                                               ctypes.byref(h))
+        elif nranks > 1:
             st = lib().zkl_ctx_create_dist(device, ctypes.c_void_p(self.stream.cuda_stream), nccl_id, rank, nranks,
                                            ctypes.byref(h))
         else:
@@ -355,6 +364,28 @@ def _evals(arr, d) -> List[List[int]]:
 def _finals(f: zkl_final_evals) -> Dict[str, int]:
     return {"A": fr_to_int(f.A), "S": fr_to_int(f.S), "B": fr_to_int(f.B), "T": fr_to_int(f.T),
             "m": fr_to_int(f.m)}
+
+
+class LoopbackGroup:
+    """P virtual ranks on one device (zkl_group_create); one Context(group=..., rank=p) per host thread."""
+
+    def __init__(self, nranks: int, device: int = 0, max_D_local: int = 1 << 20, max_N: int = 1 << 16):
+        h = ctypes.c_void_p()
+        st = lib().zkl_group_create(device, nranks, max_D_local, max_N, ctypes.byref(h))
+        if st:
+            raise ZklError(st, -1, "zkl_group_create")
+        self.h, self.nranks = h, nranks
+
+    def close(self):
+        if self.h:
+            lib().zkl_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def nccl_unique_id() -> bytes:
