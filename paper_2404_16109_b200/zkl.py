@@ -235,6 +235,7 @@ class Context:
         if self.ws is None or self.ws.numel() < need:
             self.ws = None
             self.torch.cuda.synchronize(self.device)
+            self.torch.cuda.empty_cache()
             self.ws = self.torch.empty(need + 256, dtype=self.torch.uint8, device=self.device)
         ptr = self.ws.data_ptr()
         pad = (-ptr) % 256

@@ -151,6 +151,15 @@ def range_check(D: int = 1 << 10, N: int = 1 << 8, cfg: str = "1", seed: int = 1
     return Workload(f"C{cfg}-range", D, N, "int", challenges(cfg, D.bit_length() - 1), s=s, t=t)
 
 
+def activation_x(cfg: str, start: int, count: int, real: int) -> np.ndarray:
+    """X[start:start+count] of an activation workload (counter-based: any chunk can be drawn alone)."""
+    x = np.rint(4096.0 * gaussian(CONFIG_SEEDS[cfg], count, start=start))
+    x = np.clip(x, -32768, 32767).astype(np.int32)
+    if real < start + count:
+        x[max(0, real - start):] = 0
+    return x
+
+
 def activation(cfg: str = "H", D: Optional[int] = None, real: Optional[int] = None) -> Workload:
     """C2 (GELU, 2^20), C3 (SiLU, 22,544,384 -> 2^25), H (SiLU, 2^26), C5 (SiLU, 2^30)."""
     default_D = {"2": 1 << 20, "3": 1 << 25, "H": 1 << 26, "5": 1 << 30}[cfg]
