@@ -6,9 +6,9 @@ Contract (driver): `python bench.py --gpus N --steps K --warmup W`; for N > 1 la
 
 A step is one pass of the whole hot path over the workload H
 (LLaMA-2 SwiGLU/SiLU activation tlookup, D = 2^26 lookups into the N = 2^16 function table):
-  a1 import  S = X + alpha_f Y and T = T_X + alpha_f T_Y from the int32 tensors resident in HBM,
-  a2 table handle (validation + hash index),
-  a3 zkl_tlookup_prepare (multiplicities m),
+  a1 import  T = T_X + alpha_f T_Y, a2 table handle (validation + hash index),
+  a1 + a3 zkl_tlookup_prepare_pair: S = X + alpha_f Y from the int32 tensors resident in HBM, fused with
+          the index map, then the multiplicities m,
   a4-a9 zkl_tlookup_prove (A, B, the 26-round sumcheck, finals) — transcript returned to the host.
 Under P ranks the D = 2^26 lookups are split over the ranks on the top log2 P hypercube variables
 (strong scaling); value = D / max-over-ranks step time.
@@ -54,6 +54,47 @@ def kernel_work(name: str, n: int) -> float:
     if name == "k_import_pair_dev":
         return 2.0 * n
     return 0.0
+
+
+class NvmlClockSampler:
+    """SM clock and throttle reasons sampled every 2 ms during the timed region (NVML, in-process)."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, index: int):
+        self.index, self.samples, self.reasons, self.stop = index, [], set(), False
+
+    def __enter__(self):
+        import pynvml
+        pynvml.nvmlInit()
+        self.nv = pynvml
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        return self
+
+    def _run(self):
+        while not self.stop:
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in self.REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __exit__(self, *a):
+        self.stop = True
+        self.t.join(timeout=1)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max, "reasons": sorted(self.reasons),
+                "samples": len(self.samples), "source": "nvml"}
 
 
 class ClockSampler:
@@ -197,10 +238,10 @@ def main():
     m = torch.empty(N, dtype=torch.int32, device=dev)
 
     def step(xs, ys, txs, tys):
-        ctx.import_pair(xs, ys, ch.alpha_f, S)
+        # a1 (T) + a2, then a1 (S) fused with a3 (zkl_tlookup_prepare_pair), then a4-a9
         ctx.import_pair(txs, tys, ch.alpha_f, T)
         tab = ctx.table(T, tmem)
-        ctx.prepare(S, D, tab, m)
+        ctx.prepare_pair(xs, ys, ch.alpha_f, D, tab, S, m)
         return ctx.prove(S, D, tab, m, chal, args.variant)
 
     def barrier():
@@ -216,7 +257,7 @@ def main():
     torch.cuda.synchronize(dev)
     l0 = ctx.launches
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with NvmlClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
             pf = step(xd, yd, txd, tyd)
@@ -276,12 +317,31 @@ def main():
         while n_old > 4096:                   # rounds 2.. fold from n_old = Dp, Dp/2, ...
             per_step_work += kernel_work(dom, n_old)
             n_old //= 2
-    elif dom == "k_import_pair_dev":
-        per_step_work = kernel_work(dom, Dp + N)
+    elif dom in ("k_import_pair_dev", "k_import_pair_index"):
+        per_step_work = kernel_work("k_import_pair_dev", Dp)
     achieved = per_step_work / (tot[dom] / 1e3) / 1e9 if per_step_work else None
+    # DRAM traffic of the dominant kernel per step, from the committed ncu capture of the same workload
+    # (profiles/r01_ncu_summary.json: dram__bytes_read.sum + dram__bytes_write.sum over its launches)
+    traffic, traffic_src = None, None
+    try:
+        summ = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_summary.json")))
+        if dom in summ and args.log2d == 26 and world == 1:
+            traffic = summ[dom]["dram_bytes_per_step"]
+            traffic_src = "profiles/r01_ncu_summary.json (ncu dram__bytes_read+write, per step, cold cache)"
+    except (OSError, ValueError, KeyError):
+        pass
+    # algorithmic bytes per step of the dominant kernel: fold rounds read 64 B and write 32 B per new pair-half
+    alg_bytes = None
+    if dom == "k_round":
+        alg_bytes, n_old = 0, Dp
+        while n_old > 4096:
+            alg_bytes += 2 * 32 * n_old + 2 * 32 * n_old // 2
+            n_old //= 2
     step_ms_sum = sum(tot.values())
     roofline = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": PEAK_GFRMUL, "unit": "GFrmul/s",
-                "frac": (achieved / PEAK_GFRMUL) if achieved else None, "traffic": None,
+                "frac": (achieved / PEAK_GFRMUL) if achieved else None, "traffic": traffic,
+                "traffic_unit": "bytes per step (all launches of the kernel)", "traffic_source": traffic_src,
+                "algorithmic_bytes": alg_bytes, "work_fr_muls_per_step": per_step_work,
                 "peak_basis": "148 SM x 64 IMAD lanes/clk x 1965 MHz / 240 lane-slots per 8x32 Montgomery Fr mul",
                 "share_of_step": tot[dom] / ms, "kernel_ms_per_step": tot[dom]}
     # whole-proof work-based fraction (all kernels): Fr muls of the algorithm per lookup / time

@@ -136,6 +136,13 @@ void zkl_table_destroy(zkl_table* table);
 int zkl_tlookup_prepare(zkl_ctx* ctx, zkl_vec S_local, uint64_t D, const zkl_table* T, uint32_t* m_dev,
                         int64_t* err_index);
 
+/* Function-lookup form of tlookup-Prep (a1 + a3 fused): S_local_out[i] =
+ * x_i + alpha_f y_i (int32 device arrays of length D/P; same encoding as zkl_vec_import_pair) is written and
+ * counted into m_dev in one pass over x, y.  Same errors as zkl_tlookup_prepare. */
+int zkl_tlookup_prepare_pair(zkl_ctx* ctx, const int32_t* x_dev, const int32_t* y_dev, const zkl_fr* alpha_f,
+                             uint64_t D, const zkl_table* T, zkl_vec S_local_out, uint32_t* m_dev,
+                             int64_t* err_index);
+
 /* tlookup-Prove: A_local_out = 1/(beta + S_local), B_out = 1/(beta + T)
  * (LOGUP: m/(beta + T)), then the log2(D)-round sumcheck of Eq. tlookup-sumcheck.
  * round_evals: host, log2(D) x 4 canonical values g_k(0..3), k = 1..log2 D.  finals: host.

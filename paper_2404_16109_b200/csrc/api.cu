@@ -105,7 +105,6 @@ struct Plan {
     int k0;              // first tail round
     int fold_in;         // the tail folds its input on load
     RoundDesc rd[kMaxRounds];
-    uint32_t tnb[kMaxRounds];
     EqJob jobs[2 * kMaxRounds];
     int njobs;
     uint64_t arena;
@@ -117,9 +116,9 @@ struct Plan {
     int inv_blocks;
     int hist_rows;
     // workspace offsets
-    size_t o_out, o_sc, o_err, o_rounds, o_jobs, o_chal, o_part, o_tpart, o_tnb, o_rank, o_gath, o_repl, o_tsum,
+    size_t o_out, o_sc, o_err, o_rounds, o_jobs, o_chal, o_part, o_rank, o_gath, o_repl, o_tsum,
         o_fin, o_tfin, o_gfin, o_rc, o_arena, o_hist, o_keys, o_tot, o_totinv, o_A, o_A1, o_S1, o_A2, o_S2, o_tB, o_tX, o_tM,
-        o_tE, o_tp[2][4], total;
+        o_tE, o_twk, total;
 };
 
 void choose_round(Plan& p, int k, uint64_t npairs, int gbits, int nblocks) {
@@ -212,7 +211,6 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
     }
     p.part_total = prow;
     // ---- table rounds
-    for (int k = 1; k <= p.n; ++k) p.tnb[k - 1] = grid_for(N >> k, 256, kMaxBlocks);
     // ---- workspace layout
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o += align_up(bytes); return r; };
@@ -223,8 +221,6 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
     p.o_jobs = take(sizeof(EqJob) * 2 * kMaxRounds);
     p.o_chal = take(sizeof(zkl_fr) * (3 + 2 * kMaxRounds));
     p.o_part = take(sizeof(fr) * p.part_total);
-    p.o_tpart = take(sizeof(fr) * (size_t)kMaxRounds * 4 * kMaxBlocks);
-    p.o_tnb = take(sizeof(uint32_t) * kMaxRounds);
     p.o_rank = take(sizeof(fr) * kMaxRounds * kSlots);
     p.o_gath = take(sizeof(fr) * (size_t)P * kMaxRounds * kSlots);
     p.o_repl = take(sizeof(fr) * kMaxRounds * kSlots);
@@ -247,8 +243,7 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
     p.o_tX = take(soa_bytes(N));
     p.o_tM = take(soa_bytes(N));
     p.o_tE = take(soa_bytes(N));
-    for (int q = 0; q < 4; ++q) p.o_tp[0][q] = take(soa_bytes(N / 2));
-    for (int q = 0; q < 4; ++q) p.o_tp[1][q] = take(soa_bytes(N / 4));
+    p.o_twk = take(sizeof(fr) * 8 * std::max<uint64_t>(N, 2));
     auto inv_levels = [&](InvPlan& ip, uint64_t n0) {
         ip.n[0] = n0;
         int L = 0;
@@ -400,8 +395,6 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
     EqJob* jobs = at<EqJob>(ctx, p.o_jobs);
     zkl_fr* chal = at<zkl_fr>(ctx, p.o_chal);
     fr* partials = at<fr>(ctx, p.o_part);
-    fr* tpart = at<fr>(ctx, p.o_tpart);
-    uint32_t* tnb = at<uint32_t>(ctx, p.o_tnb);
     fr* rank_sums = at<fr>(ctx, p.o_rank);
     fr* gath = at<fr>(ctx, p.o_gath);
     fr* repl = at<fr>(ctx, p.o_repl);
@@ -416,7 +409,6 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
         zkl_fr chal[3 + 2 * kMaxRounds];
         RoundDesc rounds[kMaxRounds];
         EqJob jobs[2 * kMaxRounds];
-        uint32_t tnb[kMaxRounds];
     };
     Staging* hs = reinterpret_cast<Staging*>((uint8_t*)ctx->host_out + sizeof(ProofOut));
     hs->chal[0] = a.ch->beta;
@@ -426,11 +418,9 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
     for (int k = 0; k < p.d; ++k) hs->chal[3 + p.d + k] = a.ch->r[k];
     memcpy(hs->rounds, p.rd, sizeof(p.rd));
     memcpy(hs->jobs, p.jobs, sizeof(p.jobs));
-    memcpy(hs->tnb, p.tnb, sizeof(p.tnb));
     CUDA_TRY(ctx, cudaMemcpyAsync(chal, hs->chal, sizeof(hs->chal), cudaMemcpyHostToDevice, s));
     CUDA_TRY(ctx, cudaMemcpyAsync(rounds, hs->rounds, sizeof(hs->rounds), cudaMemcpyHostToDevice, s));
     CUDA_TRY(ctx, cudaMemcpyAsync(jobs, hs->jobs, sizeof(hs->jobs), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(ctx, cudaMemcpyAsync(tnb, hs->tnb, sizeof(hs->tnb), cudaMemcpyHostToDevice, s));
     CUDA_TRY(ctx, cudaMemsetAsync(err, 0xff, 4 * sizeof(unsigned long long), s));
     LAUNCH(ctx, k_setup, 1, 1, 0, s, chal, p.d, p.pbits, p.rank, N, D, sc);
     LAUNCH(ctx, k_eq_fill, grid_for(p.arena, 256), 256, 0, s, jobs, p.njobs, p.arena, sc, arena);
@@ -454,31 +444,12 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
             const unsigned bt = (unsigned)std::min<uint64_t>(1024, std::max<uint64_t>(32, N));
             LAUNCH(ctx, k_batch_invert, 1, bt, 4 * bt * sizeof(fr), s2, tX, N, (uint64_t)0, N, tB);
         }
-        LAUNCH(ctx, k_tab_init, grid_for(N, 256), 256, 0, s2, a.m_dev, N, tM, tB, sc, p.d, p.n, a.variant, tE);
-        if (a.B_out.limbs) LAUNCH(ctx, k_copy_vec, grid_for(8 * N, 256), 256, 0, s2, tB, N, a.B_out.limbs);
+        // B_out (if requested) is the variant's B, written by k_tab_all
+        LAUNCH(ctx, k_tab_all, 1, 1024, 0, s2, tB, Tsrc, a.m_dev, (const uint32_t*)nullptr, N, sc, p.d, p.n,
+               a.variant, at<fr>(ctx, p.o_twk), tsum, tfin, a.B_out.limbs);
     } else {
-        LAUNCH(ctx, k_copy_vec, grid_for(8 * N, 256), 256, 0, s2, a.B_in.limbs, N, tB);
-        LAUNCH(ctx, k_copy_vec, grid_for(8 * N, 256), 256, 0, s2, a.m_fr_in.limbs, N, tM);
-        // E2 = e~(u[d-n:], .) only (m == nullptr)
-        LAUNCH(ctx, k_tab_init, grid_for(N, 256), 256, 0, s2, (const uint32_t*)nullptr, N, tX, tB, sc, p.d, p.n,
-               a.variant, tE);
-    }
-    {
-        const uint32_t *cB = tB, *cT = Tsrc, *cM = tM, *cE = tE;
-        uint64_t len = N;
-        if (p.n == 0) LAUNCH(ctx, k_tab_fin0, 1, 32, 0, s2, cB, cT, cM, cE, tfin);
-        for (int k = 1; k <= p.n; ++k) {
-            const int pp = (k - 1) & 1;
-            uint32_t* nB = at<uint32_t>(ctx, p.o_tp[pp][0]);
-            uint32_t* nT = at<uint32_t>(ctx, p.o_tp[pp][1]);
-            uint32_t* nM = at<uint32_t>(ctx, p.o_tp[pp][2]);
-            uint32_t* nE = at<uint32_t>(ctx, p.o_tp[pp][3]);
-            LAUNCH(ctx, k_tab_round, p.tnb[k - 1], 256, 0, s2, cB, cT, cM, cE, len, nB, nT, nM, nE, sc, k, a.variant,
-                   tpart + (size_t)(k - 1) * 4 * kMaxBlocks, tfin);
-            cB = nB; cT = nT; cM = nM; cE = nE;
-            len /= 2;
-        }
-        if (p.n > 0) LAUNCH(ctx, k_reduce_tab, p.n, 256, 0, s2, tpart, tnb, p.n, tsum);
+        LAUNCH(ctx, k_tab_all, 1, 1024, 0, s2, a.B_in.limbs, Tsrc, (const uint32_t*)nullptr, a.m_fr_in.limbs, N, sc,
+               p.d, p.n, a.variant, at<fr>(ctx, p.o_twk), tsum, tfin, (uint32_t*)nullptr);
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join, s2));
 
@@ -515,7 +486,7 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
             // round 1 has one partial row per tile: reduce it on the aux stream while the rounds run
             CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fwd[0], s));
             CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->aux, ctx->ev_fwd[0], 0));
-            LAUNCH(ctx, k_reduce_rounds, 1, 1024, 0, ctx->aux, partials, rounds, 1, rank_sums);
+            LAUNCH(ctx, k_reduce_rounds, 1, 256, 0, ctx->aux, partials, rounds, 1, rank_sums);
             CUDA_TRY(ctx, cudaEventRecord(ctx->ev_mid[0], ctx->aux));
             r1_reduced = true;
         }
@@ -918,7 +889,16 @@ int zkl_table_create(zkl_ctx* ctx, zkl_vec T, void* mem, size_t mem_bytes, zkl_t
 void zkl_table_destroy(zkl_table* t) { free(t); }
 
 // ---------------------------------------------------------------- a3
-int zkl_tlookup_prepare(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T, uint32_t* m_dev, int64_t* err_index) {
+// Shared body of the two prepare entry points.  pair != nullptr: x, y (int32) are imported into S first,
+// fused with the index map.
+struct PairIn {
+    const int32_t* x;
+    const int32_t* y;
+    const zkl_fr* alpha_f;
+};
+
+static int prepare_impl(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T, uint32_t* m_dev, int64_t* err_index,
+                        const PairIn* pair) {
     int st;
     if (err_index) *err_index = -1;
     if ((st = check_ctx(ctx))) return st;
@@ -935,8 +915,21 @@ int zkl_tlookup_prepare(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T,
     CUDA_TRY(ctx, cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), ctx->stream));
     TableView tv{T->T, T->Taos, T->slots, T->N, T->slot_mask};
     uint32_t* keys = at<uint32_t>(ctx, p.o_keys);
-    LAUNCH(ctx, k_index_map, grid_for(p.Dp, 256, kSMs * 32), 256, 0, ctx->stream, S.limbs, p.Dp,
-           (uint64_t)ctx->rank * p.Dp, tv, keys, err);
+    if (pair) {
+        if (!pair->x || !pair->y || !pair->alpha_f) return set_err(ctx, ZKL_E_ARG, "null argument");
+        fr* af = reinterpret_cast<fr*>(ctx->dscratch + 64);
+        zkl_fr* staged = reinterpret_cast<zkl_fr*>((uint8_t*)ctx->host_out + 62000);
+        *staged = *pair->alpha_f;
+        CUDA_TRY(ctx, cudaMemcpyAsync(af, staged, sizeof(fr), cudaMemcpyHostToDevice, ctx->stream));
+        LAUNCH(ctx, k_import_canon, 1, 32, 0, ctx->stream, (const uint32_t*)af, 1, (uint32_t*)af,
+               (unsigned long long*)nullptr);
+        LAUNCH(ctx, k_pair_consts, 1, 32, 0, ctx->stream, af, af + 1);
+        LAUNCH(ctx, k_import_pair_index, grid_for(p.Dp, 256, kSMs * 32), 256, 0, ctx->stream, pair->x, pair->y, p.Dp,
+               af + 1, S.limbs, (uint64_t)ctx->rank * p.Dp, tv, keys, err);
+    } else {
+        LAUNCH(ctx, k_index_map, grid_for(p.Dp, 256, kSMs * 32), 256, 0, ctx->stream, S.limbs, p.Dp,
+               (uint64_t)ctx->rank * p.Dp, tv, keys, err);
+    }
     // key bits: n (+1 for the sentinel of a partial tile when D_local < 4096)
     const int key_bits = std::max(1, p.n + (p.Dp < (uint64_t)kHistTile ? 1 : 0));
     LAUNCH(ctx, k_hist_count, p.hist_rows, kHistThreads, 0, ctx->stream, keys, p.Dp, (uint32_t)T->N, rows, key_bits);
@@ -958,6 +951,16 @@ int zkl_tlookup_prepare(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T,
         return set_err(ctx, ZKL_E_NOT_IN_TABLE, "S_%llu is not in T", e);
     }
     return ZKL_OK;
+}
+
+int zkl_tlookup_prepare(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T, uint32_t* m_dev, int64_t* err_index) {
+    return prepare_impl(ctx, S, D, T, m_dev, err_index, nullptr);
+}
+
+int zkl_tlookup_prepare_pair(zkl_ctx* ctx, const int32_t* x_dev, const int32_t* y_dev, const zkl_fr* alpha_f,
+                             uint64_t D, const zkl_table* T, zkl_vec S_local_out, uint32_t* m_dev, int64_t* err_index) {
+    PairIn pin{x_dev, y_dev, alpha_f};
+    return prepare_impl(ctx, S_local_out, D, T, m_dev, err_index, &pin);
 }
 
 // ---------------------------------------------------------------- a4-a9

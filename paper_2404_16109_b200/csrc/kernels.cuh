@@ -195,6 +195,26 @@ k_index_map(const uint32_t* __restrict__ S, uint64_t n, uint64_t global_offset, 
     }
 }
 
+// a1 + a3(1) fused for function lookups: S = x + alpha_f y straight into Montgomery form,
+// stored, and its table index computed while it is still in registers.
+__global__ void __launch_bounds__(256)
+k_import_pair_index(const int32_t* __restrict__ x, const int32_t* __restrict__ y, uint64_t n,
+                    const fr* __restrict__ consts, uint32_t* __restrict__ dst, uint64_t global_offset, TableView tv,
+                    uint32_t* __restrict__ keys, unsigned long long* err) {
+    __shared__ fr c[4];
+    if (threadIdx.x < 4) c[threadIdx.x] = consts[threadIdx.x];
+    __syncthreads();
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const fr s = fr_from_small_pair(x[i], y[i], c);
+        st_fr(dst, n, i, s);
+        const int64_t f = table_find(tv, s);
+        uint32_t key = 0;
+        if (f < 0) atomic_min_i64(err, global_offset + i);
+        else key = (uint32_t)f;
+        keys[i] = key;
+    }
+}
+
 constexpr int kHistThreads = 512;
 constexpr int kHistItems = 8;
 constexpr int kHistTile = kHistThreads * kHistItems;   // 4096
@@ -214,8 +234,8 @@ k_hist_count(const uint32_t* __restrict__ keys_in, uint64_t n, uint32_t N, uint3
         const uint64_t base = tile * kHistTile;
         uint32_t keys[kHistItems];
 #pragma unroll
-        for (int g = 0; g < 2; ++g) {
-            const uint64_t i0 = base + 2048 * g + 4 * threadIdx.x;
+        for (int g = 0; g < kHistItems / 4; ++g) {
+            const uint64_t i0 = base + 4 * kHistThreads * g + 4 * threadIdx.x;
             if (i0 + 3 < n) {
                 const uint4 q = __ldg(reinterpret_cast<const uint4*>(keys_in + i0));
                 keys[4 * g] = q.x; keys[4 * g + 1] = q.y; keys[4 * g + 2] = q.z; keys[4 * g + 3] = q.w;
@@ -575,66 +595,98 @@ k_tail(const uint32_t* __restrict__ Ain, const uint32_t* __restrict__ Sin, uint6
 }
 
 // ====================================================================== a8: table side
-// B = 1/(beta + T) (or m/(beta+T), LOGUP) is produced by the inversion kernels; here:
-// Mf = m as field elements, E2 = e~(u[d-n:], .), and the rounds k <= n evaluated directly at
-// t = 0..3 (16 Fr muls per pair), folded with r_k.
-__global__ void k_tab_init(const uint32_t* __restrict__ m, uint64_t N, uint32_t* Mf, uint32_t* B,
-                           const ProofScalars* __restrict__ sc, int d, int nbits, int variant,
-                           uint32_t* E2) {
-    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < N; j += (uint64_t)gridDim.x * blockDim.x) {
-        if (m) {   // prove mode: m (u32) -> Fr; LOGUP: B <- m B
-            fr mv = fr_zero();
-            mv.v[0] = m[j];
-            mv = fr_to_mont(mv);
-            st_fr(Mf, N, j, mv);
-            if (variant == ZKL_VARIANT_LOGUP) st_fr(B, N, j, fr_mul(ld_fr(B, N, j), mv));
-        }
-        fr e = fr_one();
-        for (int b = 0; b < nbits; ++b) {
-            const fr u = sc->u[d - nbits + b];
-            const bool bit = (j >> (nbits - 1 - b)) & 1;
-            e = fr_mul(e, bit ? u : fr_sub(fr_one(), u));
-        }
-        st_fr(E2, N, j, e);
-    }
-}
-
+// The N-sized table term, all in ONE block on the low-priority side stream (it overlaps the D side and
+// occupies a single SM): build the working vectors B (LOGUP: m B), T, m, e~(u[d-n:], .) (eq table by the
+// doubling construction), then for rounds k = 1..n evaluate sum_y B_t (alpha2 e_t (T_t + beta) - m_t)
+// (LOGUP: -B_t + alpha2 e_t (B_t (T_t + beta) - m_t)) directly at t = 0..3 and fold with r_k.  The
+// D-repeated weight N/D cancels against the D/N repetitions (a8).  tab_sums[k-1][t];
+// tfin = the fully folded B, T, m, e.  wk: 8 N fr of scratch (two AoS buffers of 4 N).
 __device__ __forceinline__ fr tab_term(const fr& b, const fr& t, const fr& m, const fr& e, const fr& beta,
                                        const fr& alpha2, int variant) {
-    // PAPER: B (alpha2 e2 (T + beta) - m);  LOGUP: -B + alpha2 e2 (B (T + beta) - m)
     if (variant == ZKL_VARIANT_PAPER) return fr_mul(b, fr_sub(fr_mul(fr_mul(alpha2, e), fr_add(t, beta)), m));
     return fr_sub(fr_mul(fr_mul(alpha2, e), fr_sub(fr_mul(b, fr_add(t, beta)), m)), b);
 }
 
-__global__ void __launch_bounds__(256)
-k_tab_round(const uint32_t* __restrict__ Bo, const uint32_t* __restrict__ To, const uint32_t* __restrict__ Mo,
-            const uint32_t* __restrict__ Eo, uint64_t nold, uint32_t* Bn, uint32_t* Tn, uint32_t* Mn,
-            uint32_t* En, const ProofScalars* __restrict__ sc, int k, int variant, fr* partials, fr* fin) {
-    const fr beta = sc->beta, alpha2 = sc->alpha2, r = sc->r[k - 1];
-    const uint64_t np = nold / 2;
-    fr g[4] = {fr_zero(), fr_zero(), fr_zero(), fr_zero()};
-    for (uint64_t y = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; y < np; y += (uint64_t)gridDim.x * blockDim.x) {
-        fr b0 = ld_fr(Bo, nold, 2 * y), b1 = ld_fr(Bo, nold, 2 * y + 1);
-        fr t0 = ld_fr(To, nold, 2 * y), t1 = ld_fr(To, nold, 2 * y + 1);
-        fr m0 = ld_fr(Mo, nold, 2 * y), m1 = ld_fr(Mo, nold, 2 * y + 1);
-        fr e0 = ld_fr(Eo, nold, 2 * y), e1 = ld_fr(Eo, nold, 2 * y + 1);
-        const fr db = fr_sub(b1, b0), dt = fr_sub(t1, t0), dm = fr_sub(m1, m0), de = fr_sub(e1, e0);
-        fr bt = b0, tt = t0, mt = m0, et = e0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (q > 0) { bt = fr_add(bt, db); tt = fr_add(tt, dt); mt = fr_add(mt, dm); et = fr_add(et, de); }
-            g[q] = fr_add(g[q], tab_term(bt, tt, mt, et, beta, alpha2, variant));
+__global__ void __launch_bounds__(1024)
+k_tab_all(const uint32_t* __restrict__ Bin, const uint32_t* __restrict__ Tin, const uint32_t* __restrict__ m_u32,
+          const uint32_t* __restrict__ Mfin, uint64_t N, const ProofScalars* __restrict__ sc, int d, int nbits,
+          int variant, fr* wk, fr* tab_sums, fr* tfin, uint32_t* Bout) {
+    __shared__ fr scratch[4 * 32];
+    const int t = threadIdx.x, nt = blockDim.x;
+    fr* cur = wk;              // [B | T | M | E], N each
+    fr* nxt = wk + 4 * N;
+    // ---- working vectors
+    for (uint64_t j = t; j < N; j += nt) {
+        fr mv;
+        if (m_u32) {
+            mv = fr_zero();
+            mv.v[0] = m_u32[j];
+            mv = fr_to_mont(mv);
+        } else {
+            mv = ld_fr(Mfin, N, j);
         }
-        const fr nb = fr_add(b0, fr_mul(r, db)), ntt = fr_add(t0, fr_mul(r, dt));
-        const fr nm = fr_add(m0, fr_mul(r, dm)), ne = fr_add(e0, fr_mul(r, de));
-        st_fr(Bn, np, y, nb); st_fr(Tn, np, y, ntt); st_fr(Mn, np, y, nm); st_fr(En, np, y, ne);
-        if (np == 1) { fin[0] = nb; fin[1] = ntt; fin[2] = nm; fin[3] = ne; }
+        fr b = ld_fr(Bin, N, j);
+        if (m_u32 && variant == ZKL_VARIANT_LOGUP) b = fr_mul(b, mv);
+        if (Bout) st_fr(Bout, N, j, b);   // the variant's B, for the caller
+        cur[j] = b;
+        cur[N + j] = ld_fr(Tin, N, j);
+        cur[2 * N + j] = mv;
     }
-    __shared__ fr scratch[4 * 8];
-    block_sum_fr<4>(g, scratch);
-    if (threadIdx.x == 0) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) partials[q * kMaxBlocks + blockIdx.x] = g[q];
+    // e~(u[d-n:], .): E[j] over n bits, coordinate d-n+b at bit position (n-1-b) of j
+    fr* E = cur + 3 * N;
+    fr* E2 = nxt;              // scratch for the doubling
+    if (t == 0) E[0] = fr_one();
+    __syncthreads();
+    for (int c = 0; c < nbits; ++c) {
+        const uint64_t sz = 1ull << c;
+        const fr u = sc->u[d - nbits + c];
+        const fr um = fr_sub(fr_one(), u);
+        for (uint64_t j = t; j < sz; j += nt) {
+            const fr e = E[j];
+            E2[2 * j] = fr_mul(e, um);
+            E2[2 * j + 1] = fr_mul(e, u);
+        }
+        __syncthreads();
+        for (uint64_t j = t; j < 2 * sz; j += nt) E[j] = E2[j];
+        __syncthreads();
+    }
+    // ---- rounds
+    const fr beta = sc->beta, alpha2 = sc->alpha2;
+    uint64_t len = N;
+    for (int k = 1; k <= nbits; ++k) {
+        const uint64_t np = len / 2;
+        const fr r = sc->r[k - 1];
+        fr g[4] = {fr_zero(), fr_zero(), fr_zero(), fr_zero()};
+        for (uint64_t y = t; y < np; y += nt) {
+            const fr b0 = cur[2 * y], b1 = cur[2 * y + 1];
+            const fr t0 = cur[len + 2 * y], t1 = cur[len + 2 * y + 1];
+            const fr m0 = cur[2 * len + 2 * y], m1 = cur[2 * len + 2 * y + 1];
+            const fr e0 = cur[3 * len + 2 * y], e1 = cur[3 * len + 2 * y + 1];
+            const fr db = fr_sub(b1, b0), dt = fr_sub(t1, t0), dm = fr_sub(m1, m0), de = fr_sub(e1, e0);
+            fr bt = b0, tt = t0, mt = m0, et = e0;
+#pragma unroll 1
+            for (int q = 0; q < 4; ++q) {
+                if (q > 0) { bt = fr_add(bt, db); tt = fr_add(tt, dt); mt = fr_add(mt, dm); et = fr_add(et, de); }
+                g[q] = fr_add(g[q], tab_term(bt, tt, mt, et, beta, alpha2, variant));
+            }
+            nxt[y] = fr_add(b0, fr_mul(r, db));
+            nxt[np + y] = fr_add(t0, fr_mul(r, dt));
+            nxt[2 * np + y] = fr_add(m0, fr_mul(r, dm));
+            nxt[3 * np + y] = fr_add(e0, fr_mul(r, de));
+        }
+        block_sum_fr<4>(g, scratch);
+        if (t == 0) {
+            for (int q = 0; q < 4; ++q) tab_sums[(k - 1) * 4 + q] = g[q];
+        }
+        __syncthreads();
+        fr* tmp = cur; cur = nxt; nxt = tmp;
+        len = np;
+    }
+    if (t == 0) {
+        tfin[0] = cur[0];
+        tfin[1] = cur[len];
+        tfin[2] = cur[2 * len];
+        tfin[3] = cur[3 * len];
     }
 }
 
@@ -706,25 +758,6 @@ __global__ void k_reduce_rounds(const fr* __restrict__ partials, const RoundDesc
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int s = 0; s < 5; ++s) rank_sums[k * kSlots + s] = v[s];
-    }
-}
-
-__global__ void k_reduce_tab(const fr* __restrict__ tpart, const uint32_t* __restrict__ tnb, int nrounds, fr* tab_sums) {
-    __shared__ fr scratch[4 * 8];
-    const int k = blockIdx.x;
-    if (k >= nrounds) return;
-    const uint32_t nb = tnb[k];
-    fr v[4];
-#pragma unroll
-    for (int s = 0; s < 4; ++s) {
-        v[s] = fr_zero();
-        for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x)
-            v[s] = fr_add(v[s], tpart[((uint64_t)k * 4 + s) * kMaxBlocks + b]);
-    }
-    block_sum_fr<4>(v, scratch);
-    if (threadIdx.x == 0) {
-#pragma unroll
-        for (int s = 0; s < 4; ++s) tab_sums[k * 4 + s] = v[s];
     }
 }
 
@@ -913,13 +946,6 @@ __global__ void k_add_beta(const uint32_t* __restrict__ T, uint64_t N, const Pro
         const fr v = fr_add(ld_fr(T, N, j), sc->beta);
         if (fr_is_zero(v)) atomic_min_i64(err, j);
         st_fr(x, N, j, v);
-    }
-}
-
-// N = 1: the table vectors are already fully bound
-__global__ void k_tab_fin0(const uint32_t* B, const uint32_t* T, const uint32_t* M, const uint32_t* E, fr* fin) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        fin[0] = ld_fr(B, 1, 0); fin[1] = ld_fr(T, 1, 0); fin[2] = ld_fr(M, 1, 0); fin[3] = ld_fr(E, 1, 0);
     }
 }
 

@@ -84,6 +84,7 @@ def lib() -> ctypes.CDLL:
             "zkl_table_create": ([P, zkl_vec, P, ctypes.c_size_t, ctypes.POINTER(P), I64P], I32),
             "zkl_table_destroy": ([P], None),
             "zkl_tlookup_prepare": ([P, zkl_vec, U64, P, P, I64P], I32),
+            "zkl_tlookup_prepare_pair": ([P, P, P, ctypes.POINTER(zkl_fr), U64, P, zkl_vec, P, I64P], I32),
             "zkl_tlookup_prove": ([P, zkl_vec, U64, P, P, ctypes.POINTER(zkl_challenges), I32, zkl_vec, zkl_vec,
                                    ctypes.POINTER(zkl_fr), ctypes.POINTER(zkl_final_evals), I64P], I32),
             "zkl_sumcheck_prove": ([P, zkl_vec, zkl_vec, U64, zkl_vec, zkl_vec, zkl_vec,
@@ -103,7 +104,8 @@ EXPORTED = ["zkl_strerror", "zkl_ctx_create", "zkl_nccl_unique_id", "zkl_ctx_cre
             "zkl_last_error", "zkl_workspace_bytes", "zkl_ctx_set_workspace", "zkl_ctx_launch_count",
             "zkl_ctx_set_profiling", "zkl_ctx_profile_read",
             "zkl_vec_import", "zkl_vec_import_i64", "zkl_vec_import_pair", "zkl_vec_export", "zkl_table_bytes",
-            "zkl_table_create", "zkl_table_destroy", "zkl_tlookup_prepare", "zkl_tlookup_prove",
+            "zkl_table_create", "zkl_table_destroy", "zkl_tlookup_prepare", "zkl_tlookup_prepare_pair",
+            "zkl_tlookup_prove",
             "zkl_sumcheck_prove"]
 
 
@@ -310,6 +312,20 @@ class Context:
         st = lib().zkl_tlookup_prepare(self.h, S.c, D, tab.h, ctypes.c_void_p(m.data_ptr()), ctypes.byref(err))
         self._check(st, err.value)
         return m
+
+    def prepare_pair(self, x, y, alpha_f: int, D: int, tab: "Table", S: Optional[Vec] = None, m=None):
+        """a1 + a3 fused for function lookups: S = x + alpha_f y is written to S and counted into m."""
+        tx = x if hasattr(x, "data_ptr") else self.torch.as_tensor(np.asarray(x, np.int32)).to(self.device)
+        ty = y if hasattr(y, "data_ptr") else self.torch.as_tensor(np.asarray(y, np.int32)).to(self.device)
+        S = S or self.vec(tx.numel())
+        m = m if m is not None else self.torch.empty(tab.N, dtype=self.torch.int32, device=self.device)
+        af = fr_from_int(alpha_f % R_MODULUS)
+        err = ctypes.c_int64(-1)
+        st = lib().zkl_tlookup_prepare_pair(self.h, ctypes.c_void_p(tx.data_ptr()), ctypes.c_void_p(ty.data_ptr()),
+                                            ctypes.byref(af), D, tab.h, S.c, ctypes.c_void_p(m.data_ptr()),
+                                            ctypes.byref(err))
+        self._check(st, err.value)
+        return S, m
 
     # -- a4..a9
     @staticmethod

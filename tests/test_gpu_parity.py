@@ -112,6 +112,25 @@ def test_multiplicities_skew(ctx):
     assert list(m) == list(np.bincount(S, minlength=N))
 
 
+def test_prepare_pair_not_in_table(ctx):
+    zkl = zkl_mod()
+    D, N = 1 << 14, 1 << 8
+    ctx.reserve(D, N)
+    tx = np.arange(N, dtype=np.int32) - 128
+    ty = tx * 3 + 1
+    tab = ctx.table(ctx.import_pair(tx, ty, 12345))
+    rng = np.random.default_rng(1)
+    x = rng.integers(-128, 128, D).astype(np.int32)
+    y = (x * 3 + 1).astype(np.int32)
+    S, m = ctx.prepare_pair(x, y, 12345, D, tab)
+    assert list(m.cpu().numpy()) == list(np.bincount(x.astype(np.int64) + 128, minlength=N))
+    y[9000] += 1             # (x, y) no longer on the function's graph
+    y[12000] += 1
+    with pytest.raises(zkl.ZklError) as e:
+        ctx.prepare_pair(x, y, 12345, D, tab)
+    assert e.value.name == "ZKL_E_NOT_IN_TABLE" and e.value.index == 9000
+
+
 def test_not_in_table_and_dup(ctx):
     zkl = zkl_mod()
     D, N = 1 << 13, 1 << 6
@@ -268,10 +287,14 @@ def test_c2_activation_full(ctx, variant):
     ch = TL.challenges_from(wl.chal)
     ref = C.prove(S, T, C.chal_array(ch.beta, ch.alpha1, ch.alpha2, ch.u, ch.r), variant, want_A=False)
     ctx.reserve(wl.D, wl.N)
-    Sv = ctx.import_pair(wl.x, wl.y, wl.chal.alpha_f)
     Tv = ctx.import_pair(wl.tx, wl.ty, wl.chal.alpha_f)
     tab = ctx.table(Tv)
-    m = ctx.prepare(Sv, wl.D, tab)
+    if variant == TL.PAPER:      # the fused a1 + a3 entry point
+        Sv, m = ctx.prepare_pair(wl.x, wl.y, wl.chal.alpha_f, wl.D, tab)
+    else:
+        Sv = ctx.import_pair(wl.x, wl.y, wl.chal.alpha_f)
+        m = ctx.prepare(Sv, wl.D, tab)
+    assert ctx.export_ints(Sv) == C.limbs_to_ints(S)
     assert np.array_equal(m.cpu().numpy().astype(np.uint32), ref.m)
     pf = ctx.prove(Sv, wl.D, tab, m, _chal_gpu(ch), variant, want_B=True)
     assert ctx.export_ints(pf.B) == C.limbs_to_ints(ref.B)

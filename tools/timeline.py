@@ -18,8 +18,8 @@ txd, tyd = torch.from_numpy(wl.tx).to(dev), torch.from_numpy(wl.ty).to(dev)
 S, T, tmem = ctx.vec(D), ctx.vec(wl.N), ctx.table_mem(wl.N)
 m = torch.empty(wl.N, dtype=torch.int32, device=dev)
 def step():
-    ctx.import_pair(xd, yd, ch.alpha_f, S); ctx.import_pair(txd, tyd, ch.alpha_f, T)
-    tab = ctx.table(T, tmem); ctx.prepare(S, D, tab, m); return ctx.prove(S, D, tab, m, chal)
+    ctx.import_pair(txd, tyd, ch.alpha_f, T)
+    tab = ctx.table(T, tmem); ctx.prepare_pair(xd, yd, ch.alpha_f, D, tab, S, m); return ctx.prove(S, D, tab, m, chal)
 for _ in range(2): step()
 torch.cuda.synchronize()
 ctx.set_profiling(True)
