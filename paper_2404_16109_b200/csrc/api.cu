@@ -107,6 +107,7 @@ struct Plan {
     RoundDesc rd[kMaxRounds];
     EqJob jobs[2 * kMaxRounds];
     int njobs;
+    uint32_t tnb[kMaxRounds];
     uint64_t arena;
     uint64_t part_total;
     uint64_t ntiles;     // inversion tiles (Dp / 4096)
@@ -116,9 +117,9 @@ struct Plan {
     int inv_blocks;
     int hist_rows;
     // workspace offsets
-    size_t o_out, o_sc, o_err, o_rounds, o_jobs, o_chal, o_part, o_rank, o_gath, o_repl, o_tsum,
+    size_t o_out, o_sc, o_err, o_rounds, o_jobs, o_chal, o_part, o_tpart, o_tnb, o_rank, o_gath, o_repl, o_tsum,
         o_fin, o_tfin, o_gfin, o_rc, o_arena, o_hist, o_keys, o_tot, o_totinv, o_A, o_A1, o_S1, o_A2, o_S2, o_tB, o_tX, o_tM,
-        o_tE, o_twk, total;
+        o_tE, o_twk, o_tBaos, total;
 };
 
 void choose_round(Plan& p, int k, uint64_t npairs, int gbits, int nblocks) {
@@ -244,6 +245,10 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
     p.o_tM = take(soa_bytes(N));
     p.o_tE = take(soa_bytes(N));
     p.o_twk = take(sizeof(fr) * 8 * std::max<uint64_t>(N, 2));
+    for (int k = 1; k <= p.n; ++k) p.tnb[k - 1] = grid_for(N >> k, 256, kMaxBlocks);
+    p.o_tpart = take(sizeof(fr) * (size_t)kMaxRounds * 4 * kMaxBlocks);
+    p.o_tnb = take(sizeof(uint32_t) * kMaxRounds);
+    p.o_tBaos = take(32 * std::max<uint64_t>(N, 4));
     auto inv_levels = [&](InvPlan& ip, uint64_t n0) {
         ip.n[0] = n0;
         int L = 0;
@@ -356,6 +361,32 @@ int inv_backward0(zkl_ctx* ctx, const InvPlan& ip, const uint32_t* X0, uint64_t 
     return ZKL_OK;
 }
 
+// ------------------------------------------------------------------ table side (a8)
+// init + the big rounds multi-block on the main stream (a few tens of microseconds), the small rounds and
+// the reduction of all table rounds in one block on the side stream (joined before the derivation).
+int table_side(zkl_ctx* ctx, const Plan& p, cudaStream_t s, cudaStream_t s2, const uint32_t* B, const uint32_t* T,
+               const uint32_t* m_u32, const uint32_t* Mf, int variant, const ProofScalars* sc, fr* tsum, fr* tfin,
+               uint32_t* Bout) {
+    const uint64_t N = p.N;
+    fr* wk = at<fr>(ctx, p.o_twk);
+    fr *cur = wk, *nxt = wk + 4 * N;
+    LAUNCH(ctx, k_tab_init, grid_for(N, 256), 256, 0, s, B, T, m_u32, Mf, N, sc, p.d, p.n, variant, cur, Bout);
+    fr* tpart = at<fr>(ctx, p.o_tpart);
+    uint64_t len = N;
+    int k = 1;
+    for (; k <= p.n && len / 2 > kTabTailPairs; ++k) {
+        LAUNCH(ctx, k_tab_round, p.tnb[k - 1], 256, 0, s, cur, len, nxt, sc, k, variant,
+               tpart + (size_t)(k - 1) * 4 * kMaxBlocks);
+        fr* t = cur; cur = nxt; nxt = t;
+        len /= 2;
+    }
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, s));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(s2, ctx->ev_fork, 0));
+    LAUNCH(ctx, k_tab_tail, 1, 256, 0, s2, cur, nxt, len, k, p.n, sc, variant, tpart, kMaxBlocks,
+           at<uint32_t>(ctx, p.o_tnb), tsum, tfin);
+    return ZKL_OK;
+}
+
 // ------------------------------------------------------------------ shared proof driver
 struct ProveArgs {
     bool prove_mode;
@@ -365,6 +396,7 @@ struct ProveArgs {
     zkl_vec B_in, T_in, m_fr_in;         // sumcheck mode
     const zkl_challenges* ch;
     int variant;
+    bool force_inversion;                // prove mode: batch-invert beta + S instead of gathering B[j(i)]
 };
 
 int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals, zkl_final_evals* finals,
@@ -409,6 +441,7 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
         zkl_fr chal[3 + 2 * kMaxRounds];
         RoundDesc rounds[kMaxRounds];
         EqJob jobs[2 * kMaxRounds];
+        uint32_t tnb[kMaxRounds];
     };
     Staging* hs = reinterpret_cast<Staging*>((uint8_t*)ctx->host_out + sizeof(ProofOut));
     hs->chal[0] = a.ch->beta;
@@ -418,9 +451,11 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
     for (int k = 0; k < p.d; ++k) hs->chal[3 + p.d + k] = a.ch->r[k];
     memcpy(hs->rounds, p.rd, sizeof(p.rd));
     memcpy(hs->jobs, p.jobs, sizeof(p.jobs));
+    memcpy(hs->tnb, p.tnb, sizeof(p.tnb));
     CUDA_TRY(ctx, cudaMemcpyAsync(chal, hs->chal, sizeof(hs->chal), cudaMemcpyHostToDevice, s));
     CUDA_TRY(ctx, cudaMemcpyAsync(rounds, hs->rounds, sizeof(hs->rounds), cudaMemcpyHostToDevice, s));
     CUDA_TRY(ctx, cudaMemcpyAsync(jobs, hs->jobs, sizeof(hs->jobs), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(at<uint32_t>(ctx, p.o_tnb), hs->tnb, sizeof(hs->tnb), cudaMemcpyHostToDevice, s));
     CUDA_TRY(ctx, cudaMemsetAsync(err, 0xff, 4 * sizeof(unsigned long long), s));
     LAUNCH(ctx, k_setup, 1, 1, 0, s, chal, p.d, p.pbits, p.rank, N, D, sc);
     LAUNCH(ctx, k_eq_fill, grid_for(p.arena, 256), 256, 0, s, jobs, p.njobs, p.arena, sc, arena);
@@ -435,21 +470,26 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
     uint32_t* tM = at<uint32_t>(ctx, p.o_tM);
     uint32_t* tE = at<uint32_t>(ctx, p.o_tE);
     const uint32_t* Tsrc = a.prove_mode ? a.table->T : a.T_in.limbs;
+    // the gather path (A_i = B_j(i)) needs B on the critical path: compute it on the main stream first
+    const bool gather = a.prove_mode && !p.small && !a.force_inversion;
     if (a.prove_mode) {
+        cudaStream_t sb = s;   // B feeds both the table side and (gather path) the D side
         if (N >= (uint64_t)kInvTile) {
-            if ((st = inv_forward(ctx, p.tinv, Tsrc, N, tB, sc, 0, err + 1, s2, s2, nullptr))) return st;
-            if ((st = inv_backward0(ctx, p.tinv, Tsrc, N, tB, sc, nullptr, nullptr, nullptr, 0, s2))) return st;
+            if ((st = inv_forward(ctx, p.tinv, Tsrc, N, tB, sc, 0, err + 1, sb, sb, nullptr))) return st;
+            if ((st = inv_backward0(ctx, p.tinv, Tsrc, N, tB, sc, nullptr, nullptr, nullptr, 0, sb))) return st;
         } else {
-            LAUNCH(ctx, k_add_beta, grid_for(N, 256), 256, 0, s2, Tsrc, N, sc, tX, err + 1);
+            LAUNCH(ctx, k_add_beta, grid_for(N, 256), 256, 0, sb, Tsrc, N, sc, tX, err + 1);
             const unsigned bt = (unsigned)std::min<uint64_t>(1024, std::max<uint64_t>(32, N));
-            LAUNCH(ctx, k_batch_invert, 1, bt, 4 * bt * sizeof(fr), s2, tX, N, (uint64_t)0, N, tB);
+            LAUNCH(ctx, k_batch_invert, 1, bt, 4 * bt * sizeof(fr), sb, tX, N, (uint64_t)0, N, tB);
         }
-        // B_out (if requested) is the variant's B, written by k_tab_all
-        LAUNCH(ctx, k_tab_all, 1, 1024, 0, s2, tB, Tsrc, a.m_dev, (const uint32_t*)nullptr, N, sc, p.d, p.n,
-               a.variant, at<fr>(ctx, p.o_twk), tsum, tfin, a.B_out.limbs);
+        if (gather) LAUNCH(ctx, k_soa_to_aos, grid_for(N, 256), 256, 0, s, tB, N, at<uint4>(ctx, p.o_tBaos));
+        // B_out (if requested) is the variant's B, written by k_tab_init
+        if ((st = table_side(ctx, p, s, s2, tB, Tsrc, a.m_dev, nullptr, a.variant, sc, tsum, tfin, a.B_out.limbs)))
+            return st;
     } else {
-        LAUNCH(ctx, k_tab_all, 1, 1024, 0, s2, a.B_in.limbs, Tsrc, (const uint32_t*)nullptr, a.m_fr_in.limbs, N, sc,
-               p.d, p.n, a.variant, at<fr>(ctx, p.o_twk), tsum, tfin, (uint32_t*)nullptr);
+        if ((st = table_side(ctx, p, s, s2, a.B_in.limbs, Tsrc, nullptr, a.m_fr_in.limbs, a.variant, sc, tsum, tfin,
+                             nullptr)))
+            return st;
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join, s2));
 
@@ -465,7 +505,19 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
         LAUNCH(ctx, k_tail, 1, kTailThreads, tail_smem, s, A1in, S1in, p.Dp, 0, a.prove_mode ? 1 : 0, Abuf,
                errS_off, err, sc, 1, p.dl, rounds, arena, partials, fin);
     } else {
-        if (a.prove_mode) {
+        if (gather) {
+            // a4 + a5 through the table: A_i = B_j(i), one block per 4096-element tile (partial row = tile)
+            TableView tv{a.table->T, a.table->Taos, a.table->slots, a.table->N, a.table->slot_mask};
+            LAUNCH(ctx, k_gather_round1, (unsigned)p.ntiles, kInvThreads, 0, s, a.S.limbs, p.Dp, tv,
+                   at<uint4>(ctx, p.o_tBaos), Abuf, arena + p.rd[0].elo_off, arena + p.rd[0].ehi_off,
+                   partials + p.rd[0].part_base, (int)p.ntiles, err + 2);
+            rounds_nb0 = (int)p.ntiles;
+            CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fwd[0], s));
+            CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->aux, ctx->ev_fwd[0], 0));
+            LAUNCH(ctx, k_reduce_rounds, 1, 256, 0, ctx->aux, partials, rounds, 1, rank_sums);
+            CUDA_TRY(ctx, cudaEventRecord(ctx->ev_mid[0], ctx->aux));
+            r1_reduced = true;
+        } else if (a.prove_mode) {
             // hierarchical batched inversion in two halves: the upper levels + one-block top (one Fermat) of
             // half h run on the aux stream while the main stream does the level-0 forward pass of the other
             // half (h = 0) or the level-0 backward pass of half 0 (h = 1), hiding their latency.
@@ -543,14 +595,22 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
            a.variant, a.prove_mode ? 1 : 0, fin, tfin, out);
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->host_out, out, sizeof(ProofOut), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(ctx, cudaMemcpyAsync((uint8_t*)ctx->host_out + offsetof(ProofOut, err_index), err,
-                                  2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+                                  3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     if ((st = sync_stream(ctx))) return st;
     const ProofOut* ho = reinterpret_cast<const ProofOut*>(ctx->host_out);
-    const unsigned long long* he = reinterpret_cast<const unsigned long long*>(&ho->err_index);
-    unsigned long long eS = he[0], eT = he[1];
+    const unsigned long long* he = reinterpret_cast<const unsigned long long*>((const uint8_t*)ctx->host_out +
+                                                                               offsetof(ProofOut, err_index));
+    unsigned long long eS = he[0], eT = he[1], eMiss = gather ? he[2] : ~0ull;
     if (ctx->nranks > 1) {
         int rc = zkl_dist_min_u64(ctx, &eS);
         if (rc) return rc;
+        if (gather && (rc = zkl_dist_min_u64(ctx, &eMiss))) return rc;
+    }
+    if (eMiss != ~0ull && eT == ~0ull) {
+        // an S_i with no table entry (S was not the prepared lookup vector): redo with the inversion path
+        ProveArgs b = a;
+        b.force_inversion = true;
+        return run_proof(ctx, D, b, round_evals, finals, err_index);
     }
     if (eT != ~0ull) {
         if (err_index) *err_index = (int64_t)eT;
@@ -602,7 +662,7 @@ static int ctx_create_common(int device, void* stream, zkl_ctx** out) {
     c->nranks = 1;
     if (cudaSetDevice(device) != cudaSuccess ||
         cudaDeviceGetStreamPriorityRange(&c->prio_lo, &c->prio_hi) != cudaSuccess ||
-        cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, c->prio_lo) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, c->prio_hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, c->prio_hi) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fwd[0], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fwd[1], cudaEventDisableTiming) != cudaSuccess ||

@@ -127,7 +127,7 @@ struct ProofScalars {
 struct ProofOut {
     zkl_fr evals[kMaxRounds][4];
     zkl_fr finals[5];
-    unsigned long long err_index;   // atomicMin target (ULLONG_MAX = none)
+    unsigned long long err_index[3];   // host copies of the error words: S div0, T div0, gather miss
     int status;
     int pad;
 };
@@ -155,7 +155,7 @@ struct zkl_group {
 struct zkl_ctx {
     int device;
     cudaStream_t stream;
-    cudaStream_t side;             // table-side work overlapping the D side
+    cudaStream_t side;             // table-side work overlapping the D side (high priority, one block)
     cudaStream_t aux;              // upper inversion levels (high priority, latency hidden behind the D side)
     int prio_lo, prio_hi;
     cudaEvent_t ev_fork, ev_join;

@@ -204,6 +204,43 @@ k_import_pair_index(const int32_t* __restrict__ x, const int32_t* __restrict__ y
     __shared__ fr c[4];
     if (threadIdx.x < 4) c[threadIdx.x] = consts[threadIdx.x];
     __syncthreads();
+    if ((n & 3) == 0) {
+        // 4 consecutive elements per thread: 128-bit loads of x, y; 128-bit stores per limb plane; 4 hash
+        // probes in flight together
+        for (uint64_t i = 4 * (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x); i < n;
+             i += 4 * (uint64_t)gridDim.x * blockDim.x) {
+            const int4 xv = __ldg(reinterpret_cast<const int4*>(x + i));
+            const int4 yv = __ldg(reinterpret_cast<const int4*>(y + i));
+            fr s[4];
+            s[0] = fr_from_small_pair(xv.x, yv.x, c);
+            s[1] = fr_from_small_pair(xv.y, yv.y, c);
+            s[2] = fr_from_small_pair(xv.z, yv.z, c);
+            s[3] = fr_from_small_pair(xv.w, yv.w, c);
+            st_fr4(dst, n, i, s);
+            uint32_t h[4], slot[4], kk[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) h[q] = hash_fr(s[q]) & tv.mask;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) slot[q] = __ldg(tv.slots + h[q]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                bool ok = slot[q] != 0 && aos_eq(tv.Taos + 2 * (uint64_t)(slot[q] - 1), s[q]);
+                uint32_t key = slot[q] - 1;
+                if (!ok && slot[q] != 0) {                 // collision: keep probing
+                    const int64_t f = table_find(tv, s[q]);
+                    ok = f >= 0;
+                    key = (uint32_t)f;
+                }
+                if (!ok) {
+                    atomic_min_i64(err, global_offset + i + q);
+                    key = 0;
+                }
+                kk[q] = key;
+            }
+            *reinterpret_cast<uint4*>(keys + i) = make_uint4(kk[0], kk[1], kk[2], kk[3]);
+        }
+        return;
+    }
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const fr s = fr_from_small_pair(x[i], y[i], c);
         st_fr(dst, n, i, s);
@@ -324,11 +361,13 @@ k_inv_fwd(const uint32_t* __restrict__ X, uint64_t n, const ProofScalars* __rest
     for (uint64_t tile = t0 + blockIdx.x; tile < t1; tile += gridDim.x) {
         const uint64_t base = tile * kInvTile + 2 * threadIdx.x;
         fr p = fr_zero();
+        fr xn[2];
+        ld_fr2(X, n, base, xn);
 #pragma unroll 1
         for (int g = 0; g < 8; ++g) {
             const uint64_t i0 = base + 512 * g;
-            fr x[2];
-            ld_fr2(X, n, i0, x);
+            fr x[2] = {xn[0], xn[1]};
+            if (g < 7) ld_fr2(X, n, i0 + 512, xn);   // prefetch the next step
             if (LEVEL0) {
                 x[0] = fr_add(x[0], beta);
                 x[1] = fr_add(x[1], beta);
@@ -421,6 +460,68 @@ k_inv_bwd(const uint32_t* __restrict__ X, uint64_t n, const ProofScalars* __rest
             partials[SLOT_A0 * rows + row] = v[1];
             partials[SLOT_A1 * rows + row] = v[2];
         }
+    }
+}
+
+// ---------------------------------------------------------------------- a4 via the table (gather path)
+// Every S_i is a table entry T_j (a3 checked it), so A_i = 1/(beta + S_i) = 1/(beta + T_j) = B_j: the D-sized
+// batch inversion is replaced by N inversions (B, computed first) and a gather through the hash index.
+// Same tile / thread layout as k_inv_bwd<true>, and the same fused round-1 evaluation (a5).  An S_i with
+// no table entry (possible only when prove is called on an S that was not prepared, e.g. a tamper trial)
+// sets *miss; the host then redoes the proof with the inversion path (bit-identical A by definition).
+__device__ __forceinline__ fr ld_aos_fr(const uint4* p) {
+    const uint4 a = __ldg(p), b = __ldg(p + 1);
+    fr x;
+    x.v[0] = a.x; x.v[1] = a.y; x.v[2] = a.z; x.v[3] = a.w;
+    x.v[4] = b.x; x.v[5] = b.y; x.v[6] = b.z; x.v[7] = b.w;
+    return x;
+}
+
+__global__ void __launch_bounds__(kInvThreads)
+k_gather_round1(const uint32_t* __restrict__ S, uint64_t n, TableView tv, const uint4* __restrict__ Baos,
+                uint32_t* __restrict__ Aout, const fr* __restrict__ elo, const fr* __restrict__ ehi, fr* partials,
+                int rows, unsigned long long* miss) {
+    fr acc = fr_zero(), a0 = fr_zero(), a1 = fr_zero();
+    const uint64_t tile = blockIdx.x;
+    const uint64_t base = tile * kInvTile + 2 * threadIdx.x;
+#pragma unroll 1
+    for (int g = 0; g < 8; ++g) {
+        const uint64_t i0 = base + 512 * g;
+        fr x[2];
+        ld_fr2(S, n, i0, x);
+        uint32_t h0 = hash_fr(x[0]) & tv.mask, h1 = hash_fr(x[1]) & tv.mask;
+        uint32_t s0 = __ldg(tv.slots + h0), s1 = __ldg(tv.slots + h1);
+        int64_t j0 = (s0 != 0 && aos_eq(tv.Taos + 2 * (uint64_t)(s0 - 1), x[0])) ? (int64_t)(s0 - 1) : -2;
+        int64_t j1 = (s1 != 0 && aos_eq(tv.Taos + 2 * (uint64_t)(s1 - 1), x[1])) ? (int64_t)(s1 - 1) : -2;
+        if (j0 == -2) j0 = s0 ? table_find(tv, x[0]) : -1;
+        if (j1 == -2) j1 = s1 ? table_find(tv, x[1]) : -1;
+        if (j0 < 0 || j1 < 0) {
+            atomic_min_i64(miss, i0);
+            j0 = j0 < 0 ? 0 : j0;
+            j1 = j1 < 0 ? 0 : j1;
+        }
+        const fr A0 = ld_aos_fr(Baos + 2 * j0), A1 = ld_aos_fr(Baos + 2 * j1);
+        st_fr2(Aout, n, i0, A0, A1);
+        const fr dA = fr_sub(A1, A0), dS = fr_sub(x[1], x[0]);
+        acc = fr_add(acc, fr_mul(elo[256 * g + threadIdx.x], fr_mul(dA, dS)));
+        a0 = fr_add(a0, A0);
+        a1 = fr_add(a1, A1);
+    }
+    fr v[3] = {fr_mul(ehi[tile], acc), a0, a1};
+    __shared__ fr scratch[3 * (kInvThreads / 32)];
+    block_sum_fr<3>(v, scratch);
+    if (threadIdx.x == 0) {
+        partials[SLOT_HINF * rows + tile] = v[0];
+        partials[SLOT_A0 * rows + tile] = v[1];
+        partials[SLOT_A1 * rows + tile] = v[2];
+    }
+}
+
+__global__ void k_soa_to_aos(const uint32_t* __restrict__ src, uint64_t n, uint4* __restrict__ dst) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const fr x = ld_fr(src, n, i);
+        dst[2 * i] = make_uint4(x.v[0], x.v[1], x.v[2], x.v[3]);
+        dst[2 * i + 1] = make_uint4(x.v[4], x.v[5], x.v[6], x.v[7]);
     }
 }
 
@@ -607,16 +708,15 @@ __device__ __forceinline__ fr tab_term(const fr& b, const fr& t, const fr& m, co
     return fr_sub(fr_mul(fr_mul(alpha2, e), fr_sub(fr_mul(b, fr_add(t, beta)), m)), b);
 }
 
-__global__ void __launch_bounds__(1024)
-k_tab_all(const uint32_t* __restrict__ Bin, const uint32_t* __restrict__ Tin, const uint32_t* __restrict__ m_u32,
-          const uint32_t* __restrict__ Mfin, uint64_t N, const ProofScalars* __restrict__ sc, int d, int nbits,
-          int variant, fr* wk, fr* tab_sums, fr* tfin, uint32_t* Bout) {
-    __shared__ fr scratch[4 * 32];
-    const int t = threadIdx.x, nt = blockDim.x;
-    fr* cur = wk;              // [B | T | M | E], N each
-    fr* nxt = wk + 4 * N;
-    // ---- working vectors
-    for (uint64_t j = t; j < N; j += nt) {
+// Big table rounds run multi-block on the main stream (pairs > kTabTailPairs), the rest in one block on the
+// side stream.  Working vectors are AoS: [B | T | M | E] with stride len.
+constexpr uint64_t kTabTailPairs = 4096;
+
+__global__ void k_tab_init(const uint32_t* __restrict__ Bin, const uint32_t* __restrict__ Tin,
+                           const uint32_t* __restrict__ m_u32, const uint32_t* __restrict__ Mfin, uint64_t N,
+                           const ProofScalars* __restrict__ sc, int d, int nbits, int variant, fr* cur,
+                           uint32_t* Bout) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < N; j += (uint64_t)gridDim.x * blockDim.x) {
         fr mv;
         if (m_u32) {
             mv = fr_zero();
@@ -631,53 +731,76 @@ k_tab_all(const uint32_t* __restrict__ Bin, const uint32_t* __restrict__ Tin, co
         cur[j] = b;
         cur[N + j] = ld_fr(Tin, N, j);
         cur[2 * N + j] = mv;
-    }
-    // e~(u[d-n:], .): E[j] over n bits, coordinate d-n+b at bit position (n-1-b) of j
-    fr* E = cur + 3 * N;
-    fr* E2 = nxt;              // scratch for the doubling
-    if (t == 0) E[0] = fr_one();
-    __syncthreads();
-    for (int c = 0; c < nbits; ++c) {
-        const uint64_t sz = 1ull << c;
-        const fr u = sc->u[d - nbits + c];
-        const fr um = fr_sub(fr_one(), u);
-        for (uint64_t j = t; j < sz; j += nt) {
-            const fr e = E[j];
-            E2[2 * j] = fr_mul(e, um);
-            E2[2 * j + 1] = fr_mul(e, u);
+        // e~(u[d-n:], j): coordinate d-n+b at bit position n-1-b of j
+        fr e = fr_one();
+        for (int c = 0; c < nbits; ++c) {
+            const fr u = sc->u[d - nbits + c];
+            e = fr_mul(e, ((j >> (nbits - 1 - c)) & 1) ? u : fr_sub(fr_one(), u));
         }
-        __syncthreads();
-        for (uint64_t j = t; j < 2 * sz; j += nt) E[j] = E2[j];
-        __syncthreads();
+        cur[3 * N + j] = e;
     }
-    // ---- rounds
-    const fr beta = sc->beta, alpha2 = sc->alpha2;
-    uint64_t len = N;
-    for (int k = 1; k <= nbits; ++k) {
-        const uint64_t np = len / 2;
-        const fr r = sc->r[k - 1];
-        fr g[4] = {fr_zero(), fr_zero(), fr_zero(), fr_zero()};
-        for (uint64_t y = t; y < np; y += nt) {
-            const fr b0 = cur[2 * y], b1 = cur[2 * y + 1];
-            const fr t0 = cur[len + 2 * y], t1 = cur[len + 2 * y + 1];
-            const fr m0 = cur[2 * len + 2 * y], m1 = cur[2 * len + 2 * y + 1];
-            const fr e0 = cur[3 * len + 2 * y], e1 = cur[3 * len + 2 * y + 1];
-            const fr db = fr_sub(b1, b0), dt = fr_sub(t1, t0), dm = fr_sub(m1, m0), de = fr_sub(e1, e0);
-            fr bt = b0, tt = t0, mt = m0, et = e0;
-#pragma unroll 1
-            for (int q = 0; q < 4; ++q) {
-                if (q > 0) { bt = fr_add(bt, db); tt = fr_add(tt, dt); mt = fr_add(mt, dm); et = fr_add(et, de); }
-                g[q] = fr_add(g[q], tab_term(bt, tt, mt, et, beta, alpha2, variant));
-            }
-            nxt[y] = fr_add(b0, fr_mul(r, db));
-            nxt[np + y] = fr_add(t0, fr_mul(r, dt));
-            nxt[2 * np + y] = fr_add(m0, fr_mul(r, dm));
-            nxt[3 * np + y] = fr_add(e0, fr_mul(r, de));
+}
+
+// one table round over `len` entries: direct evaluation at t = 0..3 and fold with r_k; per-block partials
+__device__ __forceinline__ void tab_pair(const fr* cur, uint64_t len, uint64_t y, fr* nxt, const fr& r, const fr& beta,
+                                         const fr& alpha2, int variant, fr (&g)[4]) {
+    const uint64_t np = len / 2;
+    const fr b0 = cur[2 * y], b1 = cur[2 * y + 1];
+    const fr t0 = cur[len + 2 * y], t1 = cur[len + 2 * y + 1];
+    const fr m0 = cur[2 * len + 2 * y], m1 = cur[2 * len + 2 * y + 1];
+    const fr e0 = cur[3 * len + 2 * y], e1 = cur[3 * len + 2 * y + 1];
+    const fr db = fr_sub(b1, b0), dt = fr_sub(t1, t0), dm = fr_sub(m1, m0), de = fr_sub(e1, e0);
+    fr bt = b0, tt = t0, mt = m0, et = e0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if (q > 0) { bt = fr_add(bt, db); tt = fr_add(tt, dt); mt = fr_add(mt, dm); et = fr_add(et, de); }
+        g[q] = fr_add(g[q], tab_term(bt, tt, mt, et, beta, alpha2, variant));
+    }
+    nxt[y] = fr_add(b0, fr_mul(r, db));
+    nxt[np + y] = fr_add(t0, fr_mul(r, dt));
+    nxt[2 * np + y] = fr_add(m0, fr_mul(r, dm));
+    nxt[3 * np + y] = fr_add(e0, fr_mul(r, de));
+}
+
+__global__ void __launch_bounds__(256)
+k_tab_round(const fr* __restrict__ cur, uint64_t len, fr* nxt, const ProofScalars* __restrict__ sc, int k, int variant,
+            fr* tpart) {
+    const fr beta = sc->beta, alpha2 = sc->alpha2, r = sc->r[k - 1];
+    fr g[4] = {fr_zero(), fr_zero(), fr_zero(), fr_zero()};
+    for (uint64_t y = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; y < len / 2; y += (uint64_t)gridDim.x * blockDim.x)
+        tab_pair(cur, len, y, nxt, r, beta, alpha2, variant, g);
+    __shared__ fr scratch[4 * 8];
+    block_sum_fr<4>(g, scratch);
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < 4; ++q) tpart[q * kMaxBlocks + blockIdx.x] = g[q];   // row stride kMaxBlocks
+    }
+}
+
+// The remaining table rounds k0..n in one block; also reduces the partial rows of the big rounds.
+// tpart: rounds 1..k0-1, round k at tpart + (k-1) * 4 * rows_max, [q][blk], tnb[k-1] blocks.
+__global__ void __launch_bounds__(256)
+k_tab_tail(fr* cur, fr* nxt, uint64_t len, int k0, int nbits, const ProofScalars* __restrict__ sc, int variant,
+           const fr* __restrict__ tpart, int rows_max, const uint32_t* __restrict__ tnb, fr* tab_sums, fr* tfin) {
+    __shared__ fr scratch[4 * 8];
+    const int t = threadIdx.x, nt = blockDim.x;
+    for (int k = 1; k < k0; ++k) {
+        fr g[4];
+        for (int q = 0; q < 4; ++q) {
+            g[q] = fr_zero();
+            for (uint32_t b = t; b < tnb[k - 1]; b += nt) g[q] = fr_add(g[q], tpart[((uint64_t)(k - 1) * 4 + q) * rows_max + b]);
         }
         block_sum_fr<4>(g, scratch);
-        if (t == 0) {
+        if (t == 0)
             for (int q = 0; q < 4; ++q) tab_sums[(k - 1) * 4 + q] = g[q];
-        }
+    }
+    const fr beta = sc->beta, alpha2 = sc->alpha2;
+    for (int k = k0; k <= nbits; ++k) {
+        const uint64_t np = len / 2;
+        fr g[4] = {fr_zero(), fr_zero(), fr_zero(), fr_zero()};
+        for (uint64_t y = t; y < np; y += nt) tab_pair(cur, len, y, nxt, sc->r[k - 1], beta, alpha2, variant, g);
+        block_sum_fr<4>(g, scratch);
+        if (t == 0)
+            for (int q = 0; q < 4; ++q) tab_sums[(k - 1) * 4 + q] = g[q];
         __syncthreads();
         fr* tmp = cur; cur = nxt; nxt = tmp;
         len = np;

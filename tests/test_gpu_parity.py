@@ -264,6 +264,36 @@ def test_div_zero(ctx):
     assert e.value.name == "ZKL_E_DIV_ZERO_S" and e.value.index == 1234
 
 
+@pytest.mark.parametrize("variant", [TL.PAPER, TL.LOGUP])
+def test_prove_unprepared_nonmember_falls_back(ctx, variant):
+    """prove on an S with an element outside T (a tamper trial): the gather path A_i = B_j(i) cannot apply,
+    the library redoes the proof with the batched inversion; the transcript is that of the given data."""
+    rng = random.Random(31 + variant)
+    d, n = 14, 5
+    D, N = 1 << d, 1 << n
+    T = [rng.randrange(R) for _ in range(N)]
+    S = [T[rng.randrange(N)] for _ in range(D)]
+    ch = TL.Challenges(rng.randrange(R), rng.randrange(R), 0, [rng.randrange(R) for _ in range(d)],
+                       [rng.randrange(R) for _ in range(d)])
+    ch.alpha2 = ch.alpha1 ** 2 % R
+    ctx.reserve(D, N)
+    _, tab = _table_from_ints(ctx, T)
+    m = ctx.prepare(ctx.import_canon(_canon(S)), D, tab)
+    bad = list(S)
+    bad[777] = rng.randrange(R)
+    pf = ctx.prove(ctx.import_canon(_canon(bad)), D, tab, m, _chal_gpu(ch), variant, want_A=True, want_B=True)
+    mm = m.cpu().numpy().astype(np.uint32)
+    A = [pow((ch.beta + s) % R, -1, R) for s in bad]
+    B = [pow((ch.beta + t) % R, -1, R) for t in T]
+    if variant == TL.LOGUP:
+        B = [b * int(c) % R for b, c in zip(B, mm)]
+    ref = C.sumcheck(*(C.ints_to_limbs(v) for v in (A, bad, B, T)), mm,
+                     C.chal_array(ch.beta, ch.alpha1, ch.alpha2, ch.u, ch.r), variant)
+    assert ctx.export_ints(pf.A) == A
+    assert ctx.export_ints(pf.B) == B
+    assert pf.evals == ref.evals and pf.finals == ref.finals
+
+
 def test_shape_errors(ctx):
     zkl = zkl_mod()
     ctx.reserve(1 << 10, 1 << 4)
@@ -300,3 +330,21 @@ def test_c2_activation_full(ctx, variant):
     assert ctx.export_ints(pf.B) == C.limbs_to_ints(ref.B)
     assert pf.evals == ref.evals
     assert pf.finals == ref.finals
+
+
+@pytest.mark.parametrize("variant", [TL.PAPER, TL.LOGUP])
+def test_big_table_rounds(ctx, variant):
+    """N = 2^14 (> 2 x 4096 pairs): the multi-block table rounds on the main stream + the one-block tail."""
+    rng = random.Random(4242 + variant)
+    d, n = 15, 14
+    D, N = 1 << d, 1 << n
+    T = [rng.randrange(R) for _ in range(N)]
+    S = [T[rng.randrange(N)] for _ in range(D)]
+    ch = TL.Challenges(rng.randrange(R), rng.randrange(R), 0, [rng.randrange(R) for _ in range(d)],
+                       [rng.randrange(R) for _ in range(d)])
+    ch.alpha2 = ch.alpha1 ** 2 % R
+    m, pf = _gpu_prove(ctx, S, T, ch, variant, D, N)
+    ref = C.prove(C.ints_to_limbs(S), C.ints_to_limbs(T), C.chal_array(ch.beta, ch.alpha1, ch.alpha2, ch.u, ch.r),
+                  variant)
+    assert ctx.export_ints(pf.B) == C.limbs_to_ints(ref.B)
+    assert pf.evals == ref.evals and pf.finals == ref.finals
