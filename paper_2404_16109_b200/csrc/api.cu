@@ -508,9 +508,17 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
         if (gather) {
             // a4 + a5 through the table: A_i = B_j(i), one block per 4096-element tile (partial row = tile)
             TableView tv{a.table->T, a.table->Taos, a.table->slots, a.table->N, a.table->slot_mask};
-            LAUNCH(ctx, k_gather_round1, (unsigned)p.ntiles, kInvThreads, 0, s, a.S.limbs, p.Dp, tv,
-                   at<uint4>(ctx, p.o_tBaos), Abuf, arena + p.rd[0].elo_off, arena + p.rd[0].ehi_off,
-                   partials + p.rd[0].part_base, (int)p.ntiles, err + 2);
+            if (ctx->prep_S == a.S.limbs && ctx->prep_n == p.Dp && ctx->prep_table == a.table) {
+                // keys from the preceding prepare on this S (each still verified against T)
+                LAUNCH(ctx, k_gather_keys_round1, (unsigned)p.ntiles, kInvThreads, 0, s, a.S.limbs, p.Dp,
+                       at<uint32_t>(ctx, p.o_keys), a.table->Taos, N, at<uint4>(ctx, p.o_tBaos), Abuf,
+                       arena + p.rd[0].elo_off, arena + p.rd[0].ehi_off, partials + p.rd[0].part_base,
+                       (int)p.ntiles, err + 2);
+            } else {
+                LAUNCH(ctx, k_gather_round1, (unsigned)p.ntiles, kInvThreads, 0, s, a.S.limbs, p.Dp, tv,
+                       at<uint4>(ctx, p.o_tBaos), Abuf, arena + p.rd[0].elo_off, arena + p.rd[0].ehi_off,
+                       partials + p.rd[0].part_base, (int)p.ntiles, err + 2);
+            }
             rounds_nb0 = (int)p.ntiles;
             CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fwd[0], s));
             CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->aux, ctx->ev_fwd[0], 0));
@@ -779,6 +787,7 @@ int zkl_ctx_set_workspace(zkl_ctx* c, void* ptr, size_t bytes) {
     if (((uintptr_t)ptr) & 255) return set_err(c, ZKL_E_ARG, "workspace must be 256-byte aligned");
     c->ws = (uint8_t*)ptr;
     c->ws_bytes = bytes;
+    c->prep_S = nullptr;   // the cached index-map keys lived in the old workspace
     return ZKL_OK;
 }
 
@@ -1008,8 +1017,12 @@ static int prepare_impl(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T,
     }
     if (e != ~0ull) {
         if (err_index) *err_index = (int64_t)e;
+        ctx->prep_S = nullptr;
         return set_err(ctx, ZKL_E_NOT_IN_TABLE, "S_%llu is not in T", e);
     }
+    ctx->prep_S = S.limbs;   // the index-map keys in the workspace belong to this S and table
+    ctx->prep_n = p.Dp;
+    ctx->prep_table = T;
     return ZKL_OK;
 }
 

@@ -169,6 +169,10 @@ struct zkl_ctx {
     uint8_t* dscratch;             // 4 KiB device scratch (scalars, error words) owned by the ctx
     int poisoned;
     uint64_t launches;
+    // keys of the last successful zkl_tlookup_prepare (in the workspace): valid for this S / table
+    const uint32_t* prep_S;
+    uint64_t prep_n;
+    const zkl_table* prep_table;
     char last_error[512];
     // optional per-kernel timing (zkl_ctx_set_profiling): events around every launch
     int profiling;

@@ -517,6 +517,49 @@ k_gather_round1(const uint32_t* __restrict__ S, uint64_t n, TableView tv, const 
     }
 }
 
+// Same as k_gather_round1, but the table index of every S_i comes from the keys of the preceding
+// zkl_tlookup_prepare on this S (ctx-cached): each key is still verified (S_i == T_key, one sector of the
+// AoS table copy, loaded in parallel with B_key), so a stale or foreign S only costs the fallback.
+__global__ void __launch_bounds__(kInvThreads)
+k_gather_keys_round1(const uint32_t* __restrict__ S, uint64_t n, const uint32_t* __restrict__ keys,
+                     const uint4* __restrict__ Taos, uint64_t N, const uint4* __restrict__ Baos,
+                     uint32_t* __restrict__ Aout, const fr* __restrict__ elo, const fr* __restrict__ ehi,
+                     fr* partials, int rows, unsigned long long* miss) {
+    fr acc = fr_zero(), a0 = fr_zero(), a1 = fr_zero();
+    const uint64_t tile = blockIdx.x;
+    const uint64_t base = tile * kInvTile + 2 * threadIdx.x;
+    uint2 kn = __ldg(reinterpret_cast<const uint2*>(keys + base));
+#pragma unroll 1
+    for (int g = 0; g < 8; ++g) {
+        const uint64_t i0 = base + 512 * g;
+        uint2 k = kn;
+        if (g < 7) kn = __ldg(reinterpret_cast<const uint2*>(keys + i0 + 512));   // prefetch
+        if (k.x >= N || k.y >= N) {
+            atomic_min_i64(miss, i0);
+            k.x = k.x >= N ? 0 : k.x;
+            k.y = k.y >= N ? 0 : k.y;
+        }
+        const fr A0 = ld_aos_fr(Baos + 2 * (uint64_t)k.x), A1 = ld_aos_fr(Baos + 2 * (uint64_t)k.y);
+        fr x[2];
+        ld_fr2(S, n, i0, x);
+        if (!aos_eq(Taos + 2 * (uint64_t)k.x, x[0]) || !aos_eq(Taos + 2 * (uint64_t)k.y, x[1]))
+            atomic_min_i64(miss, i0);
+        st_fr2(Aout, n, i0, A0, A1);
+        const fr dA = fr_sub(A1, A0), dS = fr_sub(x[1], x[0]);
+        acc = fr_add(acc, fr_mul(elo[256 * g + threadIdx.x], fr_mul(dA, dS)));
+        a0 = fr_add(a0, A0);
+        a1 = fr_add(a1, A1);
+    }
+    fr v[3] = {fr_mul(ehi[tile], acc), a0, a1};
+    __shared__ fr scratch[3 * (kInvThreads / 32)];
+    block_sum_fr<3>(v, scratch);
+    if (threadIdx.x == 0) {
+        partials[SLOT_HINF * rows + tile] = v[0];
+        partials[SLOT_A0 * rows + tile] = v[1];
+        partials[SLOT_A1 * rows + tile] = v[2];
+    }
+}
+
 __global__ void k_soa_to_aos(const uint32_t* __restrict__ src, uint64_t n, uint4* __restrict__ dst) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const fr x = ld_fr(src, n, i);
