@@ -507,7 +507,7 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
     } else {
         if (gather) {
             // a4 + a5 through the table: A_i = B_j(i), one block per 4096-element tile (partial row = tile)
-            TableView tv{a.table->T, a.table->Taos, a.table->slots, a.table->N, a.table->slot_mask};
+            TableView tv{a.table->T, a.table->Taos, a.table->slots, a.table->Skeys, a.table->N, a.table->slot_mask};
             if (ctx->prep_S == a.S.limbs && ctx->prep_n == p.Dp && ctx->prep_table == a.table) {
                 // keys from the preceding prepare on this S (each still verified against T)
                 LAUNCH(ctx, k_gather_keys_round1, (unsigned)p.ntiles, kInvThreads, 0, s, a.S.limbs, p.Dp,
@@ -906,7 +906,7 @@ int zkl_vec_export(zkl_ctx* ctx, zkl_vec src, void* canon, int dst_on_device) {
 size_t zkl_table_bytes(uint64_t N) {
     if (!is_pow2(N)) return 0;
     uint64_t slots = std::max<uint64_t>(64, 4 * N);   // load factor <= 1/4
-    return soa_bytes(N) + align_up(32 * N) + align_up(4 * slots);
+    return soa_bytes(N) + align_up(32 * N) + align_up(4 * slots) + align_up(32 * slots);
 }
 
 int zkl_table_create(zkl_ctx* ctx, zkl_vec T, void* mem, size_t mem_bytes, zkl_table** out, int64_t* err_index) {
@@ -927,6 +927,8 @@ int zkl_table_create(zkl_ctx* ctx, zkl_vec T, void* mem, size_t mem_bytes, zkl_t
     t->T = (uint32_t*)mem;
     t->Taos = (uint4*)((uint8_t*)mem + soa_bytes(N));
     t->slots = (uint32_t*)((uint8_t*)mem + soa_bytes(N) + align_up(32 * N));
+    t->Skeys = (uint4*)((uint8_t*)mem + soa_bytes(N) + align_up(32 * N) + align_up(4 * nslots));
+    t->nslots = nslots;
     t->slot_mask = (uint32_t)(nslots - 1);
     t->device = ctx->device;
     unsigned long long* derr = reinterpret_cast<unsigned long long*>(ctx->dscratch + 8);
@@ -937,8 +939,10 @@ int zkl_table_create(zkl_ctx* ctx, zkl_vec T, void* mem, size_t mem_bytes, zkl_t
         auto launch_all = [&]() -> int {
             LAUNCH(ctx, k_table_copy, grid_for(N, 256), 256, 0, ctx->stream, T.limbs, N, t->T, t->Taos);
             LAUNCH(ctx, k_table_insert, grid_for(N, 256), 256, 0, ctx->stream, t->T, N, t->slots, t->slot_mask);
-            LAUNCH(ctx, k_table_dups, grid_for(N, 256), 256, 0, ctx->stream, t->T, t->Taos, N, t->slots, t->slot_mask,
-                   derr);
+            LAUNCH(ctx, k_table_fill_keys, grid_for(nslots, 256), 256, 0, ctx->stream, t->T, N, t->slots, nslots,
+                   t->Skeys);
+            LAUNCH(ctx, k_table_dups, grid_for(N, 256), 256, 0, ctx->stream, t->T, t->Taos, N, t->slots, t->Skeys,
+                   t->slot_mask, derr);
             return ZKL_OK;
         };
         if ((st = launch_all())) return fail(st);
@@ -982,7 +986,7 @@ static int prepare_impl(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T,
     unsigned long long* err = at<unsigned long long>(ctx, p.o_err);
     uint32_t* rows = at<uint32_t>(ctx, p.o_hist);
     CUDA_TRY(ctx, cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), ctx->stream));
-    TableView tv{T->T, T->Taos, T->slots, T->N, T->slot_mask};
+    TableView tv{T->T, T->Taos, T->slots, T->Skeys, T->N, T->slot_mask};
     uint32_t* keys = at<uint32_t>(ctx, p.o_keys);
     if (pair) {
         if (!pair->x || !pair->y || !pair->alpha_f) return set_err(ctx, ZKL_E_ARG, "null argument");

@@ -187,8 +187,10 @@ struct zkl_ctx {
 struct zkl_table {
     uint64_t N;
     uint32_t* T;        // SoA Montgomery copy, N entries
-    uint4* Taos;        // AoS copy (32 B per entry) for key compares
-    uint32_t* slots;    // open-addressing hash: slot -> index+1 (0 = empty)
+    uint4* Taos;        // AoS copy (32 B per entry) by table index
+    uint32_t* slots;
+    uint4* Skeys;       // AoS key per slot    // open-addressing hash: slot -> index+1 (0 = empty)
     uint32_t slot_mask;
+    uint64_t nslots;
     int device;
 };

@@ -113,8 +113,9 @@ __device__ __forceinline__ uint32_t hash_fr(const fr& x) {
 
 struct TableView {
     const uint32_t* T;       // SoA Montgomery
-    const uint4* Taos;       // AoS copy (2 x uint4 per entry) for one-sector key compares
+    const uint4* Taos;       // AoS copy (2 x uint4 per entry), indexed by table index
     const uint32_t* slots;   // index + 1, 0 = empty
+    const uint4* Skeys;      // AoS key stored WITH each occupied slot: one probe = two independent loads
     uint64_t N;
     uint32_t mask;
 };
@@ -125,14 +126,26 @@ __device__ __forceinline__ bool aos_eq(const uint4* p, const fr& x) {
             (b.z ^ x.v[6]) | (b.w ^ x.v[7])) == 0;
 }
 
-// index of x in T, or -1 (linear probing)
+// index of x in T, or -1 (linear probing; slot index and slot key are loaded together)
 __device__ __forceinline__ int64_t table_find(const TableView& tv, const fr& x) {
     uint32_t h = hash_fr(x) & tv.mask;
     for (;;) {
-        uint32_t s = __ldg(tv.slots + h);
+        const uint32_t s = __ldg(tv.slots + h);
+        const bool eq = aos_eq(tv.Skeys + 2 * (uint64_t)h, x);
         if (s == 0) return -1;
-        if (aos_eq(tv.Taos + 2 * (uint64_t)(s - 1), x)) return (int64_t)(s - 1);
+        if (eq) return (int64_t)(s - 1);
         h = (h + 1) & tv.mask;
+    }
+}
+
+// insert-time helper: the (final) key of every occupied slot
+__global__ void k_table_fill_keys(const uint32_t* __restrict__ T, uint64_t N, const uint32_t* __restrict__ slots,
+                                  uint64_t nslots, uint4* Skeys) {
+    for (uint64_t h = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; h < nslots; h += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = slots[h];
+        fr x = s ? ld_fr(T, N, s - 1) : fr_zero();
+        Skeys[2 * h] = make_uint4(x.v[0], x.v[1], x.v[2], x.v[3]);
+        Skeys[2 * h + 1] = make_uint4(x.v[4], x.v[5], x.v[6], x.v[7]);
     }
 }
 
@@ -164,8 +177,8 @@ __global__ void k_table_insert(const uint32_t* __restrict__ T, uint64_t N, uint3
 
 // j is a duplicate iff its key's slot holds a smaller index; report the smallest such j.
 __global__ void k_table_dups(const uint32_t* __restrict__ T, const uint4* __restrict__ aos, uint64_t N,
-                             const uint32_t* slots, uint32_t mask, unsigned long long* err) {
-    TableView tv{T, aos, slots, N, mask};
+                             const uint32_t* slots, const uint4* skeys, uint32_t mask, unsigned long long* err) {
+    TableView tv{T, aos, slots, skeys, N, mask};
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < N; j += (uint64_t)gridDim.x * blockDim.x) {
         int64_t f = table_find(tv, ld_fr(T, N, j));
         if (f != (int64_t)j) atomic_min_i64(err, j);
@@ -224,7 +237,7 @@ k_import_pair_index(const int32_t* __restrict__ x, const int32_t* __restrict__ y
             for (int q = 0; q < 4; ++q) slot[q] = __ldg(tv.slots + h[q]);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                bool ok = slot[q] != 0 && aos_eq(tv.Taos + 2 * (uint64_t)(slot[q] - 1), s[q]);
+                bool ok = slot[q] != 0 && aos_eq(tv.Skeys + 2 * (uint64_t)h[q], s[q]);
                 uint32_t key = slot[q] - 1;
                 if (!ok && slot[q] != 0) {                 // collision: keep probing
                     const int64_t f = table_find(tv, s[q]);
@@ -491,8 +504,8 @@ k_gather_round1(const uint32_t* __restrict__ S, uint64_t n, TableView tv, const 
         ld_fr2(S, n, i0, x);
         uint32_t h0 = hash_fr(x[0]) & tv.mask, h1 = hash_fr(x[1]) & tv.mask;
         uint32_t s0 = __ldg(tv.slots + h0), s1 = __ldg(tv.slots + h1);
-        int64_t j0 = (s0 != 0 && aos_eq(tv.Taos + 2 * (uint64_t)(s0 - 1), x[0])) ? (int64_t)(s0 - 1) : -2;
-        int64_t j1 = (s1 != 0 && aos_eq(tv.Taos + 2 * (uint64_t)(s1 - 1), x[1])) ? (int64_t)(s1 - 1) : -2;
+        int64_t j0 = (s0 != 0 && aos_eq(tv.Skeys + 2 * (uint64_t)h0, x[0])) ? (int64_t)(s0 - 1) : -2;
+        int64_t j1 = (s1 != 0 && aos_eq(tv.Skeys + 2 * (uint64_t)h1, x[1])) ? (int64_t)(s1 - 1) : -2;
         if (j0 == -2) j0 = s0 ? table_find(tv, x[0]) : -1;
         if (j1 == -2) j1 = s1 ? table_find(tv, x[1]) : -1;
         if (j0 < 0 || j1 < 0) {
