@@ -184,7 +184,7 @@ def run_reference(args):
     out = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "u32x8 (Fr, exact)", "data": "synthetic",
-           "config": {"workload": WORKLOAD, "D": Ds, "N": 1 << 16, "sample": sample},
+           "config": {"workload": WORKLOAD, "D": 1 << 26, "N": 1 << 16, "P": 1, "sample_D": Ds, "sample": sample},
            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
