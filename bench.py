@@ -280,6 +280,27 @@ def main():
                 kern.setdefault(name, []).append(kms)
     ctx.set_profiling(False)
 
+    # ---------------- Fiat-Shamir mode (f1, single rank): the same step with challenges derived on the device
+    fs_ms = None
+    if world == 1:
+        seed = bytes(32)
+
+        def step_fs():
+            ctx.import_pair(txd, tyd, ch.alpha_f, T)
+            tab = ctx.table(T, tmem)
+            ctx.prepare_pair(xd, yd, ch.alpha_f, D, tab, S, m)
+            return ctx.prove_fs(S, D, tab, m, seed, args.variant)
+
+        step_fs()
+        torch.cuda.synchronize(dev)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            step_fs()
+        f1.record(stream)
+        torch.cuda.synchronize(dev)
+        fs_ms = f0.elapsed_time(f1) / args.steps
+
     # ---------------- e2e: host (pinned) X, Y, T_X, T_Y -> device each step, transcript back to the host
     xh, yh, txh, tyh = (t.pin_memory() for t in (x, y, tx, ty))
     xe, ye, txe, tye = (torch.empty_like(t) for t in (xd, yd, txd, tyd))
@@ -359,7 +380,9 @@ def main():
                       "l2": "inputs larger than L2 (X,Y int32 512 MiB; S 2 GiB)"},
            "e2e": {"value": D / (ms_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
            "gpu_launches": launches, "roofline": roofline, "clocks": clk.summary(),
-           "kernel_ms_per_step": kernels, "kernel_ms_sum": step_ms_sum}
+           "kernel_ms_per_step": kernels, "kernel_ms_sum": step_ms_sum,
+           "fiat_shamir": {"ms_per_step": fs_ms, "lookups_per_s": (D / (fs_ms / 1e3)) if fs_ms else None,
+                           "note": "same step, challenges derived on the device (SHA-256 transcript, per-round)"}}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import c_oracle as C
         from oracle import tlookup as TL

@@ -152,6 +152,17 @@ int zkl_tlookup_prove(zkl_ctx* ctx, zkl_vec S_local, uint64_t D, const zkl_table
                       const zkl_challenges* ch, zkl_variant variant, zkl_vec A_local_out, zkl_vec B_out,
                       zkl_fr* round_evals, zkl_final_evals* finals, int64_t* err_index);
 
+/* Fiat-Shamir (non-interactive) tlookup-Prove: the same proof, with beta, alpha1, alpha2 = alpha1^2, u and every
+ * r_k derived on the device from a SHA-256 transcript: h_0 = SHA256("zkl-fs-v1" || seed ||
+ * le64(D) || le64(N) || le32(variant)); chal(label, i) = SHA256(h || label || le32(i)) mod r; beta = chal("beta",0),
+ * alpha1 = chal("alpha",0), u_c = chal("u",c); after round k, h_k = SHA256(h_{k-1} || "g" || le32(k) ||
+ * g_k(0..3) as 32-byte LE) and r_k = chal("r", k).  `seed` (32 bytes) stands for the commitments sent before
+ * beta ([T], [S], [m]; commitments are outside this path).  derived (host, 3 + 2 log2 D): beta, alpha1,
+ * alpha2, u[0..d-1], r[0..d-1], canonical.  Single rank; D >= 2. */
+int zkl_tlookup_prove_fs(zkl_ctx* ctx, zkl_vec S_local, uint64_t D, const zkl_table* T, const uint32_t* m_dev,
+                         const uint8_t seed[32], zkl_variant variant, zkl_vec A_local_out, zkl_vec B_out,
+                         zkl_fr* round_evals, zkl_final_evals* finals, zkl_fr* derived, int64_t* err_index);
+
 /* The sumcheck alone on caller-supplied vectors (any values: tamper trials, benchmarking); inputs are
  * never modified.  m_fr is m as field elements (SoA Montgomery, N).  B is the variant's B. */
 int zkl_sumcheck_prove(zkl_ctx* ctx, zkl_vec A_local, zkl_vec S_local, uint64_t D, zkl_vec B, zkl_vec T,

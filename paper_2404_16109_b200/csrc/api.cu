@@ -16,6 +16,7 @@
 #include <new>
 #include <vector>
 
+#include "fs.cuh"
 #include "kernels.cuh"
 #include "nccl_loader.h"
 
@@ -118,7 +119,7 @@ struct Plan {
     int hist_rows;
     // workspace offsets
     size_t o_out, o_sc, o_err, o_rounds, o_jobs, o_chal, o_part, o_tpart, o_tnb, o_rank, o_gath, o_repl, o_tsum,
-        o_fin, o_tfin, o_gfin, o_rc, o_arena, o_hist, o_keys, o_tot, o_totinv, o_A, o_A1, o_S1, o_A2, o_S2, o_tB, o_tX, o_tM,
+        o_fin, o_tfin, o_gfin, o_rc, o_fs, o_small, o_derived, o_arena, o_hist, o_keys, o_tot, o_totinv, o_A, o_A1, o_S1, o_A2, o_S2, o_tB, o_tX, o_tM,
         o_tE, o_twk, o_tBaos, total;
 };
 
@@ -129,7 +130,7 @@ void choose_round(Plan& p, int k, uint64_t npairs, int gbits, int nblocks) {
     (void)npairs;
 }
 
-void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode, const zkl_fr* u) {
+void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode, const zkl_fr* u, bool fs = false) {
     memset(&p, 0, sizeof(p));
     p.D = D; p.N = N; p.P = P; p.rank = rank;
     p.d = ilog2(D); p.n = ilog2(N); p.pbits = ilog2(P);
@@ -147,7 +148,25 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
     }
     p.hist_rows = hist_rows_for(p.Dp, N);
     // ---- D-side local rounds
-    if (p.small) {
+    if (fs) {
+        // Fiat-Shamir: every round is its own launch (r_k is derived between rounds); round 1 from the
+        // gather/inversion tiles, or, for D_local < 4096, k_round<false> on A and S
+        for (int k = 1; k <= p.dl; ++k) {
+            const uint64_t nk = p.Dp >> (k - 1);
+            const uint64_t np = nk / 2;
+            if (k == 1 && !p.small) {
+                choose_round(p, 1, np, 11, (int)p.ntiles);
+                continue;
+            }
+            int gbits = 12;
+            while (gbits > 8 && (np >> gbits) < (uint64_t)kSMs) --gbits;
+            if ((1ull << gbits) > np) gbits = ilog2(np);
+            choose_round(p, k, np, gbits, (int)std::max<uint64_t>(1, std::min<uint64_t>(np >> gbits, kMaxBlocks)));
+        }
+        for (int k = 1; k <= p.dl; ++k) p.rd[k - 1].direct_h1 = 1;
+        p.k0 = p.dl + 1;
+        p.fold_in = 0;
+    } else if (p.small) {
         p.k0 = 1;
         p.fold_in = 0;
     } else {
@@ -230,6 +249,9 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
     p.o_tfin = take(sizeof(fr) * 4);
     p.o_gfin = take(sizeof(fr) * 2 * (size_t)P);
     p.o_rc = take(sizeof(RoundConst) * kMaxRounds);
+    p.o_fs = take(sizeof(FsState));
+    p.o_small = take(soa_bytes(std::min<uint64_t>(p.Dp, kInvTile)));
+    p.o_derived = take(sizeof(zkl_fr) * (3 + 2 * kMaxRounds));
     p.o_arena = take(sizeof(fr) * p.arena);
     p.o_hist = take(sizeof(uint32_t) * (size_t)p.hist_rows * N);
     p.o_keys = take(sizeof(uint32_t) * std::max<uint64_t>(p.Dp, 4));
@@ -634,6 +656,161 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
     finals->B = ho->finals[2];
     finals->T = ho->finals[3];
     finals->m = ho->finals[4];
+    return ZKL_OK;
+}
+
+// ------------------------------------------------------------------ Fiat-Shamir driver (f1)
+int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, const uint32_t* m_dev,
+                 const uint8_t* seed, int variant, zkl_vec A_out, zkl_vec B_out, zkl_fr* round_evals,
+                 zkl_final_evals* finals, zkl_fr* derived, int64_t* err_index, bool force_inversion) {
+    if (err_index) *err_index = -1;
+    int st;
+    const uint64_t N = table->N;
+    if ((st = check_shape(ctx, D, N))) return st;
+    if (D < 2) return set_err(ctx, ZKL_E_SHAPE, "Fiat-Shamir mode needs D >= 2");
+    if (ctx->nranks != 1) return set_err(ctx, ZKL_E_ARG, "Fiat-Shamir mode: single rank only (this build)");
+    if (!seed || !m_dev || !round_evals || !finals || !derived) return set_err(ctx, ZKL_E_ARG, "null argument");
+    std::vector<zkl_fr> u1(kMaxRounds);
+    for (auto& x : u1) { memset(&x, 0, sizeof(x)); x.w[0] = 1; }
+    Plan p;
+    make_plan(p, D, N, 1, 0, true, u1.data(), true);
+    if ((st = need_ws(ctx, p))) return st;
+    if ((st = check_vec(ctx, S, p.Dp, "S_local"))) return st;
+    if (A_out.limbs && (st = check_vec(ctx, A_out, p.Dp, "A_local_out"))) return st;
+    if (B_out.limbs && (st = check_vec(ctx, B_out, N, "B_out"))) return st;
+    cudaStream_t s = ctx->stream;
+    ProofScalars* sc = at<ProofScalars>(ctx, p.o_sc);
+    unsigned long long* err = at<unsigned long long>(ctx, p.o_err);
+    RoundDesc* rounds = at<RoundDesc>(ctx, p.o_rounds);
+    EqJob* jobs = at<EqJob>(ctx, p.o_jobs);
+    fr* partials = at<fr>(ctx, p.o_part);
+    fr* fin = at<fr>(ctx, p.o_fin);
+    fr* tfin = at<fr>(ctx, p.o_tfin);
+    fr* arena = at<fr>(ctx, p.o_arena);
+    fr* tpart = at<fr>(ctx, p.o_tpart);
+    FsState* fst = at<FsState>(ctx, p.o_fs);
+    zkl_fr* dder = at<zkl_fr>(ctx, p.o_derived);
+    ProofOut* out = at<ProofOut>(ctx, p.o_out);
+    uint8_t* dseed = reinterpret_cast<uint8_t*>(at<zkl_fr>(ctx, p.o_chal));
+    struct Staging {
+        uint8_t seed[32];
+        RoundDesc rounds[kMaxRounds];
+        EqJob jobs[2 * kMaxRounds];
+    };
+    Staging* hs = reinterpret_cast<Staging*>((uint8_t*)ctx->host_out + sizeof(ProofOut));
+    memcpy(hs->seed, seed, 32);
+    memcpy(hs->rounds, p.rd, sizeof(p.rd));
+    memcpy(hs->jobs, p.jobs, sizeof(p.jobs));
+    CUDA_TRY(ctx, cudaMemcpyAsync(dseed, hs->seed, 32, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(rounds, hs->rounds, sizeof(hs->rounds), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(jobs, hs->jobs, sizeof(hs->jobs), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(ctx, cudaMemsetAsync(err, 0xff, 4 * sizeof(unsigned long long), s));
+    LAUNCH(ctx, k_fs_init, 1, 1, 0, s, dseed, D, N, variant, p.d, sc, fst, dder);
+    LAUNCH(ctx, k_eq_fill, grid_for(p.arena, 256), 256, 0, s, jobs, p.njobs, p.arena, sc, arena);
+    // ---- B = 1/(beta + T) and the table working vectors
+    uint32_t* tB = at<uint32_t>(ctx, p.o_tB);
+    uint32_t* tX = at<uint32_t>(ctx, p.o_tX);
+    if (N >= (uint64_t)kInvTile) {
+        if ((st = inv_forward(ctx, p.tinv, table->T, N, tB, sc, 0, err + 1, s, s, nullptr))) return st;
+        if ((st = inv_backward0(ctx, p.tinv, table->T, N, tB, sc, nullptr, nullptr, nullptr, 0, s))) return st;
+    } else {
+        LAUNCH(ctx, k_add_beta, grid_for(N, 256), 256, 0, s, table->T, N, sc, tX, err + 1);
+        const unsigned bt = (unsigned)std::min<uint64_t>(1024, std::max<uint64_t>(32, N));
+        LAUNCH(ctx, k_batch_invert, 1, bt, 4 * bt * sizeof(fr), s, tX, N, (uint64_t)0, N, tB);
+    }
+    fr* wk = at<fr>(ctx, p.o_twk);
+    fr *tcur = wk, *tnxt = wk + 4 * N;
+    LAUNCH(ctx, k_tab_init, grid_for(N, 256), 256, 0, s, tB, table->T, m_dev, (const uint32_t*)nullptr, N, sc, p.d,
+           p.n, variant, tcur, B_out.limbs);
+    uint64_t tlen = N;
+    if (p.n == 0) LAUNCH(ctx, k_tab_fin_copy, 1, 32, 0, s, tcur, tfin);   // the table is fully bound from the start
+    // ---- round 1: A (gather through the prepared index, or inversion) + the round-1 sums
+    uint32_t* Abuf = A_out.limbs ? A_out.limbs : at<uint32_t>(ctx, p.o_A);
+    const bool gather = !p.small && !force_inversion;
+    int h01 = 1;
+    if (gather) {
+        LAUNCH(ctx, k_soa_to_aos, grid_for(N, 256), 256, 0, s, tB, N, at<uint4>(ctx, p.o_tBaos));
+        TableView tv{table->T, table->Taos, table->slots, table->Skeys, table->N, table->slot_mask};
+        if (ctx->prep_S == S.limbs && ctx->prep_n == p.Dp && ctx->prep_table == table)
+            LAUNCH(ctx, k_gather_keys_round1, (unsigned)p.ntiles, kInvThreads, 0, s, S.limbs, p.Dp,
+                   at<uint32_t>(ctx, p.o_keys), table->Taos, N, at<uint4>(ctx, p.o_tBaos), Abuf,
+                   arena + p.rd[0].elo_off, arena + p.rd[0].ehi_off, partials + p.rd[0].part_base, (int)p.ntiles,
+                   err + 2);
+        else
+            LAUNCH(ctx, k_gather_round1, (unsigned)p.ntiles, kInvThreads, 0, s, S.limbs, p.Dp, tv,
+                   at<uint4>(ctx, p.o_tBaos), Abuf, arena + p.rd[0].elo_off, arena + p.rd[0].ehi_off,
+                   partials + p.rd[0].part_base, (int)p.ntiles, err + 2);
+    } else if (!p.small) {
+        for (int h = 0; h < p.nhalves; ++h)
+            if ((st = inv_forward(ctx, p.inv[h], S.limbs, p.Dp, Abuf, sc, 0, err, s, s, nullptr))) return st;
+        for (int h = 0; h < p.nhalves; ++h)
+            if ((st = inv_backward0(ctx, p.inv[h], S.limbs, p.Dp, Abuf, sc, arena + p.rd[0].elo_off,
+                                    arena + p.rd[0].ehi_off, partials + p.rd[0].part_base, (int)p.ntiles, s)))
+                return st;
+    } else {
+        // small D: A by one batch inversion, round 1 summed directly from A and S
+        LAUNCH(ctx, k_add_beta, grid_for(p.Dp, 256), 256, 0, s, S.limbs, p.Dp, sc, at<uint32_t>(ctx, p.o_small), err);
+        const unsigned bt = (unsigned)std::min<uint64_t>(1024, std::max<uint64_t>(32, p.Dp));
+        LAUNCH(ctx, k_batch_invert, 1, bt, 4 * bt * sizeof(fr), s, at<uint32_t>(ctx, p.o_small), p.Dp, (uint64_t)0,
+               p.Dp, Abuf);
+        const RoundDesc& r = p.rd[0];
+        LAUNCH(ctx, (k_round<false, true>), r.nblocks, kRoundThreads, 0, s, Abuf, S.limbs, p.Dp, nullptr, nullptr, sc, 1,
+               arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, partials + r.part_base);
+        h01 = 0;
+    }
+    if (p.n >= 1) LAUNCH(ctx, k_tab_eval, p.tnb[0], 256, 0, s, tcur, tlen, sc, variant, tpart);
+    LAUNCH(ctx, k_fs_round, 1, 256, 0, s, 1, p.d, p.n, variant, partials + p.rd[0].part_base, p.rd[0].nblocks, h01,
+           tpart, p.n >= 1 ? p.tnb[0] : 0u, tfin, sc, fst, out, dder);
+    // ---- rounds 2..d
+    const uint32_t *cA = Abuf, *cS = S.limbs;
+    uint64_t len = p.Dp;
+    for (int k = 2; k <= p.d; ++k) {
+        const RoundDesc& r = p.rd[k - 1];
+        uint32_t* nA = at<uint32_t>(ctx, (k & 1) == 0 ? p.o_A1 : p.o_A2);
+        uint32_t* nS = at<uint32_t>(ctx, (k & 1) == 0 ? p.o_S1 : p.o_S2);
+        LAUNCH(ctx, (k_round<true, true>), r.nblocks, kRoundThreads, 0, s, cA, cS, len, nA, nS, sc, k,
+               arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, partials + r.part_base);
+        cA = nA; cS = nS;
+        len /= 2;
+        if (k - 1 <= p.n) {   // fold the table with r_{k-1}
+            LAUNCH(ctx, k_tab_fold, grid_for(tlen / 2, 256, kMaxBlocks), 256, 0, s, tcur, tlen, tnxt, sc, k - 1, tfin);
+            fr* t = tcur; tcur = tnxt; tnxt = t;
+            tlen /= 2;
+        }
+        if (k <= p.n) LAUNCH(ctx, k_tab_eval, p.tnb[k - 1], 256, 0, s, tcur, tlen, sc, variant, tpart);
+        LAUNCH(ctx, k_fs_round, 1, 256, 0, s, k, p.d, p.n, variant, partials + r.part_base, r.nblocks, 0, tpart,
+               k <= p.n ? p.tnb[k - 1] : 0u, tfin, sc, fst, out, dder);
+    }
+    LAUNCH(ctx, k_fold_final, 1, 32, 0, s, cA, cS, len, sc, p.d, fin);
+    if (p.n == p.d) LAUNCH(ctx, k_tab_fold, 1, 32, 0, s, tcur, tlen, tnxt, sc, p.d, tfin);
+    LAUNCH(ctx, k_fs_finish, 1, 32, 0, s, fin, tfin, out);
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->host_out, out, sizeof(ProofOut), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync((uint8_t*)ctx->host_out + offsetof(ProofOut, err_index), err,
+                                  3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    zkl_fr* hder = reinterpret_cast<zkl_fr*>((uint8_t*)ctx->host_out + 32768);
+    CUDA_TRY(ctx, cudaMemcpyAsync(hder, dder, sizeof(zkl_fr) * (3 + 2 * p.d), cudaMemcpyDeviceToHost, s));
+    if ((st = sync_stream(ctx))) return st;
+    const ProofOut* ho = reinterpret_cast<const ProofOut*>(ctx->host_out);
+    const unsigned long long* he = reinterpret_cast<const unsigned long long*>((const uint8_t*)ctx->host_out +
+                                                                               offsetof(ProofOut, err_index));
+    if (he[1] != ~0ull) {
+        if (err_index) *err_index = (int64_t)he[1];
+        return set_err(ctx, ZKL_E_DIV_ZERO_T, "beta + T_%llu = 0", he[1]);
+    }
+    if (gather && he[2] != ~0ull)
+        return run_proof_fs(ctx, S, D, table, m_dev, seed, variant, A_out, B_out, round_evals, finals, derived,
+                            err_index, true);
+    if (he[0] != ~0ull) {
+        if (err_index) *err_index = (int64_t)he[0];
+        return set_err(ctx, ZKL_E_DIV_ZERO_S, "beta + S_%llu = 0", he[0]);
+    }
+    memcpy(round_evals, ho->evals, sizeof(zkl_fr) * 4 * p.d);
+    finals->A = ho->finals[0];
+    finals->S = ho->finals[1];
+    finals->B = ho->finals[2];
+    finals->T = ho->finals[3];
+    finals->m = ho->finals[4];
+    memcpy(derived, hder, sizeof(zkl_fr) * (3 + 2 * p.d));
     return ZKL_OK;
 }
 
@@ -1058,6 +1235,16 @@ int zkl_tlookup_prove(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T, c
     a.ch = ch;
     a.variant = variant;
     return run_proof(ctx, D, a, round_evals, finals, err_index);
+}
+
+int zkl_tlookup_prove_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T, const uint32_t* m_dev,
+                         const uint8_t seed[32], zkl_variant variant, zkl_vec A_out, zkl_vec B_out, zkl_fr* round_evals,
+                         zkl_final_evals* finals, zkl_fr* derived, int64_t* err_index) {
+    int st;
+    if ((st = check_ctx(ctx))) return st;
+    if (!T) return set_err(ctx, ZKL_E_ARG, "null table");
+    return run_proof_fs(ctx, S, D, T, m_dev, seed, variant, A_out, B_out, round_evals, finals, derived, err_index,
+                        false);
 }
 
 int zkl_sumcheck_prove(zkl_ctx* ctx, zkl_vec A, zkl_vec S, uint64_t D, zkl_vec B, zkl_vec T, zkl_vec m_fr,

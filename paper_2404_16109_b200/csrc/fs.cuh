@@ -1,0 +1,205 @@
+// Fiat-Shamir mode: the verifier's challenges are derived on the device from a SHA-256
+// transcript, so r_k depends on g_k and every round waits for the previous round's derivation (one small
+// kernel per round).  Transcript:
+//   h_0   = SHA256("zkl-fs-v1" || seed[32] || le64(D) || le64(N) || le32(variant))
+//   chal(label, i) = le-integer(SHA256(h || label || le32(i))) mod r
+//   beta = chal("beta", 0), alpha1 = chal("alpha", 0), alpha2 = alpha1^2, u_c = chal("u", c)
+//   round k: h_k = SHA256(h_{k-1} || "g" || le32(k) || g_k(0) || g_k(1) || g_k(2) || g_k(3)),  r_k = chal("r", k)
+// The seed stands for the commitments the prover would have sent ([T], [S], [m]); commitments are NEXT f3.
+#pragma once
+#include "kernels.cuh"
+#include "sha256.cuh"
+
+namespace zkl {
+
+struct FsState {
+    uint8_t h[32];
+    fr C;        // C_k = prod_{j<k} l_{d-j}(r_j)
+    fr tscale;   // 2^{-(k-n)} once the table coordinates are bound
+};
+
+// canonical 256-bit little-endian value of a digest, reduced mod r (x < 2^256 < 3r)
+__device__ inline fr fs_digest_to_fr(const uint8_t* dg) {
+    fr x;
+    for (int l = 0; l < 8; ++l)
+        x.v[l] = (uint32_t)dg[4 * l] | ((uint32_t)dg[4 * l + 1] << 8) | ((uint32_t)dg[4 * l + 2] << 16) |
+                 ((uint32_t)dg[4 * l + 3] << 24);
+    fr_reduce_once(x);
+    fr_reduce_once(x);
+    return x;
+}
+
+__device__ inline fr fs_challenge(const uint8_t* h, const char* label, int llen, uint32_t idx) {
+    uint8_t msg[48], dg[32];
+    int p = 0;
+    for (int i = 0; i < 32; ++i) msg[p++] = h[i];
+    for (int i = 0; i < llen; ++i) msg[p++] = (uint8_t)label[i];
+    for (int i = 0; i < 4; ++i) msg[p++] = (uint8_t)(idx >> (8 * i));
+    sha256(msg, p, dg);
+    return fs_digest_to_fr(dg);
+}
+
+__device__ inline zkl_fr fs_canon_out(const fr& c) {
+    zkl_fr z;
+    for (int l = 0; l < 8; ++l) z.w[l] = c.v[l];
+    return z;
+}
+
+// derive beta, alpha1, alpha2, u into sc (Montgomery) and `derived` (canonical: beta, alpha1, alpha2, u[d], r[d])
+__global__ void k_fs_init(const uint8_t* __restrict__ seed, uint64_t D, uint64_t N, int variant, int d,
+                          ProofScalars* sc, FsState* st, zkl_fr* derived) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    uint8_t msg[9 + 32 + 8 + 8 + 4];
+    const char* tag = "zkl-fs-v1";
+    int p = 0;
+    for (int i = 0; i < 9; ++i) msg[p++] = (uint8_t)tag[i];
+    for (int i = 0; i < 32; ++i) msg[p++] = seed[i];
+    for (int i = 0; i < 8; ++i) msg[p++] = (uint8_t)(D >> (8 * i));
+    for (int i = 0; i < 8; ++i) msg[p++] = (uint8_t)(N >> (8 * i));
+    for (int i = 0; i < 4; ++i) msg[p++] = (uint8_t)((uint32_t)variant >> (8 * i));
+    sha256(msg, p, st->h);
+    const fr beta = fs_challenge(st->h, "beta", 4, 0);
+    const fr a1 = fs_challenge(st->h, "alpha", 5, 0);
+    const fr a1m = fr_to_mont(a1);
+    const fr a2m = fr_mul(a1m, a1m);
+    sc->beta = fr_to_mont(beta);
+    sc->alpha1 = a1m;
+    sc->alpha2 = a2m;
+    derived[0] = fs_canon_out(beta);
+    derived[1] = fs_canon_out(a1);
+    derived[2] = to_canon(a2m);
+    for (int c = 0; c < d; ++c) {
+        const fr u = fs_challenge(st->h, "u", 1, (uint32_t)c);
+        sc->u[c] = fr_to_mont(u);
+        derived[3 + c] = fs_canon_out(u);
+    }
+    sc->rank_eq = fr_one();
+    st->C = fr_one();
+    st->tscale = fr_one();
+}
+
+// table side, split for the causal order: fold with r_{k-1} (after it is derived), then evaluate round k
+__global__ void __launch_bounds__(256)
+k_tab_eval(const fr* __restrict__ cur, uint64_t len, const ProofScalars* __restrict__ sc, int variant, fr* tpart) {
+    const fr beta = sc->beta, alpha2 = sc->alpha2;
+    fr g[4] = {fr_zero(), fr_zero(), fr_zero(), fr_zero()};
+    for (uint64_t y = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; y < len / 2; y += (uint64_t)gridDim.x * blockDim.x) {
+        const fr b0 = cur[2 * y], b1 = cur[2 * y + 1];
+        const fr t0 = cur[len + 2 * y], t1 = cur[len + 2 * y + 1];
+        const fr m0 = cur[2 * len + 2 * y], m1 = cur[2 * len + 2 * y + 1];
+        const fr e0 = cur[3 * len + 2 * y], e1 = cur[3 * len + 2 * y + 1];
+        const fr db = fr_sub(b1, b0), dt = fr_sub(t1, t0), dm = fr_sub(m1, m0), de = fr_sub(e1, e0);
+        fr bt = b0, tt = t0, mt = m0, et = e0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (q > 0) { bt = fr_add(bt, db); tt = fr_add(tt, dt); mt = fr_add(mt, dm); et = fr_add(et, de); }
+            g[q] = fr_add(g[q], tab_term(bt, tt, mt, et, beta, alpha2, variant));
+        }
+    }
+    __shared__ fr scratch[4 * 8];
+    block_sum_fr<4>(g, scratch);
+    if (threadIdx.x == 0)
+        for (int q = 0; q < 4; ++q) tpart[q * kMaxBlocks + blockIdx.x] = g[q];
+}
+
+__global__ void k_tab_fold(const fr* __restrict__ cur, uint64_t len, fr* nxt, const ProofScalars* __restrict__ sc, int k,
+                           fr* tfin) {
+    const fr r = sc->r[k - 1];
+    const uint64_t np = len / 2;
+    for (uint64_t y = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; y < np; y += (uint64_t)gridDim.x * blockDim.x) {
+        for (int v = 0; v < 4; ++v) {
+            const fr a = cur[v * len + 2 * y], b = cur[v * len + 2 * y + 1];
+            const fr f = fr_add(a, fr_mul(r, fr_sub(b, a)));
+            nxt[v * np + y] = f;
+            if (np == 1) tfin[v] = f;
+        }
+    }
+}
+
+__global__ void k_tab_fin_copy(const fr* __restrict__ cur, fr* tfin) {
+    if (threadIdx.x < 4 && blockIdx.x == 0) tfin[threadIdx.x] = cur[threadIdx.x];
+}
+
+// fold the last pair of A, S with r_d: the finals A(v), S(v)
+__global__ void k_fold_final(const uint32_t* __restrict__ A, const uint32_t* __restrict__ S, uint64_t n,
+                             const ProofScalars* __restrict__ sc, int d, fr* fin) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const fr r = sc->r[d - 1];
+    const fr a0 = ld_fr(A, n, 0), a1 = ld_fr(A, n, 1), s0 = ld_fr(S, n, 0), s1 = ld_fr(S, n, 1);
+    fin[0] = fr_add(a0, fr_mul(r, fr_sub(a1, a0)));
+    fin[1] = fr_add(s0, fr_mul(r, fr_sub(s1, s0)));
+}
+
+// Round k: reduce the D-side partial rows (and the table rows, k <= n), form g_k(0..3) directly, absorb it,
+// derive r_k.  h01_one: round 1 of the gather/inversion path, where H(0) = H(1) = sum eq = 1.
+__global__ void k_fs_round(int k, int d, int n, int variant, const fr* __restrict__ part, uint32_t nrows,
+                           int h01_one, const fr* __restrict__ tpart, uint32_t tnb, const fr* __restrict__ tfin,
+                           ProofScalars* sc, FsState* st, ProofOut* out, zkl_fr* derived) {
+    __shared__ fr scratch[5 * 8];
+    fr s[5];
+    for (int q = 0; q < 5; ++q) {
+        s[q] = fr_zero();
+        for (uint32_t b = threadIdx.x; b < nrows; b += blockDim.x) s[q] = fr_add(s[q], part[(uint64_t)q * nrows + b]);
+    }
+    block_sum_fr<5>(s, scratch);
+    fr tab[4] = {fr_zero(), fr_zero(), fr_zero(), fr_zero()};
+    if (k <= n) {
+        for (int q = 0; q < 4; ++q)
+            for (uint32_t b = threadIdx.x; b < tnb; b += blockDim.x) tab[q] = fr_add(tab[q], tpart[q * kMaxBlocks + b]);
+        block_sum_fr<4>(tab, scratch);
+    }
+    if (threadIdx.x != 0) return;
+    const fr one = fr_one(), two = fr_two_m(), three = fr_three_m(), six = fr_six_m();
+    if (k > n) {
+        const fr tb = tfin[0], tt = tfin[1], tm = tfin[2], te = tfin[3];
+        const fr tau = (variant == ZKL_VARIANT_PAPER)
+            ? fr_mul(tb, fr_sub(fr_mul(fr_mul(sc->alpha2, te), fr_add(tt, sc->beta)), tm))
+            : fr_sub(fr_mul(fr_mul(sc->alpha2, te), fr_sub(fr_mul(tb, fr_add(tt, sc->beta)), tm)), tb);
+        st->tscale = fr_mul(st->tscale, fr_inv2_m());
+        const fr c = fr_mul(tau, st->tscale);
+        for (int q = 0; q < 4; ++q) tab[q] = c;
+    }
+    const fr u = sc->u[d - k];
+    const fr coef = fr_mul(sc->alpha1, st->C);
+    const fr cl0 = fr_mul(coef, fr_sub(one, u)), cl1 = fr_mul(coef, u);
+    const fr cl2 = fr_mul(coef, fr_sub(fr_mul(three, u), one)), cl3 = fr_mul(coef, fr_sub(fr_mul(fr_five_m(), u), two));
+    fr H0 = s[SLOT_H0], H1 = s[SLOT_H1];
+    if (h01_one) { H0 = one; H1 = one; }
+    const fr Hinf = s[SLOT_HINF], a0 = s[SLOT_A0], a1 = s[SLOT_A1], da = fr_sub(a1, a0);
+    const fr H2 = fr_add(fr_sub(fr_add(H1, H1), H0), fr_add(Hinf, Hinf));
+    const fr H3 = fr_add(fr_sub(fr_mul(three, H1), fr_add(H0, H0)), fr_mul(six, Hinf));
+    fr g[4];
+    g[0] = fr_add(fr_add(fr_mul(cl0, H0), a0), tab[0]);
+    g[1] = fr_add(fr_add(fr_mul(cl1, H1), a1), tab[1]);
+    g[2] = fr_add(fr_add(fr_mul(cl2, H2), fr_add(a0, fr_add(da, da))), tab[2]);
+    g[3] = fr_add(fr_add(fr_mul(cl3, H3), fr_add(a0, fr_mul(three, da))), tab[3]);
+    uint8_t msg[32 + 1 + 4 + 128];
+    int p = 0;
+    for (int i = 0; i < 32; ++i) msg[p++] = st->h[i];
+    msg[p++] = 'g';
+    for (int i = 0; i < 4; ++i) msg[p++] = (uint8_t)((uint32_t)k >> (8 * i));
+    for (int t = 0; t < 4; ++t) {
+        const zkl_fr c = to_canon(g[t]);
+        out->evals[k - 1][t] = c;
+        for (int l = 0; l < 8; ++l)
+            for (int b = 0; b < 4; ++b) msg[p++] = (uint8_t)(c.w[l] >> (8 * b));
+    }
+    sha256(msg, p, st->h);
+    const fr r = fs_challenge(st->h, "r", 1, (uint32_t)k);
+    derived[3 + d + (k - 1)] = fs_canon_out(r);
+    const fr rm = fr_to_mont(r);
+    sc->r[k - 1] = rm;
+    const fr l0 = fr_sub(one, u);
+    st->C = fr_mul(st->C, fr_add(l0, fr_mul(rm, fr_sub(u, l0))));
+}
+
+__global__ void k_fs_finish(const fr* __restrict__ fin, const fr* __restrict__ tfin, ProofOut* out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    out->finals[0] = to_canon(fin[0]);
+    out->finals[1] = to_canon(fin[1]);
+    out->finals[2] = to_canon(tfin[0]);
+    out->finals[3] = to_canon(tfin[1]);
+    out->finals[4] = to_canon(tfin[2]);
+}
+
+}  // namespace zkl

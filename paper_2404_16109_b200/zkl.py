@@ -87,6 +87,9 @@ def lib() -> ctypes.CDLL:
             "zkl_tlookup_prepare_pair": ([P, P, P, ctypes.POINTER(zkl_fr), U64, P, zkl_vec, P, I64P], I32),
             "zkl_tlookup_prove": ([P, zkl_vec, U64, P, P, ctypes.POINTER(zkl_challenges), I32, zkl_vec, zkl_vec,
                                    ctypes.POINTER(zkl_fr), ctypes.POINTER(zkl_final_evals), I64P], I32),
+            "zkl_tlookup_prove_fs": ([P, zkl_vec, U64, P, P, ctypes.c_char_p, I32, zkl_vec, zkl_vec,
+                                      ctypes.POINTER(zkl_fr), ctypes.POINTER(zkl_final_evals), ctypes.POINTER(zkl_fr),
+                                      I64P], I32),
             "zkl_sumcheck_prove": ([P, zkl_vec, zkl_vec, U64, zkl_vec, zkl_vec, zkl_vec,
                                     ctypes.POINTER(zkl_challenges), I32, ctypes.POINTER(zkl_fr),
                                     ctypes.POINTER(zkl_final_evals)], I32),
@@ -105,7 +108,7 @@ EXPORTED = ["zkl_strerror", "zkl_ctx_create", "zkl_nccl_unique_id", "zkl_ctx_cre
             "zkl_ctx_set_profiling", "zkl_ctx_profile_read",
             "zkl_vec_import", "zkl_vec_import_i64", "zkl_vec_import_pair", "zkl_vec_export", "zkl_table_bytes",
             "zkl_table_create", "zkl_table_destroy", "zkl_tlookup_prepare", "zkl_tlookup_prepare_pair",
-            "zkl_tlookup_prove",
+            "zkl_tlookup_prove", "zkl_tlookup_prove_fs",
             "zkl_sumcheck_prove"]
 
 
@@ -350,6 +353,26 @@ class Context:
                                      A.c, B.c, evals, ctypes.byref(fin), ctypes.byref(err))
         self._check(st, err.value)
         return Proof(_evals(evals, d), _finals(fin), A if want_A else None, B if want_B else None)
+
+    def prove_fs(self, S: Vec, D: int, tab: "Table", m, seed: bytes, variant: int = PAPER, want_A: bool = False,
+                 want_B: bool = False):
+        """Fiat-Shamir prove: challenges derived on the device from a SHA-256 transcript seeded by `seed` (32 B).
+        Returns (Proof, derived) with derived = dict(beta, alpha1, alpha2, u, r) (canonical ints)."""
+        if len(seed) != 32:
+            raise ValueError("seed must be 32 bytes")
+        d = D.bit_length() - 1
+        A = self.vec(S.n) if want_A else Vec(None, S.n)
+        B = self.vec(tab.N) if want_B else Vec(None, tab.N)
+        evals = (zkl_fr * (4 * max(d, 1)))()
+        der = (zkl_fr * (3 + 2 * max(d, 1)))()
+        fin = zkl_final_evals()
+        err = ctypes.c_int64(-1)
+        st = lib().zkl_tlookup_prove_fs(self.h, S.c, D, tab.h, ctypes.c_void_p(m.data_ptr()), seed, variant, A.c,
+                                        B.c, evals, ctypes.byref(fin), der, ctypes.byref(err))
+        self._check(st, err.value)
+        dv = [fr_to_int(der[i]) for i in range(3 + 2 * d)]
+        derived = {"beta": dv[0], "alpha1": dv[1], "alpha2": dv[2], "u": dv[3:3 + d], "r": dv[3 + d:3 + 2 * d]}
+        return Proof(_evals(evals, d), _finals(fin), A if want_A else None, B if want_B else None), derived
 
     def sumcheck(self, A: Vec, S: Vec, D: int, B: Vec, T: Vec, mfr: Vec, ch, variant: int = PAPER) -> Proof:
         d = D.bit_length() - 1
