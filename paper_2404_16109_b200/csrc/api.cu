@@ -234,6 +234,8 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
     // ---- workspace layout
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o += align_up(bytes); return r; };
+    // the index-map keys outlive the call (prepare -> prove): first, at an offset that depends on nothing else
+    p.o_keys = take(sizeof(uint32_t) * std::max<uint64_t>(p.Dp, 4));
     p.o_out = take(sizeof(ProofOut));
     p.o_sc = take(sizeof(ProofScalars));
     p.o_err = take(4 * sizeof(unsigned long long));
@@ -254,7 +256,6 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
     p.o_derived = take(sizeof(zkl_fr) * (3 + 2 * kMaxRounds));
     p.o_arena = take(sizeof(fr) * p.arena);
     p.o_hist = take(sizeof(uint32_t) * (size_t)p.hist_rows * N);
-    p.o_keys = take(sizeof(uint32_t) * std::max<uint64_t>(p.Dp, 4));
     p.o_tot = take(soa_bytes(p.ntiles));
     p.o_totinv = take(soa_bytes(p.ntiles));
     p.o_A = take(soa_bytes(p.Dp));

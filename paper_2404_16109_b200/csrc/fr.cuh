@@ -161,6 +161,99 @@ __device__ __forceinline__ fr fr_sub(const fr& a, const fr& b) {
 __device__ __forceinline__ fr fr_neg(const fr& a) { return fr_sub(fr_zero(), a); }
 
 // ---------------------------------------------------------------------------------------
+// Lazy forms.  fr_mul(a, b) needs a < r but accepts any b < 2^256 (the CIOS bound T < 2r only uses a < r and
+// the 32-bit size of each limb of b), so a difference or sum feeding the b side need not be reduced.
+// a - b as a + (r - b), in (0, 2r) for canonical a, b: two carry chains, no select.
+__device__ __forceinline__ fr fr_sub_lazy(const fr& a, const fr& b) {
+    fr d;
+    asm("sub.cc.u32  %0, %8,  %16;\n\t"
+        "subc.cc.u32 %1, %9,  %17;\n\t"
+        "subc.cc.u32 %2, %10, %18;\n\t"
+        "subc.cc.u32 %3, %11, %19;\n\t"
+        "subc.cc.u32 %4, %12, %20;\n\t"
+        "subc.cc.u32 %5, %13, %21;\n\t"
+        "subc.cc.u32 %6, %14, %22;\n\t"
+        "subc.u32    %7, %15, %23;"
+        : "=r"(d.v[0]), "=r"(d.v[1]), "=r"(d.v[2]), "=r"(d.v[3]), "=r"(d.v[4]), "=r"(d.v[5]), "=r"(d.v[6]),
+          "=r"(d.v[7])
+        : "n"(ZKL_R0), "n"(ZKL_R1), "n"(ZKL_R2), "n"(ZKL_R3), "n"(ZKL_R4), "n"(ZKL_R5), "n"(ZKL_R6), "n"(ZKL_R7),
+          "r"(b.v[0]), "r"(b.v[1]), "r"(b.v[2]), "r"(b.v[3]), "r"(b.v[4]), "r"(b.v[5]), "r"(b.v[6]), "r"(b.v[7]));
+    fr s;
+    asm("add.cc.u32  %0, %8,  %16;\n\t"
+        "addc.cc.u32 %1, %9,  %17;\n\t"
+        "addc.cc.u32 %2, %10, %18;\n\t"
+        "addc.cc.u32 %3, %11, %19;\n\t"
+        "addc.cc.u32 %4, %12, %20;\n\t"
+        "addc.cc.u32 %5, %13, %21;\n\t"
+        "addc.cc.u32 %6, %14, %22;\n\t"
+        "addc.u32    %7, %15, %23;"
+        : "=r"(s.v[0]), "=r"(s.v[1]), "=r"(s.v[2]), "=r"(s.v[3]), "=r"(s.v[4]), "=r"(s.v[5]), "=r"(s.v[6]),
+          "=r"(s.v[7])
+        : "r"(a.v[0]), "r"(a.v[1]), "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]), "r"(a.v[6]), "r"(a.v[7]),
+          "r"(d.v[0]), "r"(d.v[1]), "r"(d.v[2]), "r"(d.v[3]), "r"(d.v[4]), "r"(d.v[5]), "r"(d.v[6]), "r"(d.v[7]));
+    return s;
+}
+
+// a + b without reduction, in [0, 2r) for canonical a, b
+__device__ __forceinline__ fr fr_add_lazy(const fr& a, const fr& b) {
+    fr s;
+    asm("add.cc.u32  %0, %8,  %16;\n\t"
+        "addc.cc.u32 %1, %9,  %17;\n\t"
+        "addc.cc.u32 %2, %10, %18;\n\t"
+        "addc.cc.u32 %3, %11, %19;\n\t"
+        "addc.cc.u32 %4, %12, %20;\n\t"
+        "addc.cc.u32 %5, %13, %21;\n\t"
+        "addc.cc.u32 %6, %14, %22;\n\t"
+        "addc.u32    %7, %15, %23;"
+        : "=r"(s.v[0]), "=r"(s.v[1]), "=r"(s.v[2]), "=r"(s.v[3]), "=r"(s.v[4]), "=r"(s.v[5]), "=r"(s.v[6]),
+          "=r"(s.v[7])
+        : "r"(a.v[0]), "r"(a.v[1]), "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]), "r"(a.v[6]), "r"(a.v[7]),
+          "r"(b.v[0]), "r"(b.v[1]), "r"(b.v[2]), "r"(b.v[3]), "r"(b.v[4]), "r"(b.v[5]), "r"(b.v[6]), "r"(b.v[7]));
+    return s;
+}
+
+// 288-bit accumulator of canonical values (no reduction per add); fr_acc_final reduces it mod r.
+struct fr_acc {
+    uint32_t v[9];
+};
+
+__device__ __forceinline__ fr_acc fr_acc_zero() {
+    fr_acc a;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) a.v[i] = 0;
+    return a;
+}
+
+__device__ __forceinline__ void fr_acc_add(fr_acc& acc, const fr& x) {
+    asm("add.cc.u32  %0, %0, %9;\n\t"
+        "addc.cc.u32 %1, %1, %10;\n\t"
+        "addc.cc.u32 %2, %2, %11;\n\t"
+        "addc.cc.u32 %3, %3, %12;\n\t"
+        "addc.cc.u32 %4, %4, %13;\n\t"
+        "addc.cc.u32 %5, %5, %14;\n\t"
+        "addc.cc.u32 %6, %6, %15;\n\t"
+        "addc.cc.u32 %7, %7, %16;\n\t"
+        "addc.u32    %8, %8, 0;"
+        : "+r"(acc.v[0]), "+r"(acc.v[1]), "+r"(acc.v[2]), "+r"(acc.v[3]), "+r"(acc.v[4]), "+r"(acc.v[5]),
+          "+r"(acc.v[6]), "+r"(acc.v[7]), "+r"(acc.v[8])
+        : "r"(x.v[0]), "r"(x.v[1]), "r"(x.v[2]), "r"(x.v[3]), "r"(x.v[4]), "r"(x.v[5]), "r"(x.v[6]), "r"(x.v[7]));
+}
+
+__device__ __forceinline__ fr fr_mul(const fr& a, const fr& b);
+
+// acc = hi 2^256 + lo  ->  (lo mod r) + hi (2^256 mod r); hi (2^256 mod r) = mont(R^2, hi)
+__device__ __forceinline__ fr fr_acc_final(const fr_acc& acc) {
+    fr lo;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) lo.v[i] = acc.v[i];
+    fr_reduce_once(lo);     // lo < 2^256 < 3r
+    fr_reduce_once(lo);
+    fr hi = fr_zero();
+    hi.v[0] = acc.v[8];
+    return fr_add(lo, fr_mul(fr_r2(), hi));
+}
+
+// ---------------------------------------------------------------------------------------
 // Montgomery multiplication, CIOS with aligned register pairs.
 //
 // The running value T (< 2r) is held as X + Y*2^32: X = x0..x8 aligned at word 0, Y = y0..y7

@@ -220,10 +220,19 @@ k_import_pair_index(const int32_t* __restrict__ x, const int32_t* __restrict__ y
     if ((n & 3) == 0) {
         // 4 consecutive elements per thread: 128-bit loads of x, y; 128-bit stores per limb plane; 4 hash
         // probes in flight together
-        for (uint64_t i = 4 * (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x); i < n;
-             i += 4 * (uint64_t)gridDim.x * blockDim.x) {
-            const int4 xv = __ldg(reinterpret_cast<const int4*>(x + i));
-            const int4 yv = __ldg(reinterpret_cast<const int4*>(y + i));
+        const uint64_t stride = 4 * (uint64_t)gridDim.x * blockDim.x;
+        uint64_t i = 4 * (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x);
+        int4 xn = make_int4(0, 0, 0, 0), yn = make_int4(0, 0, 0, 0);
+        if (i < n) {
+            xn = __ldg(reinterpret_cast<const int4*>(x + i));
+            yn = __ldg(reinterpret_cast<const int4*>(y + i));
+        }
+        for (; i < n; i += stride) {
+            const int4 xv = xn, yv = yn;
+            if (i + stride < n) {   // prefetch the next iteration's inputs
+                xn = __ldg(reinterpret_cast<const int4*>(x + i + stride));
+                yn = __ldg(reinterpret_cast<const int4*>(y + i + stride));
+            }
             fr s[4];
             s[0] = fr_from_small_pair(xv.x, yv.x, c);
             s[1] = fr_from_small_pair(xv.y, yv.y, c);
@@ -538,32 +547,36 @@ k_gather_keys_round1(const uint32_t* __restrict__ S, uint64_t n, const uint32_t*
                      const uint4* __restrict__ Taos, uint64_t N, const uint4* __restrict__ Baos,
                      uint32_t* __restrict__ Aout, const fr* __restrict__ elo, const fr* __restrict__ ehi,
                      fr* partials, int rows, unsigned long long* miss) {
-    fr acc = fr_zero(), a0 = fr_zero(), a1 = fr_zero();
+    fr_acc acc = fr_acc_zero(), a0 = fr_acc_zero(), a1 = fr_acc_zero();
     const uint64_t tile = blockIdx.x;
     const uint64_t base = tile * kInvTile + 2 * threadIdx.x;
     uint2 kn = __ldg(reinterpret_cast<const uint2*>(keys + base));
+    fr xn[2];
+    ld_fr2(S, n, base, xn);
 #pragma unroll 1
     for (int g = 0; g < 8; ++g) {
         const uint64_t i0 = base + 512 * g;
         uint2 k = kn;
-        if (g < 7) kn = __ldg(reinterpret_cast<const uint2*>(keys + i0 + 512));   // prefetch
+        fr x[2] = {xn[0], xn[1]};
+        if (g < 7) {   // prefetch the next step's keys and S
+            kn = __ldg(reinterpret_cast<const uint2*>(keys + i0 + 512));
+            ld_fr2(S, n, i0 + 512, xn);
+        }
         if (k.x >= N || k.y >= N) {
             atomic_min_i64(miss, i0);
             k.x = k.x >= N ? 0 : k.x;
             k.y = k.y >= N ? 0 : k.y;
         }
         const fr A0 = ld_aos_fr(Baos + 2 * (uint64_t)k.x), A1 = ld_aos_fr(Baos + 2 * (uint64_t)k.y);
-        fr x[2];
-        ld_fr2(S, n, i0, x);
         if (!aos_eq(Taos + 2 * (uint64_t)k.x, x[0]) || !aos_eq(Taos + 2 * (uint64_t)k.y, x[1]))
             atomic_min_i64(miss, i0);
         st_fr2(Aout, n, i0, A0, A1);
-        const fr dA = fr_sub(A1, A0), dS = fr_sub(x[1], x[0]);
-        acc = fr_add(acc, fr_mul(elo[256 * g + threadIdx.x], fr_mul(dA, dS)));
-        a0 = fr_add(a0, A0);
-        a1 = fr_add(a1, A1);
+        const fr dA = fr_sub(A1, A0), dS = fr_sub_lazy(x[1], x[0]);
+        fr_acc_add(acc, fr_mul(elo[256 * g + threadIdx.x], fr_mul(dA, dS)));
+        fr_acc_add(a0, A0);
+        fr_acc_add(a1, A1);
     }
-    fr v[3] = {fr_mul(ehi[tile], acc), a0, a1};
+    fr v[3] = {fr_mul(ehi[tile], fr_acc_final(acc)), fr_acc_final(a0), fr_acc_final(a1)};
     __shared__ fr scratch[3 * (kInvThreads / 32)];
     block_sum_fr<3>(v, scratch);
     if (threadIdx.x == 0) {
@@ -600,7 +613,8 @@ k_round(const uint32_t* __restrict__ Aold, const uint32_t* __restrict__ Sold, ui
     const uint64_t nnew = nold / 2;
     const uint32_t G = 1u << gbits;
     const uint64_t ngroups = npairs >> gbits;
-    fr H0 = fr_zero(), H1 = fr_zero(), Hinf = fr_zero(), a0 = fr_zero(), a1 = fr_zero();
+    fr H0 = fr_zero(), H1 = fr_zero(), Hinf = fr_zero();
+    fr_acc a0 = fr_acc_zero(), a1 = fr_acc_zero();
     for (uint64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
         fr c0 = fr_zero(), c1 = fr_zero(), cinf = fr_zero();
         for (uint32_t yl = threadIdx.x; yl < G; yl += blockDim.x) {
@@ -610,15 +624,15 @@ k_round(const uint32_t* __restrict__ Aold, const uint32_t* __restrict__ Sold, ui
                 {
                     fr a[4];
                     ld_fr4(Aold, nold, 4 * y, a);
-                    A0 = fr_add(a[0], fr_mul(rk, fr_sub(a[1], a[0])));
-                    A1 = fr_add(a[2], fr_mul(rk, fr_sub(a[3], a[2])));
+                    A0 = fr_add(a[0], fr_mul(rk, fr_sub_lazy(a[1], a[0])));
+                    A1 = fr_add(a[2], fr_mul(rk, fr_sub_lazy(a[3], a[2])));
                 }
                 st_fr2(Anew, nnew, 2 * y, A0, A1);
                 {
                     fr s[4];
                     ld_fr4(Sold, nold, 4 * y, s);
-                    S0 = fr_add(s[0], fr_mul(rk, fr_sub(s[1], s[0])));
-                    S1 = fr_add(s[2], fr_mul(rk, fr_sub(s[3], s[2])));
+                    S0 = fr_add(s[0], fr_mul(rk, fr_sub_lazy(s[1], s[0])));
+                    S1 = fr_add(s[2], fr_mul(rk, fr_sub_lazy(s[3], s[2])));
                 }
                 st_fr2(Snew, nnew, 2 * y, S0, S1);
             } else {
@@ -628,11 +642,11 @@ k_round(const uint32_t* __restrict__ Aold, const uint32_t* __restrict__ Sold, ui
                 A0 = a[0]; A1 = a[1]; S0 = s[0]; S1 = s[1];
             }
             const fr e = elo[yl];
-            c0 = fr_add(c0, fr_mul(e, fr_mul(A0, fr_add(S0, beta))));
-            cinf = fr_add(cinf, fr_mul(e, fr_mul(fr_sub(A1, A0), fr_sub(S1, S0))));
-            if (direct_h1) c1 = fr_add(c1, fr_mul(e, fr_mul(A1, fr_add(S1, beta))));
-            a0 = fr_add(a0, A0);
-            a1 = fr_add(a1, A1);
+            c0 = fr_add(c0, fr_mul(e, fr_mul(A0, fr_add_lazy(S0, beta))));
+            cinf = fr_add(cinf, fr_mul(e, fr_mul(fr_sub(A1, A0), fr_sub_lazy(S1, S0))));
+            if (direct_h1) c1 = fr_add(c1, fr_mul(e, fr_mul(A1, fr_add_lazy(S1, beta))));
+            fr_acc_add(a0, A0);
+            fr_acc_add(a1, A1);
         }
         const fr eh = ehi[grp];
         H0 = fr_add(H0, fr_mul(eh, c0));
@@ -640,7 +654,7 @@ k_round(const uint32_t* __restrict__ Aold, const uint32_t* __restrict__ Sold, ui
         if (direct_h1) H1 = fr_add(H1, fr_mul(eh, c1));
     }
     __shared__ fr scratch[5 * (kRoundThreads / 32)];
-    fr v[5] = {H0, H1, Hinf, a0, a1};
+    fr v[5] = {H0, H1, Hinf, fr_acc_final(a0), fr_acc_final(a1)};
     block_sum_fr<5>(v, scratch);
     if (threadIdx.x == 0) {
 #pragma unroll

@@ -77,3 +77,32 @@ def test_fs_unprepared_falls_back(ctx):
     ref = C.sumcheck(*(C.ints_to_limbs(v) for v in (A, bad, B, T)), m.cpu().numpy().astype(np.uint32),
                      C.chal_array(der["beta"], der["alpha1"], der["alpha2"], der["u"], der["r"]), TL.PAPER)
     assert pf.evals == ref.evals and pf.finals == ref.finals
+
+
+@pytest.mark.parametrize("fs", [False, True])
+def test_prepared_takes_gather_path(ctx, fs):
+    """After prepare, prove / prove_fs gather A from the cached index keys in ONE pass: no D-side inversion
+    kernels and no rerun (a workspace-layout mismatch between plans once made every key miss)."""
+    from paper_2404_16109_b200 import zkl
+    rng = random.Random(7 + fs)
+    d, n = 15, 9
+    D, N = 1 << d, 1 << n
+    T = [rng.randrange(R) for _ in range(N)]
+    S = [T[rng.randrange(N)] for _ in range(D)]
+    ctx.reserve(D, N)
+    Sv = ctx.import_canon(zkl.ints_to_canon(S))
+    tab = ctx.table(ctx.import_canon(zkl.ints_to_canon(T)))
+    m = ctx.prepare(Sv, D, tab)
+    ctx.set_profiling(True)
+    try:
+        if fs:
+            ctx.prove_fs(Sv, D, tab, m, bytes(32), TL.PAPER)
+        else:
+            u = [rng.randrange(R) for _ in range(d)]
+            r = [rng.randrange(R) for _ in range(d)]
+            ctx.prove(Sv, D, tab, m, zkl.Context.challenges(5, 7, 49, u, r))
+        names = [rec[0] for rec in ctx.profile_read()]
+    finally:
+        ctx.set_profiling(False)
+    assert names.count("k_gather_keys_round1") == 1, names
+    assert not any(nm.startswith(("k_inv_fwd", "k_inv_bwd")) for nm in names), names   # N < 4096: no tiled inversion

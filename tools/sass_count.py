@@ -50,4 +50,6 @@ if __name__ == "__main__":
         for lo, hi in loop_bodies(ins):
             body = [t for a, t in ins if lo <= a <= hi]
             cb = Counter(opcode(t) for t in body)
-            print(f"   loop [{lo:#x},{hi:#x}] {len(body)} ins:", ", ".join(f"{k}:{v}" for k, v in cb.most_common(12)))
+            spill = sum(v for k, v in cb.items() if k.startswith(("STL", "LDL")))
+            print(f"   loop [{lo:#x},{hi:#x}] {len(body)} ins (local ld/st {spill}):",
+                  ", ".join(f"{k}:{v}" for k, v in cb.most_common(12)))

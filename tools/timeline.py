@@ -6,6 +6,7 @@ import workloads as W
 from paper_2404_16109_b200 import zkl
 
 log2d = int(sys.argv[1]) if len(sys.argv) > 1 else 26
+fs = len(sys.argv) > 2 and sys.argv[2] == "fs"   # Fiat-Shamir mode (challenges derived on the device)
 D = 1 << log2d
 wl = W.activation("H", D=D)
 dev = torch.device("cuda", 0)
@@ -19,7 +20,10 @@ S, T, tmem = ctx.vec(D), ctx.vec(wl.N), ctx.table_mem(wl.N)
 m = torch.empty(wl.N, dtype=torch.int32, device=dev)
 def step():
     ctx.import_pair(txd, tyd, ch.alpha_f, T)
-    tab = ctx.table(T, tmem); ctx.prepare_pair(xd, yd, ch.alpha_f, D, tab, S, m); return ctx.prove(S, D, tab, m, chal)
+    tab = ctx.table(T, tmem); ctx.prepare_pair(xd, yd, ch.alpha_f, D, tab, S, m)
+    if fs:
+        return ctx.prove_fs(S, D, tab, m, bytes(range(32)), zkl.PAPER)
+    return ctx.prove(S, D, tab, m, chal)
 for _ in range(2): step()
 torch.cuda.synchronize()
 ctx.set_profiling(True)
