@@ -122,6 +122,18 @@ int zkl_vec_import_pair(zkl_ctx* ctx, const int32_t* x_dev, const int32_t* y_dev
 /* src (SoA Montgomery) -> canonical 32-byte LE elements (host or device, AoS). */
 int zkl_vec_export(zkl_ctx* ctx, zkl_vec src, void* canon_le32, int dst_on_device);
 
+/* ---------------------------------------------------------------- async mode (many instances)
+ * With async on, zkl_tlookup_prepare(_pair), zkl_tlookup_prove(_fs) and zkl_sumcheck_prove validate their
+ * arguments, enqueue their kernels on the ctx stream and return ZKL_OK at once; their outputs (m is on the device
+ * as usual; round_evals, finals, derived and err_index in HOST memory, which must stay valid) are delivered by
+ * zkl_ctx_wait, which also returns the first error of the pending calls, in call order (later calls' outputs
+ * are then not delivered).  At most one pending prepare and one pending prove per ctx (else E_STATE): K
+ * instances in flight = K contexts, each with its own CUDA stream and workspace, so the GPU overlaps one
+ * instance's latency-bound tail with another's bandwidth/ALU-bound rounds.  Single-rank contexts only (E_ARG).
+ * A proof whose prepared keys missed falls back to the inversion path synchronously inside zkl_ctx_wait. */
+int zkl_ctx_set_async(zkl_ctx* ctx, int on);
+int zkl_ctx_wait(zkl_ctx* ctx);
+
 /* ---------------------------------------------------------------- table handle (a2) */
 /* Device memory the caller provides for a table of N entries. */
 size_t zkl_table_bytes(uint64_t N);

@@ -13,6 +13,9 @@
 #include <string.h>
 
 #include <algorithm>
+#include <array>
+#include <functional>
+#include <memory>
 #include <new>
 #include <vector>
 
@@ -271,7 +274,7 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
     for (int k = 1; k <= p.n; ++k) p.tnb[k - 1] = grid_for(N >> k, 256, kMaxBlocks);
     p.o_tpart = take(sizeof(fr) * (size_t)kMaxRounds * 4 * kMaxBlocks);
     p.o_tnb = take(sizeof(uint32_t) * kMaxRounds);
-    p.o_tBaos = take(32 * std::max<uint64_t>(N, 4));
+    p.o_tBaos = take(64 * std::max<uint64_t>(N, 4));   // (B_j, T_j) records
     auto inv_levels = [&](InvPlan& ip, uint64_t n0) {
         ip.n[0] = n0;
         int L = 0;
@@ -422,9 +425,31 @@ struct ProveArgs {
     bool force_inversion;                // prove mode: batch-invert beta + S instead of gathering B[j(i)]
 };
 
+// a ProveArgs whose challenges live here (async completion may rerun the proof after the caller's arrays are gone)
+struct OwnedArgs {
+    ProveArgs args;
+    zkl_challenges ch;
+    std::vector<zkl_fr> u, r;
+    OwnedArgs(const ProveArgs& a, int d) : args(a), ch(*a.ch), u(a.ch->u, a.ch->u + d), r(a.ch->r, a.ch->r + d) {
+        ch.u = u.data();
+        ch.r = r.data();
+        args.ch = &ch;
+    }
+    OwnedArgs(const OwnedArgs&) = delete;
+};
+
+std::vector<std::function<int()>>& pending_of(zkl_ctx* ctx) {
+    if (!ctx->pending) ctx->pending = new std::vector<std::function<int()>>();
+    return *static_cast<std::vector<std::function<int()>>*>(ctx->pending);
+}
+
+int proof_collect(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals, zkl_final_evals* finals,
+                  int64_t* err_index, bool gather, int d);
+
 int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals, zkl_final_evals* finals,
               int64_t* err_index) {
     if (err_index) *err_index = -1;
+    if (ctx->async_mode && ctx->pend_prove) return set_err(ctx, ZKL_E_STATE, "a proof is already pending (zkl_ctx_wait)");
     const uint64_t N = a.prove_mode ? a.table->N : a.T_in.n;
     int st;
     if ((st = check_shape(ctx, D, N))) return st;
@@ -505,7 +530,7 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
             const unsigned bt = (unsigned)std::min<uint64_t>(1024, std::max<uint64_t>(32, N));
             LAUNCH(ctx, k_batch_invert, 1, bt, 4 * bt * sizeof(fr), sb, tX, N, (uint64_t)0, N, tB);
         }
-        if (gather) LAUNCH(ctx, k_soa_to_aos, grid_for(N, 256), 256, 0, s, tB, N, at<uint4>(ctx, p.o_tBaos));
+        if (gather) LAUNCH(ctx, k_pack_tb, grid_for(N, 256), 256, 0, s, Tsrc, tB, N, at<uint4>(ctx, p.o_tBaos));
         // B_out (if requested) is the variant's B, written by k_tab_init
         if ((st = table_side(ctx, p, s, s2, tB, Tsrc, a.m_dev, nullptr, a.variant, sc, tsum, tfin, a.B_out.limbs)))
             return st;
@@ -534,7 +559,7 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
             if (ctx->prep_S == a.S.limbs && ctx->prep_n == p.Dp && ctx->prep_table == a.table) {
                 // keys from the preceding prepare on this S (each still verified against T)
                 LAUNCH(ctx, k_gather_keys_round1, (unsigned)p.ntiles, kInvThreads, 0, s, a.S.limbs, p.Dp,
-                       at<uint32_t>(ctx, p.o_keys), a.table->Taos, N, at<uint4>(ctx, p.o_tBaos), Abuf,
+                       at<uint32_t>(ctx, p.o_keys), N, at<uint4>(ctx, p.o_tBaos), Abuf,
                        arena + p.rd[0].elo_off, arena + p.rd[0].ehi_off, partials + p.rd[0].part_base,
                        (int)p.ntiles, err + 2);
             } else {
@@ -627,7 +652,23 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->host_out, out, sizeof(ProofOut), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(ctx, cudaMemcpyAsync((uint8_t*)ctx->host_out + offsetof(ProofOut, err_index), err,
                                   3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    if (ctx->async_mode) {
+        // completion deferred to zkl_ctx_wait: keep the arguments (challenges copied) for the gather fallback
+        auto own = std::make_shared<OwnedArgs>(a, p.d);
+        const int d = p.d;
+        ctx->pend_prove = 1;
+        pending_of(ctx).push_back([ctx, D, own, round_evals, finals, err_index, gather, d]() {
+            ctx->pend_prove = 0;
+            return proof_collect(ctx, D, own->args, round_evals, finals, err_index, gather, d);
+        });
+        return ZKL_OK;
+    }
     if ((st = sync_stream(ctx))) return st;
+    return proof_collect(ctx, D, a, round_evals, finals, err_index, gather, p.d);
+}
+
+int proof_collect(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals, zkl_final_evals* finals,
+                  int64_t* err_index, bool gather, int d) {
     const ProofOut* ho = reinterpret_cast<const ProofOut*>(ctx->host_out);
     const unsigned long long* he = reinterpret_cast<const unsigned long long*>((const uint8_t*)ctx->host_out +
                                                                                offsetof(ProofOut, err_index));
@@ -639,9 +680,14 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
     }
     if (eMiss != ~0ull && eT == ~0ull) {
         // an S_i with no table entry (S was not the prepared lookup vector): redo with the inversion path
+        // (synchronously, also in async mode: this runs inside zkl_ctx_wait)
         ProveArgs b = a;
         b.force_inversion = true;
-        return run_proof(ctx, D, b, round_evals, finals, err_index);
+        const int was_async = ctx->async_mode;
+        ctx->async_mode = 0;
+        const int st = run_proof(ctx, D, b, round_evals, finals, err_index);
+        ctx->async_mode = was_async;
+        return st;
     }
     if (eT != ~0ull) {
         if (err_index) *err_index = (int64_t)eT;
@@ -651,7 +697,7 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
         if (err_index) *err_index = (int64_t)eS;
         return set_err(ctx, ZKL_E_DIV_ZERO_S, "beta + S_%llu = 0", eS);
     }
-    memcpy(round_evals, ho->evals, sizeof(zkl_fr) * 4 * p.d);
+    memcpy(round_evals, ho->evals, sizeof(zkl_fr) * 4 * d);
     finals->A = ho->finals[0];
     finals->S = ho->finals[1];
     finals->B = ho->finals[2];
@@ -661,10 +707,15 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
 }
 
 // ------------------------------------------------------------------ Fiat-Shamir driver (f1)
+int proof_fs_collect(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, const uint32_t* m_dev,
+                     const uint8_t* seed, int variant, zkl_vec A_out, zkl_vec B_out, zkl_fr* round_evals,
+                     zkl_final_evals* finals, zkl_fr* derived, int64_t* err_index, bool gather, int d);
+
 int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, const uint32_t* m_dev,
                  const uint8_t* seed, int variant, zkl_vec A_out, zkl_vec B_out, zkl_fr* round_evals,
                  zkl_final_evals* finals, zkl_fr* derived, int64_t* err_index, bool force_inversion) {
     if (err_index) *err_index = -1;
+    if (ctx->async_mode && ctx->pend_prove) return set_err(ctx, ZKL_E_STATE, "a proof is already pending (zkl_ctx_wait)");
     int st;
     const uint64_t N = table->N;
     if ((st = check_shape(ctx, D, N))) return st;
@@ -730,11 +781,11 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
     const bool gather = !p.small && !force_inversion;
     int h01 = 1;
     if (gather) {
-        LAUNCH(ctx, k_soa_to_aos, grid_for(N, 256), 256, 0, s, tB, N, at<uint4>(ctx, p.o_tBaos));
+        LAUNCH(ctx, k_pack_tb, grid_for(N, 256), 256, 0, s, table->T, tB, N, at<uint4>(ctx, p.o_tBaos));
         TableView tv{table->T, table->Taos, table->slots, table->Skeys, table->N, table->slot_mask};
         if (ctx->prep_S == S.limbs && ctx->prep_n == p.Dp && ctx->prep_table == table)
             LAUNCH(ctx, k_gather_keys_round1, (unsigned)p.ntiles, kInvThreads, 0, s, S.limbs, p.Dp,
-                   at<uint32_t>(ctx, p.o_keys), table->Taos, N, at<uint4>(ctx, p.o_tBaos), Abuf,
+                   at<uint32_t>(ctx, p.o_keys), N, at<uint4>(ctx, p.o_tBaos), Abuf,
                    arena + p.rd[0].elo_off, arena + p.rd[0].ehi_off, partials + p.rd[0].part_base, (int)p.ntiles,
                    err + 2);
         else
@@ -788,30 +839,55 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->host_out, out, sizeof(ProofOut), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(ctx, cudaMemcpyAsync((uint8_t*)ctx->host_out + offsetof(ProofOut, err_index), err,
                                   3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    zkl_fr* hder = reinterpret_cast<zkl_fr*>((uint8_t*)ctx->host_out + 32768);
-    CUDA_TRY(ctx, cudaMemcpyAsync(hder, dder, sizeof(zkl_fr) * (3 + 2 * p.d), cudaMemcpyDeviceToHost, s));
+    zkl_fr* hder_w = reinterpret_cast<zkl_fr*>((uint8_t*)ctx->host_out + 32768);
+    CUDA_TRY(ctx, cudaMemcpyAsync(hder_w, dder, sizeof(zkl_fr) * (3 + 2 * p.d), cudaMemcpyDeviceToHost, s));
+    if (ctx->async_mode) {
+        std::array<uint8_t, 32> sd;
+        memcpy(sd.data(), seed, 32);
+        const int d = p.d;
+        ctx->pend_prove = 1;
+        pending_of(ctx).push_back([=]() {
+            ctx->pend_prove = 0;
+            return proof_fs_collect(ctx, S, D, table, m_dev, sd.data(), variant, A_out, B_out, round_evals, finals,
+                                    derived, err_index, gather, d);
+        });
+        return ZKL_OK;
+    }
     if ((st = sync_stream(ctx))) return st;
+    return proof_fs_collect(ctx, S, D, table, m_dev, seed, variant, A_out, B_out, round_evals, finals, derived,
+                            err_index, gather, p.d);
+}
+
+int proof_fs_collect(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, const uint32_t* m_dev,
+                     const uint8_t* seed, int variant, zkl_vec A_out, zkl_vec B_out, zkl_fr* round_evals,
+                     zkl_final_evals* finals, zkl_fr* derived, int64_t* err_index, bool gather, int d) {
     const ProofOut* ho = reinterpret_cast<const ProofOut*>(ctx->host_out);
+    const zkl_fr* hder = reinterpret_cast<const zkl_fr*>((uint8_t*)ctx->host_out + 32768);
     const unsigned long long* he = reinterpret_cast<const unsigned long long*>((const uint8_t*)ctx->host_out +
                                                                                offsetof(ProofOut, err_index));
     if (he[1] != ~0ull) {
         if (err_index) *err_index = (int64_t)he[1];
         return set_err(ctx, ZKL_E_DIV_ZERO_T, "beta + T_%llu = 0", he[1]);
     }
-    if (gather && he[2] != ~0ull)
-        return run_proof_fs(ctx, S, D, table, m_dev, seed, variant, A_out, B_out, round_evals, finals, derived,
-                            err_index, true);
+    if (gather && he[2] != ~0ull) {
+        const int was_async = ctx->async_mode;
+        ctx->async_mode = 0;
+        const int st = run_proof_fs(ctx, S, D, table, m_dev, seed, variant, A_out, B_out, round_evals, finals,
+                                    derived, err_index, true);
+        ctx->async_mode = was_async;
+        return st;
+    }
     if (he[0] != ~0ull) {
         if (err_index) *err_index = (int64_t)he[0];
         return set_err(ctx, ZKL_E_DIV_ZERO_S, "beta + S_%llu = 0", he[0]);
     }
-    memcpy(round_evals, ho->evals, sizeof(zkl_fr) * 4 * p.d);
+    memcpy(round_evals, ho->evals, sizeof(zkl_fr) * 4 * d);
     finals->A = ho->finals[0];
     finals->S = ho->finals[1];
     finals->B = ho->finals[2];
     finals->T = ho->finals[3];
     finals->m = ho->finals[4];
-    memcpy(derived, hder, sizeof(zkl_fr) * (3 + 2 * p.d));
+    memcpy(derived, hder, sizeof(zkl_fr) * (3 + 2 * d));
     return ZKL_OK;
 }
 
@@ -930,6 +1006,30 @@ int zkl_ctx_create_loopback(int device, void* cuda_stream, zkl_group* group, int
     return ZKL_OK;
 }
 
+int zkl_ctx_set_async(zkl_ctx* ctx, int on) {
+    if (!ctx) return ZKL_E_ARG;
+    if (on && ctx->nranks > 1) return set_err(ctx, ZKL_E_ARG, "async mode: single-rank contexts only");
+    if (!on && (ctx->pend_prepare || ctx->pend_prove)) return set_err(ctx, ZKL_E_STATE, "pending work: zkl_ctx_wait first");
+    ctx->async_mode = on ? 1 : 0;
+    return ZKL_OK;
+}
+
+int zkl_ctx_wait(zkl_ctx* ctx) {
+    if (!ctx) return ZKL_E_ARG;
+    int st = sync_stream(ctx);
+    std::vector<std::function<int()>> work;
+    if (ctx->pending) work.swap(pending_of(ctx));
+    for (auto& f : work) {
+        if (st == ZKL_OK) {
+            st = f();
+        } else {   // an earlier completion failed: later results are not delivered
+            ctx->pend_prepare = ctx->pend_prove = 0;
+            ctx->prep_S = nullptr;
+        }
+    }
+    return st;
+}
+
 void zkl_ctx_destroy(zkl_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
@@ -945,6 +1045,7 @@ void zkl_ctx_destroy(zkl_ctx* c) {
     cudaEventDestroy(c->ev_join);
     cudaFreeHost(c->host_out);
     cudaFree(c->dscratch);
+    delete static_cast<std::vector<std::function<int()>>*>(c->pending);
     free(c);
 }
 
@@ -1148,11 +1249,15 @@ struct PairIn {
     const zkl_fr* alpha_f;
 };
 
+static int prepare_collect(zkl_ctx* ctx, zkl_vec S, const zkl_table* T, int64_t* err_index, uint64_t Dp);
+
 static int prepare_impl(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T, uint32_t* m_dev, int64_t* err_index,
                         const PairIn* pair) {
     int st;
     if (err_index) *err_index = -1;
     if ((st = check_ctx(ctx))) return st;
+    if (ctx->async_mode && ctx->pend_prepare)
+        return set_err(ctx, ZKL_E_STATE, "a prepare is already pending (zkl_ctx_wait)");
     if (!T || !m_dev) return set_err(ctx, ZKL_E_ARG, "null argument");
     if ((st = check_shape(ctx, D, T->N))) return st;
     Plan p;
@@ -1191,8 +1296,25 @@ static int prepare_impl(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T,
     }
     unsigned long long* herr = reinterpret_cast<unsigned long long*>((uint8_t*)ctx->host_out + 60000);
     CUDA_TRY(ctx, cudaMemcpyAsync(herr, err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+    if (ctx->async_mode) {
+        // the keys are valid for a proof enqueued after this (the completion below clears them on error)
+        ctx->prep_S = S.limbs;
+        ctx->prep_n = p.Dp;
+        ctx->prep_table = T;
+        ctx->pend_prepare = 1;
+        const uint64_t Dp = p.Dp;
+        pending_of(ctx).push_back([ctx, S, T, err_index, Dp]() {
+            ctx->pend_prepare = 0;
+            return prepare_collect(ctx, S, T, err_index, Dp);
+        });
+        return ZKL_OK;
+    }
     if ((st = sync_stream(ctx))) return st;
-    unsigned long long e = *herr;
+    return prepare_collect(ctx, S, T, err_index, p.Dp);
+}
+
+static int prepare_collect(zkl_ctx* ctx, zkl_vec S, const zkl_table* T, int64_t* err_index, uint64_t Dp) {
+    unsigned long long e = *reinterpret_cast<const unsigned long long*>((const uint8_t*)ctx->host_out + 60000);
     if (ctx->nranks > 1) {
         int rc = zkl_dist_min_u64(ctx, &e);
         if (rc) return rc;
@@ -1203,7 +1325,7 @@ static int prepare_impl(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T,
         return set_err(ctx, ZKL_E_NOT_IN_TABLE, "S_%llu is not in T", e);
     }
     ctx->prep_S = S.limbs;   // the index-map keys in the workspace belong to this S and table
-    ctx->prep_n = p.Dp;
+    ctx->prep_n = Dp;
     ctx->prep_table = T;
     return ZKL_OK;
 }

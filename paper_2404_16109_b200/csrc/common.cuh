@@ -174,6 +174,11 @@ struct zkl_ctx {
     uint64_t prep_n;
     const zkl_table* prep_table;
     char last_error[512];
+    // async mode (zkl_ctx_set_async): prepare / prove enqueue and return; their host-side completion (error
+    // words, outputs, the gather fallback) runs in zkl_ctx_wait, in call order.  One of each kind in flight.
+    int async_mode;
+    int pend_prepare, pend_prove;
+    void* pending;                 // std::vector<std::function<int()>>*
     // optional per-kernel timing (zkl_ctx_set_profiling): events around every launch
     int profiling;
     int nprof;

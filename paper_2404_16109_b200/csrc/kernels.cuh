@@ -500,7 +500,7 @@ __device__ __forceinline__ fr ld_aos_fr(const uint4* p) {
 }
 
 __global__ void __launch_bounds__(kInvThreads)
-k_gather_round1(const uint32_t* __restrict__ S, uint64_t n, TableView tv, const uint4* __restrict__ Baos,
+k_gather_round1(const uint32_t* __restrict__ S, uint64_t n, TableView tv, const uint4* __restrict__ TB,
                 uint32_t* __restrict__ Aout, const fr* __restrict__ elo, const fr* __restrict__ ehi, fr* partials,
                 int rows, unsigned long long* miss) {
     fr acc = fr_zero(), a0 = fr_zero(), a1 = fr_zero();
@@ -522,7 +522,7 @@ k_gather_round1(const uint32_t* __restrict__ S, uint64_t n, TableView tv, const 
             j0 = j0 < 0 ? 0 : j0;
             j1 = j1 < 0 ? 0 : j1;
         }
-        const fr A0 = ld_aos_fr(Baos + 2 * j0), A1 = ld_aos_fr(Baos + 2 * j1);
+        const fr A0 = ld_aos_fr(TB + 4 * j0), A1 = ld_aos_fr(TB + 4 * j1);
         st_fr2(Aout, n, i0, A0, A1);
         const fr dA = fr_sub(A1, A0), dS = fr_sub(x[1], x[0]);
         acc = fr_add(acc, fr_mul(elo[256 * g + threadIdx.x], fr_mul(dA, dS)));
@@ -544,7 +544,7 @@ k_gather_round1(const uint32_t* __restrict__ S, uint64_t n, TableView tv, const 
 // AoS table copy, loaded in parallel with B_key), so a stale or foreign S only costs the fallback.
 __global__ void __launch_bounds__(kInvThreads)
 k_gather_keys_round1(const uint32_t* __restrict__ S, uint64_t n, const uint32_t* __restrict__ keys,
-                     const uint4* __restrict__ Taos, uint64_t N, const uint4* __restrict__ Baos,
+                     uint64_t N, const uint4* __restrict__ TB,
                      uint32_t* __restrict__ Aout, const fr* __restrict__ elo, const fr* __restrict__ ehi,
                      fr* partials, int rows, unsigned long long* miss) {
     fr_acc acc = fr_acc_zero(), a0 = fr_acc_zero(), a1 = fr_acc_zero();
@@ -567,8 +567,10 @@ k_gather_keys_round1(const uint32_t* __restrict__ S, uint64_t n, const uint32_t*
             k.x = k.x >= N ? 0 : k.x;
             k.y = k.y >= N ? 0 : k.y;
         }
-        const fr A0 = ld_aos_fr(Baos + 2 * (uint64_t)k.x), A1 = ld_aos_fr(Baos + 2 * (uint64_t)k.y);
-        if (!aos_eq(Taos + 2 * (uint64_t)k.x, x[0]) || !aos_eq(Taos + 2 * (uint64_t)k.y, x[1]))
+        const uint4* r0 = TB + 4 * (uint64_t)k.x;
+        const uint4* r1 = TB + 4 * (uint64_t)k.y;
+        const fr A0 = ld_aos_fr(r0), A1 = ld_aos_fr(r1);
+        if (!aos_eq(r0 + 2, x[0]) || !aos_eq(r1 + 2, x[1]))
             atomic_min_i64(miss, i0);
         st_fr2(Aout, n, i0, A0, A1);
         const fr dA = fr_sub(A1, A0), dS = fr_sub_lazy(x[1], x[0]);
@@ -586,11 +588,15 @@ k_gather_keys_round1(const uint32_t* __restrict__ S, uint64_t n, const uint32_t*
     }
 }
 
-__global__ void k_soa_to_aos(const uint32_t* __restrict__ src, uint64_t n, uint4* __restrict__ dst) {
+// (B_j, T_j) packed as one 64-byte record per entry: the gather reads both from one L2 line
+__global__ void k_pack_tb(const uint32_t* __restrict__ T, const uint32_t* __restrict__ B, uint64_t n,
+                          uint4* __restrict__ dst) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const fr x = ld_fr(src, n, i);
-        dst[2 * i] = make_uint4(x.v[0], x.v[1], x.v[2], x.v[3]);
-        dst[2 * i + 1] = make_uint4(x.v[4], x.v[5], x.v[6], x.v[7]);
+        const fr b = ld_fr(B, n, i), t = ld_fr(T, n, i);
+        dst[4 * i] = make_uint4(b.v[0], b.v[1], b.v[2], b.v[3]);
+        dst[4 * i + 1] = make_uint4(b.v[4], b.v[5], b.v[6], b.v[7]);
+        dst[4 * i + 2] = make_uint4(t.v[0], t.v[1], t.v[2], t.v[3]);
+        dst[4 * i + 3] = make_uint4(t.v[4], t.v[5], t.v[6], t.v[7]);
     }
 }
 

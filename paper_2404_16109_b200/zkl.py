@@ -74,6 +74,8 @@ def lib() -> ctypes.CDLL:
             "zkl_ctx_set_workspace": ([P, P, ctypes.c_size_t], I32),
             "zkl_ctx_launch_count": ([P], U64),
             "zkl_ctx_set_profiling": ([P, I32], I32),
+            "zkl_ctx_set_async": ([P, I32], I32),
+            "zkl_ctx_wait": ([P], I32),
             "zkl_ctx_profile_read": ([P, ctypes.c_char_p, I32, ctypes.POINTER(ctypes.c_float),
                                       ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int), I32], I32),
             "zkl_vec_import": ([P, P, I32, zkl_vec, I64P], I32),
@@ -105,7 +107,7 @@ def lib() -> ctypes.CDLL:
 EXPORTED = ["zkl_strerror", "zkl_ctx_create", "zkl_nccl_unique_id", "zkl_ctx_create_dist", "zkl_ctx_destroy",
             "zkl_group_create", "zkl_group_destroy", "zkl_ctx_create_loopback",
             "zkl_last_error", "zkl_workspace_bytes", "zkl_ctx_set_workspace", "zkl_ctx_launch_count",
-            "zkl_ctx_set_profiling", "zkl_ctx_profile_read",
+            "zkl_ctx_set_profiling", "zkl_ctx_profile_read", "zkl_ctx_set_async", "zkl_ctx_wait",
             "zkl_vec_import", "zkl_vec_import_i64", "zkl_vec_import_pair", "zkl_vec_export", "zkl_table_bytes",
             "zkl_table_create", "zkl_table_destroy", "zkl_tlookup_prepare", "zkl_tlookup_prepare_pair",
             "zkl_tlookup_prove", "zkl_tlookup_prove_fs",
@@ -165,6 +167,21 @@ class Proof:
     B: Optional[Vec] = None
 
 
+class Deferred:
+    """Result of a call made in async mode (Context.set_async): filled in by Context.wait()."""
+
+    def __init__(self, make):
+        self._make, self._value, self.done = make, None, False
+
+    def _resolve(self):
+        self._value, self.done = self._make(), True
+
+    def result(self):
+        if not self.done:
+            raise RuntimeError("not completed: call Context.wait() first")
+        return self._value
+
+
 class Context:
     """One device context: stream, workspace and the zkl_ctx handle."""
 
@@ -192,6 +209,8 @@ class Context:
         self.rank, self.nranks = rank, nranks
         self.ws = None
         self._tables = []
+        self._async = False
+        self._pending = []   # (err c_int64, Deferred or None) of calls enqueued in async mode
 
     def close(self):
         if getattr(self, "h", None):
@@ -212,6 +231,28 @@ class Context:
     @property
     def launches(self) -> int:
         return int(lib().zkl_ctx_launch_count(self.h))
+
+    # -- async mode: K instances in flight = K contexts on K streams
+    def set_async(self, on: bool):
+        """In async mode prepare*/prove*/sumcheck enqueue and return at once; prove* return a Deferred."""
+        self._check(lib().zkl_ctx_set_async(self.h, 1 if on else 0))
+        self._async = bool(on)
+
+    def _defer(self, err, make=None):
+        dfr = Deferred(make) if make is not None else None
+        self._pending.append((err, dfr))
+        return dfr
+
+    def wait(self):
+        """Complete every call enqueued in async mode (raises the first error, in call order)."""
+        st = lib().zkl_ctx_wait(self.h)
+        pend, self._pending = self._pending, []
+        if st:
+            idx = next((e.value for e, _ in pend if e is not None and e.value != -1), -1)
+            raise ZklError(st, idx, lib().zkl_last_error(self.h).decode(errors="replace"))
+        for _, dfr in pend:
+            if dfr is not None:
+                dfr._resolve()
 
     def set_profiling(self, on: bool):
         self._check(lib().zkl_ctx_set_profiling(self.h, 1 if on else 0))
@@ -314,6 +355,8 @@ class Context:
         err = ctypes.c_int64(-1)
         st = lib().zkl_tlookup_prepare(self.h, S.c, D, tab.h, ctypes.c_void_p(m.data_ptr()), ctypes.byref(err))
         self._check(st, err.value)
+        if self._async:
+            self._defer(err)
         return m
 
     def prepare_pair(self, x, y, alpha_f: int, D: int, tab: "Table", S: Optional[Vec] = None, m=None):
@@ -328,6 +371,8 @@ class Context:
                                             ctypes.byref(af), D, tab.h, S.c, ctypes.c_void_p(m.data_ptr()),
                                             ctypes.byref(err))
         self._check(st, err.value)
+        if self._async:
+            self._defer(err)
         return S, m
 
     # -- a4..a9
@@ -352,7 +397,10 @@ class Context:
         st = lib().zkl_tlookup_prove(self.h, S.c, D, tab.h, ctypes.c_void_p(m.data_ptr()), ctypes.byref(ch), variant,
                                      A.c, B.c, evals, ctypes.byref(fin), ctypes.byref(err))
         self._check(st, err.value)
-        return Proof(_evals(evals, d), _finals(fin), A if want_A else None, B if want_B else None)
+        make = lambda: Proof(_evals(evals, d), _finals(fin), A if want_A else None, B if want_B else None)  # noqa: E731
+        if self._async:
+            return self._defer(err, make)
+        return make()
 
     def prove_fs(self, S: Vec, D: int, tab: "Table", m, seed: bytes, variant: int = PAPER, want_A: bool = False,
                  want_B: bool = False):
@@ -370,9 +418,14 @@ class Context:
         st = lib().zkl_tlookup_prove_fs(self.h, S.c, D, tab.h, ctypes.c_void_p(m.data_ptr()), seed, variant, A.c,
                                         B.c, evals, ctypes.byref(fin), der, ctypes.byref(err))
         self._check(st, err.value)
-        dv = [fr_to_int(der[i]) for i in range(3 + 2 * d)]
-        derived = {"beta": dv[0], "alpha1": dv[1], "alpha2": dv[2], "u": dv[3:3 + d], "r": dv[3 + d:3 + 2 * d]}
-        return Proof(_evals(evals, d), _finals(fin), A if want_A else None, B if want_B else None), derived
+
+        def make():
+            dv = [fr_to_int(der[i]) for i in range(3 + 2 * d)]
+            derived = {"beta": dv[0], "alpha1": dv[1], "alpha2": dv[2], "u": dv[3:3 + d], "r": dv[3 + d:3 + 2 * d]}
+            return Proof(_evals(evals, d), _finals(fin), A if want_A else None, B if want_B else None), derived
+        if self._async:
+            return self._defer(err, make)
+        return make()
 
     def sumcheck(self, A: Vec, S: Vec, D: int, B: Vec, T: Vec, mfr: Vec, ch, variant: int = PAPER) -> Proof:
         d = D.bit_length() - 1
@@ -381,7 +434,10 @@ class Context:
         st = lib().zkl_sumcheck_prove(self.h, A.c, S.c, D, B.c, T.c, mfr.c, ctypes.byref(ch), variant, evals,
                                       ctypes.byref(fin))
         self._check(st)
-        return Proof(_evals(evals, d), _finals(fin))
+        make = lambda: Proof(_evals(evals, d), _finals(fin))  # noqa: E731
+        if self._async:
+            return self._defer(None, make)
+        return make()
 
 
 class Table:
