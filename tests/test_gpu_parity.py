@@ -294,6 +294,25 @@ def test_prove_unprepared_nonmember_falls_back(ctx, variant):
     assert pf.evals == ref.evals and pf.finals == ref.finals
 
 
+@pytest.mark.parametrize("y", [1, 2, 3, 1 << 31, 1 << 32, (1 << 32) + 1, 1 << 64, 5 << 96, (1 << 200) + 7,
+                               (1 << 254) + 1, R - 1, R - 2, (R + 1) // 2, 0xffffffff, (1 << 64) - 1])
+def test_inverse_edge_values(ctx, y):
+    """The single-thread inversion at the top of every batched inversion (binary extended Euclid on the
+    Montgomery integer yR... here chosen directly): N = 1 makes the table side invert beta + T_0 = beta alone, and
+    beta = y R^-1 puts the integer y into the routine -- powers of two (whole zero words), 1, r - 1."""
+    zkl = zkl_mod()
+    Rinv = pow(1 << 256, -1, R)
+    beta = y * Rinv % R
+    ctx.reserve(2, 1)
+    _, tab = _table_from_ints(ctx, [0])
+    Sv = ctx.import_canon(_canon([0, 0]))
+    m = ctx.prepare(Sv, 2, tab)
+    pf = ctx.prove(Sv, 2, tab, m, zkl.Context.challenges(beta, 1, 1, [1], [1]), TL.PAPER, want_A=True, want_B=True)
+    inv = pow(beta, -1, R)
+    assert ctx.export_ints(pf.B) == [inv]
+    assert ctx.export_ints(pf.A) == [inv, inv]
+
+
 def test_shape_errors(ctx):
     zkl = zkl_mod()
     ctx.reserve(1 << 10, 1 << 4)

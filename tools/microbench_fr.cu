@@ -95,9 +95,13 @@ __global__ void k_lat(fr* out, int iters, unsigned long long* cyc) {
     unsigned long long c1 = clock64();
     fr z = fr_inv(x);
     unsigned long long c2 = clock64();
+    fr w = fr_inv_fermat(x);
+    unsigned long long c3 = clock64();
     out[0] = fr_add(x, z);
     cyc[0] = c1 - c0;
     cyc[1] = c2 - c1;
+    cyc[2] = c3 - c2;
+    cyc[3] = fr_eq(z, w) && fr_eq(fr_mul(x, z), fr_one());   // binary Euclid == Fermat, and x z = 1
 }
 
 static double mhz_from_clk() {
@@ -142,14 +146,15 @@ int main() {
     timeit("iadd", k_iadd, (uint32_t*)buf, sms * 8, 256, 20000, 16, false);
     {
         unsigned long long* cyc;
-        CK(cudaMalloc(&cyc, 16));
+        CK(cudaMalloc(&cyc, 32));
         k_lat<<<1, 1>>>((fr*)buf, 1000, cyc);
         CK(cudaDeviceSynchronize());
         k_lat<<<1, 1>>>((fr*)buf, 1000, cyc);
         CK(cudaDeviceSynchronize());
-        unsigned long long h[2];
-        CK(cudaMemcpy(h, cyc, 16, cudaMemcpyDeviceToHost));
-        printf("{\"bench\": \"latency\", \"frmul_cycles\": %.1f, \"frinv_cycles\": %llu}\n", h[0] / 1000.0, h[1]);
+        unsigned long long h[4];
+        CK(cudaMemcpy(h, cyc, 32, cudaMemcpyDeviceToHost));
+        printf("{\"bench\": \"latency\", \"frmul_cycles\": %.1f, \"frinv_cycles\": %llu, \"frinv_fermat_cycles\": %llu, "
+               "\"inverses_agree\": %llu}\n", h[0] / 1000.0, h[1], h[2], h[3]);
     }
     for (int occ : {2, 4, 8}) {
         timeit("frmul_ilp1", k_frmul<1>, (fr*)buf, sms * occ, 256, 2000, 1, true);
