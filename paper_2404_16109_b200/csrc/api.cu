@@ -108,6 +108,10 @@ struct Plan {
     bool small;          // Dp < kInvTile: the tail kernel does everything
     int k0;              // first tail round
     int fold_in;         // the tail folds its input on load
+    int kc, nchunk_rounds;   // chunked rounds kc .. kc + nchunk_rounds - 1 (k_chunk_rounds), 0 = none
+    int tkc;                 // table side: chunked rounds tkc .. tkc + kTabChunkBits - 1 (k_tab_chunk), 0 = none
+    uint64_t tnchunks;
+    uint64_t nchunks;        // blocks of the chunk launch = elements left for the tail
     RoundDesc rd[kMaxRounds];
     EqJob jobs[2 * kMaxRounds];
     int njobs;
@@ -123,7 +127,7 @@ struct Plan {
     // workspace offsets
     size_t o_out, o_sc, o_err, o_rounds, o_jobs, o_chal, o_part, o_tpart, o_tnb, o_rank, o_gath, o_repl, o_tsum,
         o_fin, o_tfin, o_gfin, o_rc, o_fs, o_small, o_derived, o_arena, o_hist, o_keys, o_tot, o_totinv, o_A, o_A1, o_S1, o_A2, o_S2, o_tB, o_tX, o_tM,
-        o_tE, o_twk, o_tBaos, total;
+        o_tE, o_twk, o_tBaos, o_chA, o_chS, total;
 };
 
 void choose_round(Plan& p, int k, uint64_t npairs, int gbits, int nblocks) {
@@ -181,6 +185,7 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
         for (k = 1; k <= p.dl; ++k) {
             const uint64_t nk = p.Dp >> (k - 1);   // elements at round k
             if (nk <= (uint64_t)kTailMax) break;
+            if (k >= 2 && nk <= kChunkMaxElems && nk >= (uint64_t)kChunk) break;   // chunked rounds from here
             if (k == 1 && prove_mode) continue;
             const uint64_t np = nk / 2;
             int gbits = 12;
@@ -191,10 +196,26 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
         }
         p.k0 = k;
         p.fold_in = 1;
+        const uint64_t nk = p.Dp >> (k - 1);
+        if (k >= 2 && k <= p.dl && nk <= kChunkMaxElems && nk >= (uint64_t)kChunk) {
+            p.kc = k;
+            p.nchunk_rounds = kChunkBits;   // nk >= 2^kChunkBits, so these rounds are all local (k <= dl)
+            p.nchunks = nk / kChunk;
+            for (int kk = k; kk < k + kChunkBits; ++kk) {
+                RoundDesc& r = p.rd[kk - 1];
+                r.gbits = std::min(10, p.dl - kk);
+                r.nblocks = (uint32_t)(p.nchunks * kChunkWarps);   // partial rows: one per warp
+                r.direct_h1 = 0;
+            }
+            p.k0 = k + kChunkBits;
+            p.fold_in = 0;                  // the tail starts from the chunks' last elements
+        }
     }
+    // tail rounds: k_tail (small path: one partial row per warp) or k_tail_warp (one row)
+    const uint32_t tail_rows = p.small ? (uint32_t)(kTailThreads / 32) : 1u;
     for (int k = p.k0; k <= p.dl; ++k) {
         p.rd[k - 1].gbits = p.dl - k;
-        p.rd[k - 1].nblocks = 1;
+        p.rd[k - 1].nblocks = tail_rows;
         p.rd[k - 1].direct_h1 = 1;
     }
     for (int k = 1; k <= p.dl; ++k) {
@@ -207,7 +228,7 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
     // replicated rounds (P > 1): all remaining coordinates are global
     for (int k = p.dl + 1; k <= p.d; ++k) {
         p.rd[k - 1].gbits = p.d - k;
-        p.rd[k - 1].nblocks = 1;
+        p.rd[k - 1].nblocks = P <= kTailWarpMax ? 1u : (uint32_t)(kTailThreads / 32);
         p.rd[k - 1].direct_h1 = 1;
     }
     // ---- eq arena jobs: per round E_lo then E_hi
@@ -272,9 +293,22 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
     p.o_tE = take(soa_bytes(N));
     p.o_twk = take(sizeof(fr) * 8 * std::max<uint64_t>(N, 2));
     for (int k = 1; k <= p.n; ++k) p.tnb[k - 1] = grid_for(N >> k, 256, kMaxBlocks);
-    p.o_tpart = take(sizeof(fr) * (size_t)kMaxRounds * 4 * kMaxBlocks);
+    if (!fs) {   // table side: multi-block rounds while the vectors are big, then chunked rounds, then one block
+        int tk = 1;
+        uint64_t tl = N;
+        while (tk <= p.n && tl > kTabChunkMaxElems) { ++tk; tl /= 2; }
+        p.tkc = 0;
+        if (tk <= p.n && tl >= (uint64_t)kTabChunk) {
+            p.tkc = tk;
+            p.tnchunks = tl / kTabChunk;
+            for (int j = 0; j < kTabChunkBits; ++j) p.tnb[tk + j - 1] = (uint32_t)(p.tnchunks * kTabChunkWarps);
+        }
+    }
+    p.o_tpart = take(sizeof(fr) * (size_t)kMaxRounds * 4 * std::max(kMaxBlocks, kTabRowsMax));
     p.o_tnb = take(sizeof(uint32_t) * kMaxRounds);
     p.o_tBaos = take(64 * std::max<uint64_t>(N, 4));   // (B_j, T_j) records
+    p.o_chA = take(soa_bytes(std::max<uint64_t>(p.nchunks, 1)));
+    p.o_chS = take(soa_bytes(std::max<uint64_t>(p.nchunks, 1)));
     auto inv_levels = [&](InvPlan& ip, uint64_t n0) {
         ip.n[0] = n0;
         int L = 0;
@@ -400,15 +434,23 @@ int table_side(zkl_ctx* ctx, const Plan& p, cudaStream_t s, cudaStream_t s2, con
     fr* tpart = at<fr>(ctx, p.o_tpart);
     uint64_t len = N;
     int k = 1;
-    for (; k <= p.n && len / 2 > kTabTailPairs; ++k) {
+    // big rounds multi-block on the main stream (before the chunked rounds, or while > kTabTailPairs pairs)
+    for (; k <= p.n && (p.tkc ? k < p.tkc : len / 2 > kTabTailPairs); ++k) {
         LAUNCH(ctx, k_tab_round, p.tnb[k - 1], 256, 0, s, cur, len, nxt, sc, k, variant,
-               tpart + (size_t)(k - 1) * 4 * kMaxBlocks);
+               tpart + (size_t)(k - 1) * 4 * kTabRowsMax, kTabRowsMax);
         fr* t = cur; cur = nxt; nxt = t;
         len /= 2;
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, s));
     CUDA_TRY(ctx, cudaStreamWaitEvent(s2, ctx->ev_fork, 0));
-    LAUNCH(ctx, k_tab_tail, 1, 256, 0, s2, cur, nxt, len, k, p.n, sc, variant, tpart, kMaxBlocks,
+    if (p.tkc) {
+        LAUNCH(ctx, k_tab_chunk, (unsigned)p.tnchunks, kTabChunkThreads, 4 * kTabChunk * sizeof(fr), s2, cur, len,
+               nxt, sc, k, variant, tpart);
+        fr* t = cur; cur = nxt; nxt = t;
+        len = p.tnchunks;
+        k += kTabChunkBits;
+    }
+    LAUNCH(ctx, k_tab_tail, 1, 256, 0, s2, cur, nxt, len, k, p.n, sc, variant, tpart, kTabRowsMax,
            at<uint32_t>(ctx, p.o_tnb), tsum, tfin);
     return ZKL_OK;
 }
@@ -600,7 +642,8 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
         }
         const uint32_t *cA = A1in, *cS = S1in;
         uint64_t len = p.Dp;
-        for (int k = a.prove_mode ? 2 : 1; k < p.k0; ++k) {
+        const int kend_rounds = p.kc ? p.kc : p.k0;   // k_round launches for rounds < kend_rounds
+        for (int k = a.prove_mode ? 2 : 1; k < kend_rounds; ++k) {
             const RoundDesc& r = p.rd[k - 1];
             fr* part = partials + r.part_base;
             if (k == 1) {
@@ -620,9 +663,22 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
                 len /= 2;
             }
         }
-        // tail input: the vectors of round k0-1 (len elements), folded with r_{k0-1} on load
-        LAUNCH(ctx, k_tail, 1, kTailThreads, tail_smem, s, cA, cS, len, 1, 0, (uint32_t*)nullptr, errS_off, err, sc,
-               p.k0, p.dl, rounds, arena, partials, fin);
+        if (p.kc) {
+            // rounds kc .. kc+9 chunk-local in shared memory (one launch); one element per chunk remains
+            uint32_t* chA = at<uint32_t>(ctx, p.o_chA);
+            uint32_t* chS = at<uint32_t>(ctx, p.o_chS);
+            const size_t chunk_smem = 2 * kChunk * sizeof(fr);
+            LAUNCH(ctx, k_chunk_rounds, (unsigned)p.nchunks, kChunkThreads, chunk_smem, s, cA, cS, len, sc, p.kc,
+                   p.nchunk_rounds, rounds, arena, partials, chA, chS);
+            cA = chA; cS = chS;
+            len = p.nchunks;
+        }
+        // tail: the chunks' last elements are the round-k0 vectors, <= kTailWarpMax of them (one warp, one
+        // partial row per round, as planned)
+        if (p.fold_in || len > (uint64_t)kTailWarpMax)
+            return set_err(ctx, ZKL_E_STATE, "internal: tail plan (fold_in %d, %llu elements)", p.fold_in,
+                           (unsigned long long)len);
+        LAUNCH(ctx, k_tail_warp, 1, 32, 0, s, cA, cS, len, sc, p.k0, p.dl, rounds, arena, partials, fin);
     }
     if (rounds_nb0 >= 0 && (uint32_t)rounds_nb0 != p.rd[0].nblocks) {
         // the plan's round-1 row count must match what the inversion wrote
@@ -640,10 +696,15 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
         if (rc) return rc;
         gathered = gath;
         // replicated last log2 P rounds on the gathered folded (A, S) pairs: P elements
-        // gfin layout: [A_0..A_{P-1}] [S_0..S_{P-1}] as AoS fr -> treat as SoA? use tail via AoS copy
-        LAUNCH(ctx, k_tail, 1, kTailThreads, tail_smem, s, (const uint32_t*)at<fr>(ctx, p.o_gfin),
-               (const uint32_t*)(at<fr>(ctx, p.o_gfin) + p.P), (uint64_t)p.P, 0, 0, (uint32_t*)nullptr, 0, err, sc,
-               p.dl + 1, p.d, rounds, arena, partials, fin);
+        // gfin: the P ranks' folded A then S, each read as a P-element vector
+        const uint32_t* gA = (const uint32_t*)at<fr>(ctx, p.o_gfin);
+        const uint32_t* gS = (const uint32_t*)(at<fr>(ctx, p.o_gfin) + p.P);
+        if (p.P <= kTailWarpMax)
+            LAUNCH(ctx, k_tail_warp, 1, 32, 0, s, gA, gS, (uint64_t)p.P, sc, p.dl + 1, p.d, rounds, arena, partials,
+                   fin);
+        else
+            LAUNCH(ctx, k_tail, 1, kTailThreads, tail_smem, s, gA, gS, (uint64_t)p.P, 0, 0, (uint32_t*)nullptr, 0,
+                   err, sc, p.dl + 1, p.d, rounds, arena, partials, fin);
         LAUNCH(ctx, k_reduce_rounds, p.d - p.dl, 256, 0, s, partials, rounds + p.dl, p.d - p.dl, repl);
     }
     CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
@@ -946,6 +1007,9 @@ static int ctx_create_common(int device, void* stream, zkl_ctx** out) {
     const size_t tail_smem = (2 * kTailMax + 4 * kTailThreads) * sizeof(fr) + 5 * (kTailThreads / 32) * sizeof(fr);
     cudaFuncSetAttribute(k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tail_smem);
     cudaFuncSetAttribute(k_batch_invert, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 1024 * (int)sizeof(fr));
+    cudaFuncSetAttribute(k_tab_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kTabChunk * (int)sizeof(fr));
+    cudaFuncSetAttribute(k_chunk_rounds, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(2 * kChunk * sizeof(fr)));
     *out = c;
     return ZKL_OK;
 }

@@ -737,11 +737,17 @@ k_tail(const uint32_t* __restrict__ Ain, const uint32_t* __restrict__ Sin, uint6
             v[3] = fr_add(v[3], A0);
             v[4] = fr_add(v[4], A1);
         }
-        block_sum_fr<5>(v, scratch);
-        if (t == 0) {
-            fr* part = partials_base + rd.part_base;
+        // warp sums -> one partial row per warp (kTailThreads / 32 rows; no block-wide reduction per round)
 #pragma unroll
-            for (int s = 0; s < 5; ++s) part[s] = v[s];   // one row (nblocks = 1)
+        for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+            for (int q = 0; q < 5; ++q) v[q] = fr_add(v[q], shfl_down_fr(v[q], off));
+        }
+        if ((t & 31) == 0) {
+            fr* part = partials_base + rd.part_base;
+            const int nw = nt >> 5;
+#pragma unroll
+            for (int q = 0; q < 5; ++q) part[q * nw + (t >> 5)] = v[q];
         }
         // fold with r_k
         const fr r = sc->r[k - 1];
@@ -763,6 +769,169 @@ k_tail(const uint32_t* __restrict__ Ain, const uint32_t* __restrict__ Sin, uint6
     if (t == 0) {
         fin[0] = As[0];
         fin[1] = Ss[0];
+    }
+}
+
+// Rounds k0..kend on n <= kTailWarpMax round-k0 elements in ONE warp: the same sums and folds as k_tail
+// without block barriers (each round costs a few dependent Fr multiplications and a shuffle reduction).
+constexpr int kTailWarpMax = 128;
+
+__global__ void __launch_bounds__(32)
+k_tail_warp(const uint32_t* __restrict__ Ain, const uint32_t* __restrict__ Sin, uint64_t n,
+            const ProofScalars* __restrict__ sc, int k0, int kend, const RoundDesc* __restrict__ rounds,
+            const fr* __restrict__ arena, fr* partials_base, fr* fin) {
+    __shared__ fr As[kTailWarpMax], Ss[kTailWarpMax];
+    const int lane = threadIdx.x;
+    const fr beta = sc->beta;
+    for (int i = lane; i < (int)n; i += 32) {
+        As[i] = ld_fr(Ain, n, i);
+        Ss[i] = ld_fr(Sin, n, i);
+    }
+    __syncwarp();
+    int len = (int)n;
+    for (int k = k0; k <= kend; ++k) {
+        const RoundDesc rd = rounds[k - 1];
+        const fr* elo = arena + rd.elo_off;
+        const fr eh = arena[rd.ehi_off];
+        const fr rk = sc->r[k - 1];
+        const int half = len / 2;
+        fr v[5] = {fr_zero(), fr_zero(), fr_zero(), fr_zero(), fr_zero()};
+        constexpr int kPer = kTailWarpMax / 2 / 32;
+        fr na[kPer], ns[kPer];
+#pragma unroll
+        for (int c = 0; c < kPer; ++c) {
+            const int y = lane + 32 * c;
+            if (y < half) {
+                const fr e = fr_mul(eh, elo[y]);
+                const fr A0 = As[2 * y], A1 = As[2 * y + 1], S0 = Ss[2 * y], S1 = Ss[2 * y + 1];
+                v[SLOT_H0] = fr_add(v[SLOT_H0], fr_mul(e, fr_mul(A0, fr_add_lazy(S0, beta))));
+                v[SLOT_H1] = fr_add(v[SLOT_H1], fr_mul(e, fr_mul(A1, fr_add_lazy(S1, beta))));
+                v[SLOT_HINF] = fr_add(v[SLOT_HINF], fr_mul(e, fr_mul(fr_sub(A1, A0), fr_sub_lazy(S1, S0))));
+                v[SLOT_A0] = fr_add(v[SLOT_A0], A0);
+                v[SLOT_A1] = fr_add(v[SLOT_A1], A1);
+                na[c] = fr_add(A0, fr_mul(rk, fr_sub_lazy(A1, A0)));
+                ns[c] = fr_add(S0, fr_mul(rk, fr_sub_lazy(S1, S0)));
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+            for (int q = 0; q < 5; ++q) v[q] = fr_add(v[q], shfl_down_fr(v[q], off));
+        }
+        if (lane == 0) {
+            fr* part = partials_base + rd.part_base;   // one row (nblocks = 1)
+#pragma unroll
+            for (int q = 0; q < 5; ++q) part[q] = v[q];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < kPer; ++c) {
+            const int y = lane + 32 * c;
+            if (y < half) {
+                As[y] = na[c];
+                Ss[y] = ns[c];
+            }
+        }
+        __syncwarp();
+        len = half;
+    }
+    if (lane == 0) {
+        fin[0] = As[0];
+        fin[1] = Ss[0];
+    }
+}
+
+// ====================================================================== a6/a9: chunked rounds
+// The pairs of round k are (2y, 2y+1), so an aligned chunk of 2^c consecutive elements folds into an aligned
+// chunk of the next round: a block that owns one chunk runs c rounds on it in shared memory with no
+// inter-block exchange (the challenges r_k are inputs; each round's sums leave as one partial row per block,
+// reduced later).  Used once the vectors are small (<= kChunkMaxElems), where one launch per round would be
+// launch- and latency-bound: rounds kc .. kc + kChunkBits - 1 in one launch, leaving one element per chunk
+// for k_tail.  Input: the round-(kc-1) vectors (2 kChunk elements per block, folded with r_{kc-1} on load).
+constexpr int kChunkBits = 10;
+constexpr int kChunk = 1 << kChunkBits;
+constexpr int kChunkThreads = 256;
+constexpr uint64_t kChunkMaxElems = 1ull << 17;   // chunk rounds start at the first round with <= 2^17 elements
+constexpr int kChunkWarps = kChunkThreads / 32;   // partial rows per chunk and round: one per warp
+
+__global__ void __launch_bounds__(kChunkThreads, 2)
+k_chunk_rounds(const uint32_t* __restrict__ Ain, const uint32_t* __restrict__ Sin, uint64_t nin,
+               const ProofScalars* __restrict__ sc, int kc, int nrounds, const RoundDesc* __restrict__ rounds,
+               const fr* __restrict__ arena, fr* partials_base, uint32_t* __restrict__ Aout,
+               uint32_t* __restrict__ Sout) {
+    extern __shared__ fr smem_fr[];
+    fr* As = smem_fr;
+    fr* Ss = smem_fr + kChunk;
+    const int t = threadIdx.x, nt = blockDim.x;
+    const uint64_t nchunks = gridDim.x;
+    const fr beta = sc->beta;
+    {
+        const fr r = sc->r[kc - 2];
+        const uint64_t base = 2 * (uint64_t)blockIdx.x * kChunk;
+        for (int i = t; i < kChunk; i += nt) {
+            fr a[2], s2[2];
+            ld_fr2(Ain, nin, base + 2 * i, a);
+            ld_fr2(Sin, nin, base + 2 * i, s2);
+            As[i] = fr_add(a[0], fr_mul(r, fr_sub_lazy(a[1], a[0])));
+            Ss[i] = fr_add(s2[0], fr_mul(r, fr_sub_lazy(s2[1], s2[0])));
+        }
+    }
+    __syncthreads();
+    int len = kChunk;
+    for (int j = 0; j < nrounds; ++j) {
+        const int k = kc + j;
+        const RoundDesc rd = rounds[k - 1];
+        const fr* elo = arena + rd.elo_off;
+        const fr* ehi = arena + rd.ehi_off;
+        const uint32_t gmask = (1u << rd.gbits) - 1u;
+        const int half = len / 2;
+        const fr rk = sc->r[k - 1];
+        fr v[5] = {fr_zero(), fr_zero(), fr_zero(), fr_zero(), fr_zero()};
+        constexpr int kPer = kChunk / 2 / kChunkThreads;   // pairs per thread in the first chunk round
+        fr na[kPer], ns[kPer];
+#pragma unroll
+        for (int c = 0; c < kPer; ++c) {
+            const int yl = t + c * nt;
+            if (yl < half) {
+                const uint64_t y = (uint64_t)blockIdx.x * half + yl;   // pair index of round k (this rank)
+                const fr e = fr_mul(ehi[y >> rd.gbits], elo[y & gmask]);
+                const fr A0 = As[2 * yl], A1 = As[2 * yl + 1], S0 = Ss[2 * yl], S1 = Ss[2 * yl + 1];
+                v[SLOT_H0] = fr_add(v[SLOT_H0], fr_mul(e, fr_mul(A0, fr_add_lazy(S0, beta))));
+                if (rd.direct_h1) v[SLOT_H1] = fr_add(v[SLOT_H1], fr_mul(e, fr_mul(A1, fr_add_lazy(S1, beta))));
+                v[SLOT_HINF] = fr_add(v[SLOT_HINF], fr_mul(e, fr_mul(fr_sub(A1, A0), fr_sub_lazy(S1, S0))));
+                v[SLOT_A0] = fr_add(v[SLOT_A0], A0);
+                v[SLOT_A1] = fr_add(v[SLOT_A1], A1);
+                na[c] = fr_add(A0, fr_mul(rk, fr_sub_lazy(A1, A0)));
+                ns[c] = fr_add(S0, fr_mul(rk, fr_sub_lazy(S1, S0)));
+            }
+        }
+        // warp sums -> one partial row per warp (no block-wide reduction on this latency-bound path)
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+            for (int q = 0; q < 5; ++q) v[q] = fr_add(v[q], shfl_down_fr(v[q], off));
+        }
+        if ((t & 31) == 0) {
+            fr* part = partials_base + rd.part_base;
+            const uint64_t rows = nchunks * kChunkWarps, row = (uint64_t)blockIdx.x * kChunkWarps + (t >> 5);
+#pragma unroll
+            for (int q = 0; q < 5; ++q) part[(uint64_t)q * rows + row] = v[q];
+        }
+        __syncthreads();   // every pair of this round has been read
+#pragma unroll
+        for (int c = 0; c < kPer; ++c) {
+            const int yl = t + c * nt;
+            if (yl < half) {
+                As[yl] = na[c];
+                Ss[yl] = ns[c];
+            }
+        }
+        __syncthreads();
+        len = half;
+    }
+    if (t == 0) {
+        st_fr(Aout, nchunks, blockIdx.x, As[0]);
+        st_fr(Sout, nchunks, blockIdx.x, Ss[0]);
     }
 }
 
@@ -835,7 +1004,7 @@ __device__ __forceinline__ void tab_pair(const fr* cur, uint64_t len, uint64_t y
 
 __global__ void __launch_bounds__(256)
 k_tab_round(const fr* __restrict__ cur, uint64_t len, fr* nxt, const ProofScalars* __restrict__ sc, int k, int variant,
-            fr* tpart) {
+            fr* tpart, int rows_max) {
     const fr beta = sc->beta, alpha2 = sc->alpha2, r = sc->r[k - 1];
     fr g[4] = {fr_zero(), fr_zero(), fr_zero(), fr_zero()};
     for (uint64_t y = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; y < len / 2; y += (uint64_t)gridDim.x * blockDim.x)
@@ -843,7 +1012,77 @@ k_tab_round(const fr* __restrict__ cur, uint64_t len, fr* nxt, const ProofScalar
     __shared__ fr scratch[4 * 8];
     block_sum_fr<4>(g, scratch);
     if (threadIdx.x == 0) {
-        for (int q = 0; q < 4; ++q) tpart[q * kMaxBlocks + blockIdx.x] = g[q];   // row stride kMaxBlocks
+        for (int q = 0; q < 4; ++q) tpart[q * rows_max + blockIdx.x] = g[q];   // row stride rows_max
+    }
+}
+
+// Chunked table rounds (as k_chunk_rounds on the D side): a block owns kTabChunk consecutive entries of the
+// four working vectors and runs kTabChunkBits rounds on them in shared memory; partial rows per warp.
+// out: the chunks' last entries, AoS [B | T | M | E] with stride nchunks (= gridDim.x).
+constexpr int kTabChunkBits = 9;
+constexpr int kTabChunk = 1 << kTabChunkBits;
+constexpr int kTabChunkThreads = kTabChunk / 2;
+constexpr int kTabChunkWarps = kTabChunkThreads / 32;
+constexpr uint64_t kTabChunkMaxElems = (uint64_t)kTabChunk << 8;   // <= 256 chunks; bigger rounds multi-block
+constexpr int kTabRowsMax = 256 * kTabChunkWarps;                  // partial-row stride per round and slot
+
+__global__ void __launch_bounds__(kTabChunkThreads)
+k_tab_chunk(const fr* __restrict__ cur, uint64_t len, fr* __restrict__ out, const ProofScalars* __restrict__ sc,
+            int k0, int variant, fr* tpart) {
+    extern __shared__ fr smem_fr[];
+    fr* V = smem_fr;   // [4][kTabChunk]
+    const int t = threadIdx.x;
+    const uint64_t nchunks = gridDim.x, base = (uint64_t)blockIdx.x * kTabChunk;
+    for (int i = t; i < kTabChunk; i += blockDim.x) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) V[q * kTabChunk + i] = cur[q * len + base + i];
+    }
+    __syncthreads();
+    const fr beta = sc->beta, alpha2 = sc->alpha2;
+    int l = kTabChunk;
+    for (int j = 0; j < kTabChunkBits; ++j) {
+        const int k = k0 + j;
+        const int half = l / 2;
+        const fr r = sc->r[k - 1];
+        fr g[4] = {fr_zero(), fr_zero(), fr_zero(), fr_zero()};
+        fr nv[4];
+        if (t < half) {
+            fr a0[4], d[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                a0[q] = V[q * kTabChunk + 2 * t];
+                d[q] = fr_sub(V[q * kTabChunk + 2 * t + 1], a0[q]);
+            }
+            fr bt = a0[0], tt = a0[1], mt = a0[2], et = a0[3];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (q > 0) { bt = fr_add(bt, d[0]); tt = fr_add(tt, d[1]); mt = fr_add(mt, d[2]); et = fr_add(et, d[3]); }
+                g[q] = tab_term(bt, tt, mt, et, beta, alpha2, variant);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) nv[q] = fr_add(a0[q], fr_mul(r, d[q]));
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) g[q] = fr_add(g[q], shfl_down_fr(g[q], off));
+        }
+        if ((t & 31) == 0) {
+            const uint64_t row = (uint64_t)blockIdx.x * kTabChunkWarps + (t >> 5);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) tpart[((uint64_t)(k - 1) * 4 + q) * kTabRowsMax + row] = g[q];
+        }
+        __syncthreads();
+        if (t < half) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) V[q * kTabChunk + t] = nv[q];
+        }
+        __syncthreads();
+        l = half;
+    }
+    if (t == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) out[q * nchunks + blockIdx.x] = V[q * kTabChunk];
     }
 }
 
