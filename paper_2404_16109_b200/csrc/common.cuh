@@ -73,6 +73,17 @@ __device__ __forceinline__ fr shfl_down_fr(const fr& x, int off) {
     return y;
 }
 
+// One 256-bit read-only global load (sm_100: LDG.E.ENL2.256): a whole Fr element at a 32-byte aligned
+// address in one instruction -- half the L1 wavefronts of two 128-bit loads for scattered (gather) accesses.
+__device__ __forceinline__ fr ld_fr_256(const void* p) {
+    fr x;
+    asm("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(x.v[0]), "=r"(x.v[1]), "=r"(x.v[2]), "=r"(x.v[3]), "=r"(x.v[4]), "=r"(x.v[5]), "=r"(x.v[6]),
+          "=r"(x.v[7])
+        : "l"(p));
+    return x;
+}
+
 // Sum of NV Fr values over the block; result valid in thread 0.  `scratch` holds
 // NV * (blockDim/32) fr.  Contains __syncthreads (all threads must call).
 template <int NV>

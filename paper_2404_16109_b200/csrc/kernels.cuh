@@ -121,9 +121,7 @@ struct TableView {
 };
 
 __device__ __forceinline__ bool aos_eq(const uint4* p, const fr& x) {
-    const uint4 a = __ldg(p), b = __ldg(p + 1);
-    return ((a.x ^ x.v[0]) | (a.y ^ x.v[1]) | (a.z ^ x.v[2]) | (a.w ^ x.v[3]) | (b.x ^ x.v[4]) | (b.y ^ x.v[5]) |
-            (b.z ^ x.v[6]) | (b.w ^ x.v[7])) == 0;
+    return fr_eq(ld_fr_256(p), x);
 }
 
 // index of x in T, or -1 (linear probing; slot index and slot key are loaded together)
@@ -465,7 +463,7 @@ k_inv_bwd(const uint32_t* __restrict__ X, uint64_t n, const ProofScalars* __rest
             st_fr2(slots, n, i0, A0, A1);
             if (eval) {
                 const fr dA = fr_sub(A1, A0), dS = fr_sub(x[1], x[0]);
-                acc = fr_add(acc, fr_mul(elo[256 * g + threadIdx.x], fr_mul(dA, dS)));
+                acc = fr_add(acc, fr_mul(ld_fr_256(elo + 256 * g + threadIdx.x), fr_mul(dA, dS)));
                 a0 = fr_add(a0, A0);
                 a1 = fr_add(a1, A1);
             }
@@ -491,13 +489,7 @@ k_inv_bwd(const uint32_t* __restrict__ X, uint64_t n, const ProofScalars* __rest
 // Same tile / thread layout as k_inv_bwd<true>, and the same fused round-1 evaluation (a5).  An S_i with
 // no table entry (possible only when prove is called on an S that was not prepared, e.g. a tamper trial)
 // sets *miss; the host then redoes the proof with the inversion path (bit-identical A by definition).
-__device__ __forceinline__ fr ld_aos_fr(const uint4* p) {
-    const uint4 a = __ldg(p), b = __ldg(p + 1);
-    fr x;
-    x.v[0] = a.x; x.v[1] = a.y; x.v[2] = a.z; x.v[3] = a.w;
-    x.v[4] = b.x; x.v[5] = b.y; x.v[6] = b.z; x.v[7] = b.w;
-    return x;
-}
+__device__ __forceinline__ fr ld_aos_fr(const uint4* p) { return ld_fr_256(p); }
 
 __global__ void __launch_bounds__(kInvThreads)
 k_gather_round1(const uint32_t* __restrict__ S, uint64_t n, TableView tv, const uint4* __restrict__ TB,
@@ -525,7 +517,7 @@ k_gather_round1(const uint32_t* __restrict__ S, uint64_t n, TableView tv, const 
         const fr A0 = ld_aos_fr(TB + 4 * j0), A1 = ld_aos_fr(TB + 4 * j1);
         st_fr2(Aout, n, i0, A0, A1);
         const fr dA = fr_sub(A1, A0), dS = fr_sub(x[1], x[0]);
-        acc = fr_add(acc, fr_mul(elo[256 * g + threadIdx.x], fr_mul(dA, dS)));
+        acc = fr_add(acc, fr_mul(ld_fr_256(elo + 256 * g + threadIdx.x), fr_mul(dA, dS)));
         a0 = fr_add(a0, A0);
         a1 = fr_add(a1, A1);
     }
@@ -569,7 +561,7 @@ k_gather_keys_round1(const uint32_t* __restrict__ S, uint64_t n, const uint32_t*
             atomic_min_i64(miss, i0);
         st_fr2(Aout, n, i0, A0, A1);
         const fr dA = fr_sub(A1, A0), dS = fr_sub_lazy(x[1], x[0]);
-        acc = fr_add(acc, fr_mul(elo[256 * g + threadIdx.x], fr_mul(dA, dS)));
+        acc = fr_add(acc, fr_mul(ld_fr_256(elo + 256 * g + threadIdx.x), fr_mul(dA, dS)));
         a0 = fr_add(a0, A0);
         a1 = fr_add(a1, A1);
     }
@@ -642,7 +634,7 @@ k_round(const uint32_t* __restrict__ Aold, const uint32_t* __restrict__ Sold, ui
                 ld_fr2(Sold, nold, 2 * y, s);
                 A0 = a[0]; A1 = a[1]; S0 = s[0]; S1 = s[1];
             }
-            const fr e = elo[yl];
+            const fr e = ld_fr_256(elo + yl);
             c0 = fr_add(c0, fr_mul(e, fr_mul(A0, fr_add_lazy(S0, beta))));
             cinf = fr_add(cinf, fr_mul(e, fr_mul(fr_sub(A1, A0), fr_sub_lazy(S1, S0))));
             if (direct_h1) c1 = fr_add(c1, fr_mul(e, fr_mul(A1, fr_add_lazy(S1, beta))));

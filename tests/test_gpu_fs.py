@@ -106,3 +106,35 @@ def test_prepared_takes_gather_path(ctx, fs):
         ctx.set_profiling(False)
     assert names.count("k_gather_keys_round1") == 1, names
     assert not any(nm.startswith(("k_inv_fwd", "k_inv_bwd")) for nm in names), names   # N < 4096: no tiled inversion
+
+
+@pytest.mark.parametrize("fs", [False, True])
+def test_prepared_then_rewritten_in_place(ctx, fs):
+    """prepare(S), then S overwritten in place by S' (every element still in T, one moved to another entry): the
+    cached keys no longer describe S'; the per-element check against T sends the proof through the inversion path, so the
+    transcript is that of S' (with the m of S', which the caller passes)."""
+    from paper_2404_16109_b200 import zkl
+    rng = random.Random(23 + fs)
+    d, n = 14, 7
+    D, N = 1 << d, 1 << n
+    T = [rng.randrange(R) for _ in range(N)]
+    S = [T[rng.randrange(N)] for _ in range(D)]
+    S2 = list(S)
+    S2[4097] = T[(T.index(S[4097]) + 3) % N]
+    ctx.reserve(D, N)
+    Sv = ctx.import_canon(zkl.ints_to_canon(S))
+    tab = ctx.table(ctx.import_canon(zkl.ints_to_canon(T)))
+    ctx.prepare(Sv, D, tab)
+    ctx.import_canon(zkl.ints_to_canon(S2), dst=Sv)
+    import torch
+    m2 = torch.from_numpy(np.bincount([T.index(s) for s in S2], minlength=N).astype(np.int32)).to(ctx.device)
+    if fs:
+        seed = bytes(range(1, 33))
+        pf, der = ctx.prove_fs(Sv, D, tab, m2, seed, TL.PAPER)
+        ch = (der["beta"], der["alpha1"], der["alpha2"], der["u"], der["r"])
+    else:
+        ch = (rng.randrange(R), rng.randrange(R), rng.randrange(R), [rng.randrange(R) for _ in range(d)],
+              [rng.randrange(R) for _ in range(d)])
+        pf = ctx.prove(Sv, D, tab, m2, zkl.Context.challenges(*ch))
+    ref = C.prove(C.ints_to_limbs(S2), C.ints_to_limbs(T), C.chal_array(*ch), TL.PAPER)
+    assert pf.evals == ref.evals and pf.finals == ref.finals
