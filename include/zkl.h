@@ -122,6 +122,21 @@ int zkl_vec_import_pair(zkl_ctx* ctx, const int32_t* x_dev, const int32_t* y_dev
 /* src (SoA Montgomery) -> canonical 32-byte LE elements (host or device, AoS). */
 int zkl_vec_export(zkl_ctx* ctx, zkl_vec src, void* canon_le32, int dst_on_device);
 
+/* ---------------------------------------------------------------- matmul sumcheck
+ * PAPER.md:463-467 (§5.1.1, Eq. matmul): C = A B with A in F^{m x n}, B in F^{n x p} is proved by the sumcheck
+ *     C~(u, v) = sum_{i in {0,1}^{log2 n}} A~(u, i) B~(i, v).
+ * A, B: quantised int32 entries (mapped into F as x mod r), row-major, DEVICE, m x n and n x p;
+ * m, n, p powers of two, n <= 2^39.  u (log2 m), v (log2 p), r (log2 n): canonical challenges, HOST (u[0] pairs
+ * with the row MSB; r[k-1] is round k's challenge, binding coordinate log2(n) - k of i, pairs (2y, 2y+1)).
+ * Outputs: a_i = A~(u, i) and b_i = B~(i, v) into a_out / b_out (device SoA Montgomery vectors of n; limbs may be
+ * NULL), claim = sum_i a_i b_i = C~(u, v) (host), round_evals[k-1][t] = g_k(t), t = 0, 1, 2 (host, 3 log2 n
+ * values), finals = [a~(w), b~(w)] at the bound point (host).  Uses the ctx workspace (zkl_matmul_workspace_bytes;
+ * it replaces any prepared index keys).  Synchronous only (E_STATE in async mode).  E_SHAPE, E_NONCANONICAL, E_OOM. */
+size_t zkl_matmul_workspace_bytes(uint64_t m, uint64_t n, uint64_t p);
+int zkl_matmul_prove(zkl_ctx* ctx, const int32_t* A, const int32_t* B, uint64_t m, uint64_t n, uint64_t p,
+                     const zkl_fr* u, const zkl_fr* v, const zkl_fr* r, zkl_vec a_out, zkl_vec b_out, zkl_fr* claim,
+                     zkl_fr* round_evals, zkl_fr* finals);
+
 /* ---------------------------------------------------------------- async mode (many instances)
  * With async on, zkl_tlookup_prepare(_pair), zkl_tlookup_prove(_fs) and zkl_sumcheck_prove validate their
  * arguments, enqueue their kernels on the ctx stream and return ZKL_OK at once; their outputs (m is on the device

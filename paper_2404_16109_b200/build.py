@@ -11,7 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libzkl.so")
 SOURCES = ["api.cu"]
-DEPS = ["api.cu", "kernels.cuh", "common.cuh", "fr.cuh", "nccl_loader.h"]
+DEPS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh", ".h")))   # every source and header
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 def _nccl_include() -> str:
     import importlib.util

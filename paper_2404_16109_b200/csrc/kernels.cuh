@@ -675,7 +675,6 @@ k_tail(const uint32_t* __restrict__ Ain, const uint32_t* __restrict__ Sin, uint6
     fr* Ss = smem_fr + kTailMax;   // n
     fr* tree = smem_fr + 2 * kTailMax;        // 2 nt
     fr* inv = tree + 2 * nt;                  // 2 nt
-    fr* scratch = inv + 2 * nt;               // 5 * nt/32
     const fr beta = sc->beta;
     if (fold_in) {
         const fr r = sc->r[k0 - 2];

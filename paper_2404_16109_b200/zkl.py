@@ -75,6 +75,8 @@ def lib() -> ctypes.CDLL:
             "zkl_ctx_launch_count": ([P], U64),
             "zkl_ctx_set_profiling": ([P, I32], I32),
             "zkl_ctx_set_async": ([P, I32], I32),
+            "zkl_matmul_workspace_bytes": ([U64, U64, U64], ctypes.c_size_t),
+            "zkl_matmul_prove": ([P, P, P, U64, U64, U64, P, P, P, zkl_vec, zkl_vec, P, P, P], I32),
             "zkl_ctx_wait": ([P], I32),
             "zkl_ctx_profile_read": ([P, ctypes.c_char_p, I32, ctypes.POINTER(ctypes.c_float),
                                       ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int), I32], I32),
@@ -108,6 +110,7 @@ EXPORTED = ["zkl_strerror", "zkl_ctx_create", "zkl_nccl_unique_id", "zkl_ctx_cre
             "zkl_group_create", "zkl_group_destroy", "zkl_ctx_create_loopback",
             "zkl_last_error", "zkl_workspace_bytes", "zkl_ctx_set_workspace", "zkl_ctx_launch_count",
             "zkl_ctx_set_profiling", "zkl_ctx_profile_read", "zkl_ctx_set_async", "zkl_ctx_wait",
+            "zkl_matmul_workspace_bytes", "zkl_matmul_prove",
             "zkl_vec_import", "zkl_vec_import_i64", "zkl_vec_import_pair", "zkl_vec_export", "zkl_table_bytes",
             "zkl_table_create", "zkl_table_destroy", "zkl_tlookup_prepare", "zkl_tlookup_prepare_pair",
             "zkl_tlookup_prove", "zkl_tlookup_prove_fs",
@@ -278,14 +281,17 @@ class Context:
         need = int(lib().zkl_workspace_bytes(D_local, N, self.nranks))
         if need == 0:
             raise ZklError(2, -1, f"bad shape D_local={D_local} N={N}")
-        if self.ws is None or self.ws.numel() < need:
+        self._ensure_ws(need)
+
+    def _ensure_ws(self, need: int):
+        if self.ws is None or self.ws.numel() < need + 256:
             self.ws = None
             self.torch.cuda.synchronize(self.device)
             self.torch.cuda.empty_cache()
             self.ws = self.torch.empty(need + 256, dtype=self.torch.uint8, device=self.device)
         ptr = self.ws.data_ptr()
         pad = (-ptr) % 256
-        self._check(lib().zkl_ctx_set_workspace(self.h, ctypes.c_void_p(ptr + pad), need))
+        self._check(lib().zkl_ctx_set_workspace(self.h, ctypes.c_void_p(ptr + pad), self.ws.numel() - pad))
 
     def vec(self, n: int) -> Vec:
         return Vec(self.torch.empty(max(8 * n, 32), dtype=self.torch.int32, device=self.device), n)
@@ -438,6 +444,39 @@ class Context:
         if self._async:
             return self._defer(None, make)
         return make()
+
+    # -- f4: matmul sumcheck
+    def matmul_prove(self, A, B, u: Sequence[int], v: Sequence[int], r: Sequence[int], want_ab: bool = False):
+        """Sumcheck of C~(u, v) = sum_i A~(u, i) B~(i, v) for int32 A (m x n), B (n x p) (torch device tensors or
+        arrays).  Returns dict(claim, evals [[g_k(0), g_k(1), g_k(2)]...], finals [a~(w), b~(w)], a, b)."""
+        tA = A if hasattr(A, "data_ptr") else self.torch.as_tensor(np.asarray(A, np.int32)).to(self.device)
+        tB = B if hasattr(B, "data_ptr") else self.torch.as_tensor(np.asarray(B, np.int32)).to(self.device)
+        if tA.dtype != self.torch.int32 or tB.dtype != self.torch.int32 or tA.dim() != 2 or tB.dim() != 2:
+            raise ValueError("A, B: 2-D int32")
+        tA, tB = tA.contiguous(), tB.contiguous()
+        m, n = tA.shape
+        n2, p = tB.shape
+        if n != n2:
+            raise ValueError("inner dimensions differ")
+        need = int(lib().zkl_matmul_workspace_bytes(m, n, p))
+        if need == 0:
+            raise ZklError(2, -1, f"bad shape m={m} n={n} p={p}")
+        self._ensure_ws(need)
+        L = n.bit_length() - 1
+        U = (zkl_fr * max(len(u), 1))(*[fr_from_int(x % R_MODULUS) for x in u])
+        V = (zkl_fr * max(len(v), 1))(*[fr_from_int(x % R_MODULUS) for x in v])
+        Rr = (zkl_fr * max(len(r), 1))(*[fr_from_int(x % R_MODULUS) for x in r])
+        a = self.vec(n) if want_ab else Vec(None, n)
+        b = self.vec(n) if want_ab else Vec(None, n)
+        claim = zkl_fr()
+        ev = (zkl_fr * (3 * max(L, 1)))()
+        fin = (zkl_fr * 2)()
+        st = lib().zkl_matmul_prove(self.h, ctypes.c_void_p(tA.data_ptr()), ctypes.c_void_p(tB.data_ptr()), m, n, p,
+                                    U, V, Rr, a.c, b.c, ctypes.byref(claim), ev, fin)
+        self._check(st)
+        return {"claim": fr_to_int(claim), "evals": [[fr_to_int(ev[3 * k + t]) for t in range(3)] for k in range(L)],
+                "finals": [fr_to_int(fin[0]), fr_to_int(fin[1])], "a": a if want_ab else None,
+                "b": b if want_ab else None}
 
 
 class Table:
