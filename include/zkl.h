@@ -137,6 +137,38 @@ int zkl_matmul_prove(zkl_ctx* ctx, const int32_t* A, const int32_t* B, uint64_t 
                      const zkl_fr* u, const zkl_fr* v, const zkl_fr* r, zkl_vec a_out, zkl_vec b_out, zkl_fr* claim,
                      zkl_fr* round_evals, zkl_fr* finals);
 
+/* ---------------------------------------------------------------- Hyrax / Pedersen commitments
+ * PAPER.md:187-203 (§3.4; Hyrax = Pedersen without trusted setup, homomorphic), Protocol 1 lines 261, 267-269, 275.
+ * Group: BLS12-381 G1 (y^2 = x^3 + 4 over F_q).  A vector S of D = rows x cols Fr elements (row-major) commits to
+ * rows points C_j = sum_i S[j cols + i] G_i + rho_j H.  G_0..G_{cols-1}, H are public: hashed to the curve from
+ * labels by try-and-increment, so no trusted setup.  Points leave the library affine with
+ * canonical little-endian F_q coordinates (infinity = 1 for the point at infinity, coordinates 0). */
+typedef struct {
+    uint32_t x[12];
+    uint32_t y[12];
+    uint32_t infinity;
+} zkl_g1;
+
+/* Device bytes of the public parameters for `cols` generators (+ H), with their 4-bit window tables. */
+size_t zkl_hyrax_pp_bytes(uint64_t cols);
+/* Derive the generators and tables into caller-owned device memory pp (>= zkl_hyrax_pp_bytes). cols power of 2. */
+int zkl_hyrax_setup(zkl_ctx* ctx, uint64_t cols, void* pp_dev, size_t pp_bytes);
+/* Copy G_0..G_{cols-1}, H (cols + 1 points) to host memory. */
+int zkl_hyrax_export_generators(zkl_ctx* ctx, const void* pp_dev, uint64_t cols, zkl_g1* out_host);
+/* Workspace bytes (ctx workspace) of zkl_hyrax_commit / zkl_hyrax_prove_eval for D elements in rows of cols. */
+size_t zkl_hyrax_workspace_bytes(uint64_t D, uint64_t cols);
+/* Commit(S, rho; pp): C_host[j] for j < D / cols.  rho: host, D / cols canonical blinds, or NULL (no hiding, as
+ * tlookup-Setup's Commit(T; 0)).  S: device SoA Montgomery vector (n >= D).  E_SHAPE, E_NONCANONICAL,
+ * E_OOM. */
+int zkl_hyrax_commit(zkl_ctx* ctx, const void* pp_dev, uint64_t cols, zkl_vec S, uint64_t D, const zkl_fr* rho,
+                     zkl_g1* C_host);
+/* ProveEval in the row-restriction form: v = (v_rows, v_cols), host, log2 D canonical values, the
+ * first log2(D / cols) for the row index (high bits).  w_out (device, cols) = sum_j e~(v_rows, j) S_row_j, and
+ * y_host = <w, e~(v_cols, .)> = S~(v).  The verifier checks Com(w, sum_j e~ rho_j) = sum_j e~(v_rows, j) C_j; the
+ * O(log D) inner-product argument on w is not part of this build. */
+int zkl_hyrax_prove_eval(zkl_ctx* ctx, zkl_vec S, uint64_t D, uint64_t cols, const zkl_fr* v, zkl_vec w_out,
+                         zkl_fr* y_host);
+
 /* ---------------------------------------------------------------- async mode (many instances)
  * With async on, zkl_tlookup_prepare(_pair), zkl_tlookup_prove(_fs) and zkl_sumcheck_prove validate their
  * arguments, enqueue their kernels on the ctx stream and return ZKL_OK at once; their outputs (m is on the device

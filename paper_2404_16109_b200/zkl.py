@@ -28,6 +28,17 @@ class zkl_fr(ctypes.Structure):
     _fields_ = [("w", ctypes.c_uint32 * 8)]
 
 
+class zkl_g1(ctypes.Structure):
+    _fields_ = [("x", ctypes.c_uint32 * 12), ("y", ctypes.c_uint32 * 12), ("infinity", ctypes.c_uint32)]
+
+
+def g1_to_py(p: "zkl_g1"):
+    """Affine point -> (x, y) Python ints, or None for the point at infinity."""
+    if p.infinity:
+        return None
+    return (sum(int(p.x[i]) << (32 * i) for i in range(12)), sum(int(p.y[i]) << (32 * i) for i in range(12)))
+
+
 class zkl_vec(ctypes.Structure):
     _fields_ = [("limbs", ctypes.c_void_p), ("n", ctypes.c_uint64)]
 
@@ -76,6 +87,12 @@ def lib() -> ctypes.CDLL:
             "zkl_ctx_set_profiling": ([P, I32], I32),
             "zkl_ctx_set_async": ([P, I32], I32),
             "zkl_matmul_workspace_bytes": ([U64, U64, U64], ctypes.c_size_t),
+            "zkl_hyrax_pp_bytes": ([U64], ctypes.c_size_t),
+            "zkl_hyrax_setup": ([P, U64, P, ctypes.c_size_t], I32),
+            "zkl_hyrax_export_generators": ([P, P, U64, P], I32),
+            "zkl_hyrax_workspace_bytes": ([U64, U64], ctypes.c_size_t),
+            "zkl_hyrax_commit": ([P, P, U64, zkl_vec, U64, P, P], I32),
+            "zkl_hyrax_prove_eval": ([P, zkl_vec, U64, U64, P, zkl_vec, P], I32),
             "zkl_matmul_prove": ([P, P, P, U64, U64, U64, P, P, P, zkl_vec, zkl_vec, P, P, P], I32),
             "zkl_ctx_wait": ([P], I32),
             "zkl_ctx_profile_read": ([P, ctypes.c_char_p, I32, ctypes.POINTER(ctypes.c_float),
@@ -111,6 +128,8 @@ EXPORTED = ["zkl_strerror", "zkl_ctx_create", "zkl_nccl_unique_id", "zkl_ctx_cre
             "zkl_last_error", "zkl_workspace_bytes", "zkl_ctx_set_workspace", "zkl_ctx_launch_count",
             "zkl_ctx_set_profiling", "zkl_ctx_profile_read", "zkl_ctx_set_async", "zkl_ctx_wait",
             "zkl_matmul_workspace_bytes", "zkl_matmul_prove",
+            "zkl_hyrax_pp_bytes", "zkl_hyrax_setup", "zkl_hyrax_export_generators", "zkl_hyrax_workspace_bytes",
+            "zkl_hyrax_commit", "zkl_hyrax_prove_eval",
             "zkl_vec_import", "zkl_vec_import_i64", "zkl_vec_import_pair", "zkl_vec_export", "zkl_table_bytes",
             "zkl_table_create", "zkl_table_destroy", "zkl_tlookup_prepare", "zkl_tlookup_prepare_pair",
             "zkl_tlookup_prove", "zkl_tlookup_prove_fs",
@@ -477,6 +496,48 @@ class Context:
         return {"claim": fr_to_int(claim), "evals": [[fr_to_int(ev[3 * k + t]) for t in range(3)] for k in range(L)],
                 "finals": [fr_to_int(fin[0]), fr_to_int(fin[1])], "a": a if want_ab else None,
                 "b": b if want_ab else None}
+
+    # -- f3: Hyrax / Pedersen commitments
+    def hyrax_setup(self, cols: int):
+        """Public parameters for rows of `cols` entries: G_0..G_{cols-1}, H and their window tables (device)."""
+        nb = int(lib().zkl_hyrax_pp_bytes(cols))
+        if nb == 0:
+            raise ZklError(2, -1, f"bad cols {cols}")
+        pp = self.torch.empty(nb + 256, dtype=self.torch.uint8, device=self.device)
+        pad = (-pp.data_ptr()) % 256
+        self._check(lib().zkl_hyrax_setup(self.h, cols, ctypes.c_void_p(pp.data_ptr() + pad), nb))
+        return {"cols": cols, "mem": pp, "ptr": pp.data_ptr() + pad}
+
+    def hyrax_generators(self, pp):
+        out = (zkl_g1 * (pp["cols"] + 1))()
+        self._check(lib().zkl_hyrax_export_generators(self.h, ctypes.c_void_p(pp["ptr"]), pp["cols"], out))
+        pts = [g1_to_py(out[i]) for i in range(pp["cols"] + 1)]
+        return pts[:-1], pts[-1]
+
+    def hyrax_commit(self, pp, S: Vec, D: int, rho: Optional[Sequence[int]] = None):
+        cols = pp["cols"]
+        need = int(lib().zkl_hyrax_workspace_bytes(D, cols))
+        if need == 0:
+            raise ZklError(2, -1, f"bad shape D={D} cols={cols}")
+        self._ensure_ws(need)
+        rows = D // cols
+        rh = None
+        if rho is not None:
+            rh = (zkl_fr * rows)(*[fr_from_int(x % R_MODULUS) for x in rho])
+        out = (zkl_g1 * rows)()
+        self._check(lib().zkl_hyrax_commit(self.h, ctypes.c_void_p(pp["ptr"]), cols, S.c, D, rh, out))
+        return [g1_to_py(out[j]) for j in range(rows)]
+
+    def hyrax_prove_eval(self, S: Vec, D: int, cols: int, v: Sequence[int]):
+        need = int(lib().zkl_hyrax_workspace_bytes(D, cols))
+        if need == 0:
+            raise ZklError(2, -1, f"bad shape D={D} cols={cols}")
+        self._ensure_ws(need)
+        V = (zkl_fr * max(len(v), 1))(*[fr_from_int(x % R_MODULUS) for x in v])
+        w = self.vec(cols)
+        y = zkl_fr()
+        self._check(lib().zkl_hyrax_prove_eval(self.h, S.c, D, cols, V, w.c, ctypes.byref(y)))
+        return w, fr_to_int(y)
 
 
 class Table:
