@@ -1127,7 +1127,7 @@ int run_matmul(zkl_ctx* ctx, const int32_t* A, const int32_t* B, uint64_t m, uin
 // ------------------------------------------------------------------ Hyrax commitments
 struct HxPlan {
     uint64_t D, cols, rows, nslices;
-    size_t o_sc, o_part, o_rho, o_out, o_v, o_er, o_ec, o_ypart, o_y, total;
+    size_t o_sc, o_part, o_q, o_rho, o_out, o_v, o_er, o_ec, o_ypart, o_y, total;
 };
 
 void make_hx_plan(HxPlan& h, uint64_t D, uint64_t cols) {
@@ -1137,7 +1137,8 @@ void make_hx_plan(HxPlan& h, uint64_t D, uint64_t cols) {
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o += align_up(bytes); return r; };
     h.o_sc = take(soa_bytes(D));
-    h.o_part = take(sizeof(g1j) * h.rows * h.nslices);
+    h.o_part = take(sizeof(g1j) * h.rows * h.nslices * kHxGroups);
+    h.o_q = take(sizeof(g1j) * h.rows * kHxGroups);
     h.o_rho = take(sizeof(zkl_fr) * h.rows);
     h.o_out = take(sizeof(zkl_g1) * h.rows);
     h.o_v = take(sizeof(fr) * 64);
@@ -1186,12 +1187,14 @@ int run_hyrax_commit(zkl_ctx* ctx, const void* pp, uint64_t cols, zkl_vec S, uin
         CUDA_TRY(ctx, cudaMemcpyAsync(drho, rho, sizeof(zkl_fr) * h.rows, cudaMemcpyHostToDevice, s));
     }
     LAUNCH(ctx, k_hx_canon, grid_for(D, 256), 256, 0, s, S.limbs, D, Sc);
-    const uint64_t nthreads = h.rows * h.nslices;
+    const uint64_t nthreads = h.rows * h.nslices * kHxGroups;
     LAUNCH(ctx, k_hx_commit_partial, (unsigned)((nthreads + kHxThreads - 1) / kHxThreads), kHxThreads, 0, s, Sc, D,
            cols, tab, h.nslices, part);
+    g1j* Q = at<g1j>(ctx, h.o_q);
+    LAUNCH(ctx, k_hx_reduce_slices, (unsigned)(h.rows * kHxGroups), kHxRedThreads, 0, s, part, h.nslices, Q);
     zkl_g1* dout = at<zkl_g1>(ctx, h.o_out);
-    LAUNCH(ctx, k_hx_commit_rows, (unsigned)((h.rows + 63) / 64), 64, 0, s, part, h.nslices, h.rows, drho,
-           tab + cols * kHxTab, dout);
+    LAUNCH(ctx, k_hx_commit_rows, (unsigned)((h.rows + 63) / 64), 64, 0, s, Q, h.rows, drho, tab + cols * kHxTab,
+           dout);
     CUDA_TRY(ctx, cudaMemcpyAsync(C_host, dout, sizeof(zkl_g1) * h.rows, cudaMemcpyDeviceToHost, s));
     return sync_stream(ctx);
 }

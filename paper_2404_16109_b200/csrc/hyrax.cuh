@@ -3,9 +3,10 @@
 // C_j = sum_i S[j cols + i] G_i + rho_j H, with G_0..G_{cols-1}, H hashed to BLS12-381 G1 by try-and-increment
 // (SHA-256, cofactor cleared): no trusted setup.  Commit = a batch of `rows` MSMs sharing their bases, computed by
 // windowed Straus with 4-bit windows over precomputed affine tables {d G_i : d = 0..15} (L2-resident for
-// cols <= 2^13): one thread per (row, slice of columns) keeps one Jacobian accumulator, multiplies it by 16 per
-// window and adds T_i[digit] for every column of its slice (64 mixed additions per scalar, no buckets, no sort,
-// no atomics); the per-slice partial sums are added per row and normalised once.  Included by api.cu.
+// cols <= 2^13): one thread per (row, slice of 16 columns, 32-bit scalar chunk) keeps one Jacobian accumulator,
+// multiplies it by 16 per window and adds T_i[digit] for every column of its slice (64 mixed additions per scalar
+// in all, no buckets, no sort, no atomics); the partial sums are tree-reduced per (row, chunk), the chunks combined
+// by Horner (2^32 steps) and each row normalised once.  Included by api.cu.
 #pragma once
 #include "g1.cuh"
 #include "kernels.cuh"
@@ -14,7 +15,8 @@
 namespace zkl {
 
 constexpr int kHxThreads = 128;
-constexpr int kHxSlice = 64;     // columns per thread in the commit kernel
+constexpr int kHxSlice = 16;     // columns per thread in the commit kernel
+constexpr int kHxGroups = 8;     // 32-bit scalar chunks (8 windows each) handled by separate threads
 constexpr int kHxTab = 16;       // table entries per base (4-bit windows)
 
 // try-and-increment hash to G1 for index i of the tag (oracle/hyrax.py hash_to_curve)
@@ -99,42 +101,73 @@ __global__ void k_hx_canon(const uint32_t* __restrict__ S, uint64_t n, uint32_t*
         st_fr(out, n, i, fr_from_mont(ld_fr(S, n, i)));
 }
 
-// partial[j][s] = sum_{i in slice s} S[j cols + i] G_i  (windowed Straus, 4-bit windows, MSB window first)
+// Work split: s = sum_g c_g 2^{32 g} (the 8 limbs of the canonical scalar), so
+//   sum_i s_i G_i = sum_g 2^{32 g} Q_g,  Q_g = sum_i c_{i,g} G_i.
+// k_hx_commit_partial: one thread per (row j, slice of kHxSlice columns, chunk g): windowed Straus over the 8
+// 4-bit windows of c_g (MSB window first) -> partial[j][s][g].  Short dependent chains, D / 2 threads.
 __global__ void __launch_bounds__(kHxThreads)
 k_hx_commit_partial(const uint32_t* __restrict__ Sc, uint64_t D, uint64_t cols, const g1a* __restrict__ tab,
                     uint64_t nslices, g1j* partial) {
     const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t rows = D / cols;
-    if (t >= rows * nslices) return;
-    const uint64_t j = t / nslices, s = t % nslices;
+    if (t >= rows * nslices * kHxGroups) return;
+    const int g = (int)(t % kHxGroups);
+    const uint64_t js = t / kHxGroups;
+    const uint64_t j = js / nslices, s = js % nslices;
     const uint64_t i0 = s * kHxSlice;
     const int len = (int)min((uint64_t)kHxSlice, cols - i0);
-    const uint64_t base = j * cols + i0;
+    const uint32_t* plane = Sc + (uint64_t)g * D + j * cols + i0;
+    uint32_t c[kHxSlice];
+#pragma unroll
+    for (int k = 0; k < kHxSlice; ++k) c[k] = k < len ? __ldg(plane + k) : 0u;
     g1j acc = g1_infinity();
-    for (int w = 63; w >= 0; --w) {
+#pragma unroll 1
+    for (int w = 7; w >= 0; --w) {
         if (!g1_is_inf(acc)) {
             acc = g1_dbl(acc);
             acc = g1_dbl(acc);
             acc = g1_dbl(acc);
             acc = g1_dbl(acc);
         }
-        const uint32_t* plane = Sc + (uint64_t)(w >> 3) * D + base;
-        const int sh = (w & 7) * 4;
-        for (int c = 0; c < len; ++c) {
-            const uint32_t d = (__ldg(plane + c) >> sh) & 15u;
-            if (d) acc = g1_add_affine(acc, tab[(i0 + c) * kHxTab + d]);
+#pragma unroll 1
+        for (int k = 0; k < len; ++k) {
+            const uint32_t d = (c[k] >> (4 * w)) & 15u;
+            if (d) acc = g1_add_affine(acc, tab[(i0 + k) * kHxTab + d]);
         }
     }
     partial[t] = acc;
 }
 
-// C_j = sum_s partial[j][s] + rho_j H, affine, canonical coordinates
-__global__ void k_hx_commit_rows(const g1j* __restrict__ partial, uint64_t nslices, uint64_t rows,
-                                 const uint32_t* __restrict__ rho_canon, const g1a* __restrict__ htab, zkl_g1* out) {
+// Q[j][g] = sum_s partial[j][s][g]: one CTA per (row, chunk), a strided sum per thread then a tree in shared memory
+constexpr int kHxRedThreads = 64;
+__global__ void __launch_bounds__(kHxRedThreads)
+k_hx_reduce_slices(const g1j* __restrict__ partial, uint64_t nslices, g1j* Qout) {
+    __shared__ g1j sm[kHxRedThreads];
+    const uint64_t jg = blockIdx.x;   // j * kHxGroups + g
+    const uint64_t j = jg / kHxGroups;
+    const int g = (int)(jg % kHxGroups);
+    g1j acc = g1_infinity();
+    for (uint64_t s = threadIdx.x; s < nslices; s += blockDim.x)
+        acc = g1_add(acc, partial[(j * nslices + s) * kHxGroups + g]);
+    sm[threadIdx.x] = acc;
+    __syncthreads();
+    for (int off = kHxRedThreads / 2; off > 0; off >>= 1) {
+        if ((int)threadIdx.x < off) sm[threadIdx.x] = g1_add(sm[threadIdx.x], sm[threadIdx.x + off]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) Qout[jg] = sm[0];
+}
+
+// C_j = sum_g 2^{32 g} Q[j][g] (Horner, 32 doublings per chunk) + rho_j H, affine, canonical coordinates
+__global__ void k_hx_commit_rows(const g1j* __restrict__ Q, uint64_t rows, const uint32_t* __restrict__ rho_canon,
+                                 const g1a* __restrict__ htab, zkl_g1* out) {
     const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (j >= rows) return;
-    g1j acc = g1_infinity();
-    for (uint64_t s = 0; s < nslices; ++s) acc = g1_add(acc, partial[j * nslices + s]);
+    g1j acc = Q[j * kHxGroups + kHxGroups - 1];
+    for (int g = kHxGroups - 2; g >= 0; --g) {
+        for (int k = 0; k < 32; ++k) acc = g1_dbl(acc);
+        acc = g1_add(acc, Q[j * kHxGroups + g]);
+    }
     if (rho_canon) {
         g1j h = g1_infinity();
         for (int w = 63; w >= 0; --w) {
