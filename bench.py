@@ -241,6 +241,7 @@ def main():
         # a1 (T) + a2, then a1 (S) fused with a3 (zkl_tlookup_prepare_pair), then a4-a9
         ctx.import_pair(txs, tys, ch.alpha_f, T)
         tab = ctx.table(T, tmem)
+        ctx.table_attach_pair(tab, txs, tys, ch.alpha_f)   # pair-range fast path of prepare_pair
         ctx.prepare_pair(xs, ys, ch.alpha_f, D, tab, S, m)
         return ctx.prove(S, D, tab, m, chal, args.variant)
 
@@ -288,6 +289,7 @@ def main():
         def step_fs():
             ctx.import_pair(txd, tyd, ch.alpha_f, T)
             tab = ctx.table(T, tmem)
+            ctx.table_attach_pair(tab, txd, tyd, ch.alpha_f)   # pair-range fast path of prepare_pair
             ctx.prepare_pair(xd, yd, ch.alpha_f, D, tab, S, m)
             return ctx.prove_fs(S, D, tab, m, seed, args.variant)
 

@@ -188,6 +188,13 @@ size_t zkl_table_bytes(uint64_t N);
  * E_SHAPE, E_DUP_TABLE(smallest later duplicate), E_OOM. */
 int zkl_table_create(zkl_ctx* ctx, zkl_vec T, void* mem, size_t mem_bytes, zkl_table** out, int64_t* err_index);
 void zkl_table_destroy(zkl_table* table);
+/* Function-lookup fast path (a3): declare that T_j = tx_j + alpha_f ty_j with tx the contiguous range
+ * tx_0 + j (int32 device arrays of N entries; checked on the device, ty copied into the table memory).  Then
+ * zkl_tlookup_prepare_pair with the same alpha_f indexes (x, y) as j = x - tx_0 (checked: ty_j == y) instead of
+ * hashing; any pair failing the check sends the prepare through the exact hash index.  E_ARG if T is not of that
+ * form (the table stays usable without the fast path). */
+int zkl_table_attach_pair(zkl_ctx* ctx, zkl_table* table, const int32_t* tx_dev, const int32_t* ty_dev,
+                          const zkl_fr* alpha_f);
 
 /* ---------------------------------------------------------------- the hot path */
 /* tlookup-Prep (Eq. hab22-coefs): m_dev[j] = #{i : S_i = T_j}

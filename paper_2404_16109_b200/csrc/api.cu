@@ -1598,7 +1598,7 @@ int zkl_vec_export(zkl_ctx* ctx, zkl_vec src, void* canon, int dst_on_device) {
 size_t zkl_table_bytes(uint64_t N) {
     if (!is_pow2(N)) return 0;
     uint64_t slots = std::max<uint64_t>(64, 4 * N);   // load factor <= 1/4
-    return soa_bytes(N) + align_up(32 * N) + align_up(4 * slots) + align_up(32 * slots);
+    return soa_bytes(N) + align_up(32 * N) + align_up(4 * slots) + align_up(32 * slots) + align_up(4 * N);
 }
 
 int zkl_table_create(zkl_ctx* ctx, zkl_vec T, void* mem, size_t mem_bytes, zkl_table** out, int64_t* err_index) {
@@ -1620,6 +1620,8 @@ int zkl_table_create(zkl_ctx* ctx, zkl_vec T, void* mem, size_t mem_bytes, zkl_t
     t->Taos = (uint4*)((uint8_t*)mem + soa_bytes(N));
     t->slots = (uint32_t*)((uint8_t*)mem + soa_bytes(N) + align_up(32 * N));
     t->Skeys = (uint4*)((uint8_t*)mem + soa_bytes(N) + align_up(32 * N) + align_up(4 * nslots));
+    t->ty = (int32_t*)((uint8_t*)mem + soa_bytes(N) + align_up(32 * N) + align_up(4 * nslots) + align_up(32 * nslots));
+    t->has_pair = 0;
     t->nslots = nslots;
     t->slot_mask = (uint32_t)(nslots - 1);
     t->device = ctx->device;
@@ -1653,6 +1655,37 @@ int zkl_table_create(zkl_ctx* ctx, zkl_vec T, void* mem, size_t mem_bytes, zkl_t
 
 void zkl_table_destroy(zkl_table* t) { free(t); }
 
+int zkl_table_attach_pair(zkl_ctx* ctx, zkl_table* t, const int32_t* tx, const int32_t* ty, const zkl_fr* alpha_f) {
+    int st;
+    if ((st = check_ctx(ctx))) return st;
+    if (!t || !tx || !ty || !alpha_f) return set_err(ctx, ZKL_E_ARG, "null argument");
+    if (fr_ge_r_host(*alpha_f)) return set_err(ctx, ZKL_E_NONCANONICAL, "alpha_f is not canonical");
+    t->has_pair = 0;
+    const uint64_t N = t->N;
+    fr* af = reinterpret_cast<fr*>(ctx->dscratch + 64);
+    unsigned long long* bad = reinterpret_cast<unsigned long long*>(ctx->dscratch + 8);
+    zkl_fr* staged = reinterpret_cast<zkl_fr*>((uint8_t*)ctx->host_out + 62000);
+    *staged = *alpha_f;
+    CUDA_TRY(ctx, cudaMemcpyAsync(af, staged, sizeof(fr), cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(ctx, cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), ctx->stream));
+    LAUNCH(ctx, k_import_canon, 1, 32, 0, ctx->stream, (const uint32_t*)af, 1, (uint32_t*)af,
+           (unsigned long long*)nullptr);
+    LAUNCH(ctx, k_pair_consts, 1, 32, 0, ctx->stream, af, af + 1);
+    LAUNCH(ctx, k_table_check_pair, grid_for(N, 256), 256, 0, ctx->stream, tx, ty, N, af + 1, t->T, t->ty, bad);
+    unsigned long long* hb = reinterpret_cast<unsigned long long*>((uint8_t*)ctx->host_out + 60000);
+    int32_t* hx0 = reinterpret_cast<int32_t*>((uint8_t*)ctx->host_out + 60016);
+    CUDA_TRY(ctx, cudaMemcpyAsync(hb, bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpyAsync(hx0, tx, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    if ((st = sync_stream(ctx))) return st;
+    if (*hb != ~0ull)
+        return set_err(ctx, ZKL_E_ARG, "not a pair-range table at entry %llu (tx not x0 + j, or T_j != tx_j + alpha ty_j)",
+                       *hb);
+    t->x0 = *hx0;
+    t->alpha = *alpha_f;
+    t->has_pair = 1;
+    return ZKL_OK;
+}
+
 // ---------------------------------------------------------------- a3
 // Shared body of the two prepare entry points.  pair != nullptr: x, y (int32) are imported into S first,
 // fused with the index map.
@@ -1662,10 +1695,23 @@ struct PairIn {
     const zkl_fr* alpha_f;
 };
 
-static int prepare_collect(zkl_ctx* ctx, zkl_vec S, const zkl_table* T, int64_t* err_index, uint64_t Dp);
+struct PrepArgs {
+    zkl_vec S;
+    uint64_t D;
+    const zkl_table* T;
+    uint32_t* m_dev;
+    int64_t* err_index;
+    bool has_pair;
+    PairIn pair;
+    zkl_fr alpha;   // owned copy (PairIn.alpha_f may point to caller memory that is gone at completion)
+};
+
+static int prepare_collect(zkl_ctx* ctx, const PrepArgs& a, uint64_t Dp, bool range_path);
+static int prepare_impl(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T, uint32_t* m_dev, int64_t* err_index,
+                        const PairIn* pair, bool force_hash = false);
 
 static int prepare_impl(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T, uint32_t* m_dev, int64_t* err_index,
-                        const PairIn* pair) {
+                        const PairIn* pair, bool force_hash) {
     int st;
     if (err_index) *err_index = -1;
     if ((st = check_ctx(ctx))) return st;
@@ -1681,9 +1727,10 @@ static int prepare_impl(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T,
     if ((st = check_vec(ctx, S, p.Dp, "S_local"))) return st;
     unsigned long long* err = at<unsigned long long>(ctx, p.o_err);
     uint32_t* rows = at<uint32_t>(ctx, p.o_hist);
-    CUDA_TRY(ctx, cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), ctx->stream));
+    CUDA_TRY(ctx, cudaMemsetAsync(err, 0xff, 2 * sizeof(unsigned long long), ctx->stream));   // [0] NOT_IN, [1] range miss
     TableView tv{T->T, T->Taos, T->slots, T->Skeys, T->N, T->slot_mask};
     uint32_t* keys = at<uint32_t>(ctx, p.o_keys);
+    bool range_path = false;
     if (pair) {
         if (!pair->x || !pair->y || !pair->alpha_f) return set_err(ctx, ZKL_E_ARG, "null argument");
         fr* af = reinterpret_cast<fr*>(ctx->dscratch + 64);
@@ -1693,8 +1740,13 @@ static int prepare_impl(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T,
         LAUNCH(ctx, k_import_canon, 1, 32, 0, ctx->stream, (const uint32_t*)af, 1, (uint32_t*)af,
                (unsigned long long*)nullptr);
         LAUNCH(ctx, k_pair_consts, 1, 32, 0, ctx->stream, af, af + 1);
-        LAUNCH(ctx, k_import_pair_index, grid_for(p.Dp, 256, kSMs * 32), 256, 0, ctx->stream, pair->x, pair->y, p.Dp,
-               af + 1, S.limbs, (uint64_t)ctx->rank * p.Dp, tv, keys, err);
+        range_path = !force_hash && T->has_pair && memcmp(&T->alpha, pair->alpha_f, sizeof(zkl_fr)) == 0;
+        if (range_path)   // the table's x column is a range: index x - x0, checked against ty (no hash probe)
+            LAUNCH(ctx, k_import_pair_range, grid_for(p.Dp, 256, kSMs * 32), 256, 0, ctx->stream, pair->x, pair->y,
+                   p.Dp, af + 1, S.limbs, T->x0, T->ty, T->N, keys, err + 1);
+        else
+            LAUNCH(ctx, k_import_pair_index, grid_for(p.Dp, 256, kSMs * 32), 256, 0, ctx->stream, pair->x, pair->y,
+                   p.Dp, af + 1, S.limbs, (uint64_t)ctx->rank * p.Dp, tv, keys, err);
     } else {
         LAUNCH(ctx, k_index_map, grid_for(p.Dp, 256, kSMs * 32), 256, 0, ctx->stream, S.limbs, p.Dp,
                (uint64_t)ctx->rank * p.Dp, tv, keys, err);
@@ -1708,7 +1760,16 @@ static int prepare_impl(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T,
         if (rc) return rc;
     }
     unsigned long long* herr = reinterpret_cast<unsigned long long*>((uint8_t*)ctx->host_out + 60000);
-    CUDA_TRY(ctx, cudaMemcpyAsync(herr, err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpyAsync(herr, err, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+    PrepArgs pa;
+    memset(&pa, 0, sizeof(pa));
+    pa.S = S; pa.D = D; pa.T = T; pa.m_dev = m_dev; pa.err_index = err_index;
+    if (pair) {
+        pa.has_pair = true;
+        pa.pair = *pair;
+        pa.alpha = *pair->alpha_f;
+        pa.pair.alpha_f = nullptr;
+    }
     if (ctx->async_mode) {
         // the keys are valid for a proof enqueued after this (the completion below clears them on error)
         ctx->prep_S = S.limbs;
@@ -1716,22 +1777,38 @@ static int prepare_impl(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T,
         ctx->prep_table = T;
         ctx->pend_prepare = 1;
         const uint64_t Dp = p.Dp;
-        pending_of(ctx).push_back([ctx, S, T, err_index, Dp]() {
+        pending_of(ctx).push_back([ctx, pa, Dp, range_path]() {
             ctx->pend_prepare = 0;
-            return prepare_collect(ctx, S, T, err_index, Dp);
+            return prepare_collect(ctx, pa, Dp, range_path);
         });
         return ZKL_OK;
     }
     if ((st = sync_stream(ctx))) return st;
-    return prepare_collect(ctx, S, T, err_index, p.Dp);
+    return prepare_collect(ctx, pa, p.Dp, range_path);
 }
 
-static int prepare_collect(zkl_ctx* ctx, zkl_vec S, const zkl_table* T, int64_t* err_index, uint64_t Dp) {
-    unsigned long long e = *reinterpret_cast<const unsigned long long*>((const uint8_t*)ctx->host_out + 60000);
+static int prepare_collect(zkl_ctx* ctx, const PrepArgs& a, uint64_t Dp, bool range_path) {
+    const unsigned long long* he = reinterpret_cast<const unsigned long long*>((const uint8_t*)ctx->host_out + 60000);
+    unsigned long long e = he[0], miss = he[1];
     if (ctx->nranks > 1) {
         int rc = zkl_dist_min_u64(ctx, &e);
         if (rc) return rc;
+        if (range_path && (rc = zkl_dist_min_u64(ctx, &miss))) return rc;
     }
+    if (range_path && miss != ~0ull) {
+        // some (x, y) is not (x0 + j, ty_j): redo with the exact hash index (NOT_IN_TABLE, or an entry that a
+        // special alpha made equal), synchronously
+        PairIn pin = a.pair;
+        pin.alpha_f = &a.alpha;
+        const int was_async = ctx->async_mode;
+        ctx->async_mode = 0;
+        const int st = prepare_impl(ctx, a.S, a.D, a.T, a.m_dev, a.err_index, &pin, true);
+        ctx->async_mode = was_async;
+        return st;
+    }
+    zkl_vec S = a.S;
+    const zkl_table* T = a.T;
+    int64_t* err_index = a.err_index;
     if (e != ~0ull) {
         if (err_index) *err_index = (int64_t)e;
         ctx->prep_S = nullptr;

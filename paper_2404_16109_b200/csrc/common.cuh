@@ -209,4 +209,10 @@ struct zkl_table {
     uint32_t slot_mask;
     uint64_t nslots;
     int device;
+    // function-lookup tables T_j = tx_j + alpha ty_j whose tx column is the contiguous range x0, x0+1, ...
+    // (zkl_table_attach_pair): the index of a pair (x, y) is x - x0, checked by ty[x - x0] == y
+    int has_pair;
+    int32_t x0;
+    int32_t* ty;        // device copy, N entries (in the table memory)
+    zkl_fr alpha;       // canonical alpha_f of the attached pair form
 };

@@ -206,6 +206,67 @@ k_index_map(const uint32_t* __restrict__ S, uint64_t n, uint64_t global_offset, 
     }
 }
 
+// Range fast path of the fused function-lookup prepare: for a table attached as a pair range (T_j = tx_j +
+// alpha ty_j, tx_j = x0 + j), the index of (x, y) is j = x - x0, valid iff 0 <= j < N and ty[j] == y (then
+// S = T_j exactly; T is duplicate-free).  No hash probe: a 4-byte gather from the L2-resident ty column.  A pair
+// that fails this test may still equal another entry for a special alpha, so a miss only raises `miss`, and the
+// caller redoes the prepare with the exact hash index.
+__global__ void __launch_bounds__(256, 4)
+k_import_pair_range(const int32_t* __restrict__ x, const int32_t* __restrict__ y, uint64_t n,
+                    const fr* __restrict__ consts, uint32_t* __restrict__ dst, int32_t x0,
+                    const int32_t* __restrict__ ty, uint64_t N, uint32_t* __restrict__ keys,
+                    unsigned long long* miss) {
+    __shared__ fr c[4];
+    if (threadIdx.x < 4) c[threadIdx.x] = consts[threadIdx.x];
+    __syncthreads();
+    bool missed = false;
+    if ((n & 3) == 0) {
+        for (uint64_t i = 4 * (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x); i < n;
+             i += 4 * (uint64_t)gridDim.x * blockDim.x) {
+            const int4 xv = __ldg(reinterpret_cast<const int4*>(x + i));
+            const int4 yv = __ldg(reinterpret_cast<const int4*>(y + i));
+            const int xs[4] = {xv.x, xv.y, xv.z, xv.w}, ys[4] = {yv.x, yv.y, yv.z, yv.w};
+            uint32_t kk[4];
+            fr s[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int64_t j = (int64_t)xs[q] - (int64_t)x0;
+                const bool ok = j >= 0 && (uint64_t)j < N && __ldg(ty + j) == ys[q];
+                missed |= !ok;
+                kk[q] = ok ? (uint32_t)j : 0u;
+                s[q] = fr_from_small_pair(xs[q], ys[q], c);
+            }
+            st_fr4(dst, n, i, s);
+            *reinterpret_cast<uint4*>(keys + i) = make_uint4(kk[0], kk[1], kk[2], kk[3]);
+        }
+    } else {
+        for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+            const int64_t j = (int64_t)x[i] - (int64_t)x0;
+            const bool ok = j >= 0 && (uint64_t)j < N && __ldg(ty + j) == y[i];
+            missed |= !ok;
+            keys[i] = ok ? (uint32_t)j : 0u;
+            st_fr(dst, n, i, fr_from_small_pair(x[i], y[i], c));
+        }
+    }
+    if (__any_sync(0xffffffffu, missed) && (threadIdx.x & 31) == 0) atomicMin(miss, 0ull);
+}
+
+// zkl_table_attach_pair: tx is the range x0 + j and T_j = tx_j + alpha ty_j for every j; copy ty
+__global__ void k_table_check_pair(const int32_t* __restrict__ tx, const int32_t* __restrict__ ty, uint64_t N,
+                                   const fr* __restrict__ consts, const uint32_t* __restrict__ T, int32_t* ty_out,
+                                   unsigned long long* bad) {
+    __shared__ fr c[4];
+    if (threadIdx.x < 4) c[threadIdx.x] = consts[threadIdx.x];
+    __syncthreads();
+    const int64_t x0 = tx[0];
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < N; j += (uint64_t)gridDim.x * blockDim.x) {
+        const bool range = (int64_t)tx[j] == x0 + (int64_t)j;
+        const bool same = fr_eq(fr_from_small_pair(tx[j], ty[j], c), ld_fr(T, N, j));
+        if (!range || !same) atomicMin(bad, (unsigned long long)j);
+        ty_out[j] = ty[j];
+    }
+}
+
 // a1 + a3(1) fused for function lookups: S = x + alpha_f y straight into Montgomery form,
 // stored, and its table index computed while it is still in registers.
 __global__ void __launch_bounds__(256, 4)

@@ -88,6 +88,7 @@ def lib() -> ctypes.CDLL:
             "zkl_ctx_set_async": ([P, I32], I32),
             "zkl_matmul_workspace_bytes": ([U64, U64, U64], ctypes.c_size_t),
             "zkl_hyrax_pp_bytes": ([U64], ctypes.c_size_t),
+            "zkl_table_attach_pair": ([P, P, P, P, ctypes.POINTER(zkl_fr)], I32),
             "zkl_hyrax_setup": ([P, U64, P, ctypes.c_size_t], I32),
             "zkl_hyrax_export_generators": ([P, P, U64, P], I32),
             "zkl_hyrax_workspace_bytes": ([U64, U64], ctypes.c_size_t),
@@ -128,7 +129,7 @@ EXPORTED = ["zkl_strerror", "zkl_ctx_create", "zkl_nccl_unique_id", "zkl_ctx_cre
             "zkl_last_error", "zkl_workspace_bytes", "zkl_ctx_set_workspace", "zkl_ctx_launch_count",
             "zkl_ctx_set_profiling", "zkl_ctx_profile_read", "zkl_ctx_set_async", "zkl_ctx_wait",
             "zkl_matmul_workspace_bytes", "zkl_matmul_prove",
-            "zkl_hyrax_pp_bytes", "zkl_hyrax_setup", "zkl_hyrax_export_generators", "zkl_hyrax_workspace_bytes",
+            "zkl_table_attach_pair", "zkl_hyrax_pp_bytes", "zkl_hyrax_setup", "zkl_hyrax_export_generators", "zkl_hyrax_workspace_bytes",
             "zkl_hyrax_commit", "zkl_hyrax_prove_eval",
             "zkl_vec_import", "zkl_vec_import_i64", "zkl_vec_import_pair", "zkl_vec_export", "zkl_table_bytes",
             "zkl_table_create", "zkl_table_destroy", "zkl_tlookup_prepare", "zkl_tlookup_prepare_pair",
@@ -373,6 +374,19 @@ class Context:
         self._check(st, err.value)
         tab = Table(h, T.n, mem, self)
         return tab
+
+    def table_attach_pair(self, tab: "Table", tx, ty, alpha_f: int) -> bool:
+        """Declare T_j = tx_j + alpha_f ty_j with tx a contiguous range (the function-lookup fast path of
+        prepare_pair).  Returns False (and the table keeps the hash index only) if T is not of that form."""
+        ttx = tx if hasattr(tx, "data_ptr") else self.torch.as_tensor(np.asarray(tx, np.int32)).to(self.device)
+        tty = ty if hasattr(ty, "data_ptr") else self.torch.as_tensor(np.asarray(ty, np.int32)).to(self.device)
+        af = fr_from_int(alpha_f % R_MODULUS)
+        st = lib().zkl_table_attach_pair(self.h, tab.h, ctypes.c_void_p(ttx.data_ptr()), ctypes.c_void_p(tty.data_ptr()),
+                                         ctypes.byref(af))
+        if st == 1:   # E_ARG: not a pair-range table
+            return False
+        self._check(st)
+        return True
 
     # -- a3
     def prepare(self, S: Vec, D: int, tab: "Table", m=None):

@@ -51,6 +51,7 @@ def main():
         for x, y, tx, ty, ch in insts:
             c.import_pair(tx, ty, base.chal.alpha_f, T)
             tab = c.table(T, tmem)
+            c.table_attach_pair(tab, tx, ty, base.chal.alpha_f)   # pair-range fast path of prepare_pair
             c.prepare_pair(x, y, base.chal.alpha_f, D, tab, S, m)
             c.prove(S, D, tab, m, ch)
 
@@ -62,6 +63,7 @@ def main():
                 with torch.cuda.stream(c.stream):
                     c.import_pair(tx, ty, base.chal.alpha_f, T)
                     tab = c.table(T, tmem)
+                    c.table_attach_pair(tab, tx, ty, base.chal.alpha_f)   # pair-range fast path of prepare_pair
                 c.set_async(True)
                 c.prepare_pair(x, y, base.chal.alpha_f, D, tab, S, m)
                 live.append((c, c.prove(S, D, tab, m, ch)))

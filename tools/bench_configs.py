@@ -40,6 +40,7 @@ def run_instances(ctx, wls, steps=5, warmup=2):
             if wl.kind == "pair":
                 ctx.import_pair(ins[2], ins[3], wl.chal.alpha_f, T)
                 tab = ctx.table(T, tmem)
+                ctx.table_attach_pair(tab, ins[2], ins[3], wl.chal.alpha_f)   # pair-range fast path of prepare_pair
                 ctx.prepare_pair(ins[0], ins[1], wl.chal.alpha_f, wl.D, tab, S, m)
             else:
                 ctx.import_ints(ins[1], T)

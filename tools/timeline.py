@@ -42,6 +42,7 @@ def step():
     if wl.kind == "pair":
         ctx.import_pair(txd, tyd, ch.alpha_f, T)
         tab = ctx.table(T, tmem)
+        ctx.table_attach_pair(tab, txd, tyd, ch.alpha_f)   # pair-range fast path of prepare_pair
         ctx.prepare_pair(xd, yd, ch.alpha_f, D, tab, S, m)
     else:
         ctx.import_ints(td, T)
