@@ -172,7 +172,10 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
             if ((1ull << gbits) > np) gbits = ilog2(np);
             choose_round(p, k, np, gbits, (int)std::max<uint64_t>(1, std::min<uint64_t>(np >> gbits, kMaxBlocks)));
         }
-        for (int k = 1; k <= p.dl; ++k) p.rd[k - 1].direct_h1 = 1;
+        // H(1) summed directly, except in the big rounds (>= 2^20 elements), whose k_round hides the one inversion
+        // per round that deriving H(1) from the running claim needs (k_fs_inv on the side stream)
+        for (int k = 1; k <= p.dl; ++k)
+            p.rd[k - 1].direct_h1 = (k == 1 || (p.Dp >> (k - 1)) < (1ull << 20) || !prove_mode) ? 1 : 0;
         p.k0 = p.dl + 1;
         p.fold_in = 0;
     } else if (p.small) {
@@ -874,27 +877,55 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
         h01 = 0;
     }
     if (p.n >= 1) LAUNCH(ctx, k_tab_eval, p.tnb[0], 256, 0, s, tcur, tlen, sc, variant, tpart);
-    LAUNCH(ctx, k_fs_round, 1, 256, 0, s, 1, p.d, p.n, variant, partials + p.rd[0].part_base, p.rd[0].nblocks, h01,
-           tpart, p.n >= 1 ? p.tnb[0] : 0u, tfin, sc, fst, out, dder);
+    {
+        // round 1 has one partial row per 4096-element tile: fold them to 32 rows with 32 CTAs first, so the
+        // single-CTA derivation below (on the critical path of every round) does not sum 16K rows
+        const fr* r1 = partials + p.rd[0].part_base;
+        uint32_t r1rows = p.rd[0].nblocks;
+        if (r1rows > 256) {
+            fr* folded = at<fr>(ctx, p.o_rank);   // kMaxRounds x kSlots fr >= 5 x 32
+            LAUNCH(ctx, k_rows_fold, 32, 256, 0, s, r1, r1rows, folded, 32u);
+            r1 = folded;
+            r1rows = 32;
+        }
+        LAUNCH(ctx, k_fs_round, 1, 256, 0, s, 1, p.d, p.n, variant, r1, r1rows, h01, tpart,
+               p.n >= 1 ? p.tnb[0] : 0u, tfin, sc, fst, out, dder, 0, err + 2);
+    }
     // ---- rounds 2..d
     const uint32_t *cA = Abuf, *cS = S.limbs;
     uint64_t len = p.Dp;
     for (int k = 2; k <= p.d; ++k) {
         const RoundDesc& r = p.rd[k - 1];
+        const bool derive = !force_inversion && !r.direct_h1;
         uint32_t* nA = at<uint32_t>(ctx, (k & 1) == 0 ? p.o_A1 : p.o_A2);
         uint32_t* nS = at<uint32_t>(ctx, (k & 1) == 0 ? p.o_S1 : p.o_S2);
-        LAUNCH(ctx, (k_round<true, true>), r.nblocks, kRoundThreads, 0, s, cA, cS, len, nA, nS, sc, k,
-               arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, partials + r.part_base);
+        // r_{k-1} is known: the table-side fold(k-1) + eval(k) and (derived rounds) the inversion of cl1 run on the
+        // side stream while the D-side fold + eval of round k runs on the main stream
+        const bool side = derive || k - 1 <= p.n;
+        if (side) {
+            CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, s));
+            CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+            if (derive) LAUNCH(ctx, k_fs_inv, 1, 32, 0, ctx->side, k, p.d, sc, fst);
+            if (k - 1 <= p.n) {   // fold the table with r_{k-1}
+                LAUNCH(ctx, k_tab_fold, grid_for(tlen / 2, 256, kMaxBlocks), 256, 0, ctx->side, tcur, tlen, tnxt, sc,
+                       k - 1, tfin);
+                fr* t = tcur; tcur = tnxt; tnxt = t;
+                tlen /= 2;
+            }
+            if (k <= p.n) LAUNCH(ctx, k_tab_eval, p.tnb[k - 1], 256, 0, ctx->side, tcur, tlen, sc, variant, tpart);
+            CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join, ctx->side));
+        }
+        if (derive)
+            LAUNCH(ctx, (k_round<true, false>), r.nblocks, kRoundThreads, 0, s, cA, cS, len, nA, nS, sc, k,
+                   arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, partials + r.part_base);
+        else
+            LAUNCH(ctx, (k_round<true, true>), r.nblocks, kRoundThreads, 0, s, cA, cS, len, nA, nS, sc, k,
+                   arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, partials + r.part_base);
         cA = nA; cS = nS;
         len /= 2;
-        if (k - 1 <= p.n) {   // fold the table with r_{k-1}
-            LAUNCH(ctx, k_tab_fold, grid_for(tlen / 2, 256, kMaxBlocks), 256, 0, s, tcur, tlen, tnxt, sc, k - 1, tfin);
-            fr* t = tcur; tcur = tnxt; tnxt = t;
-            tlen /= 2;
-        }
-        if (k <= p.n) LAUNCH(ctx, k_tab_eval, p.tnb[k - 1], 256, 0, s, tcur, tlen, sc, variant, tpart);
+        if (side) CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
         LAUNCH(ctx, k_fs_round, 1, 256, 0, s, k, p.d, p.n, variant, partials + r.part_base, r.nblocks, 0, tpart,
-               k <= p.n ? p.tnb[k - 1] : 0u, tfin, sc, fst, out, dder);
+               k <= p.n ? p.tnb[k - 1] : 0u, tfin, sc, fst, out, dder, derive ? 1 : 0, err + 2);
     }
     LAUNCH(ctx, k_fold_final, 1, 32, 0, s, cA, cS, len, sc, p.d, fin);
     if (p.n == p.d) LAUNCH(ctx, k_tab_fold, 1, 32, 0, s, tcur, tlen, tnxt, sc, p.d, tfin);

@@ -372,8 +372,6 @@ __device__ __forceinline__ fr fr_from_mont(const fr& a) {
     return fr_mul(a, one);
 }
 
-// a^(r-2) = a^{-1} (Fermat), left-to-right with a 4-bit fixed window (252 squarings +
-// at most 63 + 14 multiplications).  a = 0 gives 0.  Montgomery in, Montgomery out.
 // R^3 mod r: fr_mul(y, R^3) = y R^2 turns y = (aR)^{-1} into the Montgomery form a^{-1} R
 ZKL_FR_CONST(fr_r3, 0x439b73afu, 0xc62c1807u, 0x8cf06990u, 0x1b3e0d18u, 0xc7b5f418u, 0x73d13c71u, 0xc8db33e9u, 0x6e2a5bb9u)
 
@@ -487,7 +485,8 @@ static __device__ __noinline__ fr fr_inv(const fr a) {
     return fr_mul(y, fr_r3());
 }
 
-// Fermat form a^(r-2), kept as the cross-check of fr_inv in the microbenchmark.
+// Fermat form a^(r-2) (4-bit fixed window: 252 squarings + at most 77 multiplications; 0 -> 0), kept as the
+// cross-check of fr_inv in the microbenchmark.  Montgomery in, Montgomery out.
 static __device__ __noinline__ fr fr_inv_fermat(const fr a) {
     // r - 2, little-endian 32-bit limbs
     const uint32_t e[8] = {0xffffffffu, 0xfffffffeu, 0xfffe5bfeu, 0x53bda402u,

@@ -12,11 +12,31 @@
 
 namespace zkl {
 
+// Single-thread scalar code (the per-round derivation) executes each instruction once: with fr_mul inlined ~30
+// times the kernel is instruction-fetch bound, so the scalar section calls one shared out-of-line copy.
+static __device__ __noinline__ fr fs_mul(const fr a, const fr b) { return fr_mul(a, b); }
+static __device__ __noinline__ zkl_fr fs_canon(const fr a) {
+    fr one = fr_zero();   // the integer 1: mont(a, 1) = a / R, the canonical value
+    one.v[0] = 1;
+    const fr c = fs_mul(a, one);
+    zkl_fr z;
+    for (int l = 0; l < 8; ++l) z.w[l] = c.v[l];
+    return z;
+}
+
 struct FsState {
     uint8_t h[32];
     fr C;        // C_k = prod_{j<k} l_{d-j}(r_j)
     fr tscale;   // 2^{-(k-n)} once the table coordinates are bound
+    fr gprev[4]; // g_{k-1}(0..3), Montgomery: the running claim g_{k-1}(r_{k-1}) of a derived-H(1) round
+    fr inv_cl1;  // 1 / (alpha1 C_k u_{d-k}) for round k (k_fs_inv, side stream, during round k's fold + eval)
 };
+
+// 1 / (alpha1 C_k u_{d-k}) for round k: launched once r_{k-1} (hence C_k) is known, overlapping k_round(k)
+__global__ void k_fs_inv(int k, int d, const ProofScalars* __restrict__ sc, FsState* st) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    st->inv_cl1 = fr_inv(fr_mul(fr_mul(sc->alpha1, st->C), sc->u[d - k]));
+}
 
 // canonical 256-bit little-endian value of a digest, reduced mod r (x < 2^256 < 3r)
 __device__ inline fr fs_digest_to_fr(const uint8_t* dg) {
@@ -132,9 +152,30 @@ __global__ void k_fold_final(const uint32_t* __restrict__ A, const uint32_t* __r
 
 // Round k: reduce the D-side partial rows (and the table rows, k <= n), form g_k(0..3) directly, absorb it,
 // derive r_k.  h01_one: round 1 of the gather/inversion path, where H(0) = H(1) = sum eq = 1.
+// part [5][nrows] -> out [5][outrows]: CTA b sums rows [b per, (b+1) per) of every slot
+__global__ void k_rows_fold(const fr* __restrict__ part, uint32_t nrows, fr* out, uint32_t outrows) {
+    __shared__ fr scratch[5 * 8];
+    const uint32_t per = (nrows + outrows - 1) / outrows, r0 = blockIdx.x * per, r1 = min(r0 + per, nrows);
+    fr v[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        v[q] = fr_zero();
+        for (uint32_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) v[q] = fr_add(v[q], part[(uint64_t)q * nrows + r]);
+    }
+    block_sum_fr<5>(v, scratch);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < 5; ++q) out[(uint64_t)q * outrows + blockIdx.x] = v[q];
+    }
+}
+
+// derive_h1: the round's k_round did not sum H(1) (k_round<true, false>); it follows from the running claim,
+// H(1) = (g_{k-1}(r_{k-1}) - cl0 H(0) - a0 - a1 - tab(0) - tab(1)) / cl1.  cl1 = 0 with alpha1 C_k != 0 (u_{d-k} = 0,
+// probability ~2^-255) cannot be derived: the proof is flagged through `miss` and redone with H(1) summed.
 __global__ void k_fs_round(int k, int d, int n, int variant, const fr* __restrict__ part, uint32_t nrows,
                            int h01_one, const fr* __restrict__ tpart, uint32_t tnb, const fr* __restrict__ tfin,
-                           ProofScalars* sc, FsState* st, ProofOut* out, zkl_fr* derived) {
+                           ProofScalars* sc, FsState* st, ProofOut* out, zkl_fr* derived, int derive_h1,
+                           unsigned long long* miss) {
     __shared__ fr scratch[5 * 8];
     fr s[5];
     for (int q = 0; q < 5; ++q) {
@@ -153,33 +194,47 @@ __global__ void k_fs_round(int k, int d, int n, int variant, const fr* __restric
     if (k > n) {
         const fr tb = tfin[0], tt = tfin[1], tm = tfin[2], te = tfin[3];
         const fr tau = (variant == ZKL_VARIANT_PAPER)
-            ? fr_mul(tb, fr_sub(fr_mul(fr_mul(sc->alpha2, te), fr_add(tt, sc->beta)), tm))
-            : fr_sub(fr_mul(fr_mul(sc->alpha2, te), fr_sub(fr_mul(tb, fr_add(tt, sc->beta)), tm)), tb);
-        st->tscale = fr_mul(st->tscale, fr_inv2_m());
-        const fr c = fr_mul(tau, st->tscale);
+            ? fs_mul(tb, fr_sub(fs_mul(fs_mul(sc->alpha2, te), fr_add(tt, sc->beta)), tm))
+            : fr_sub(fs_mul(fs_mul(sc->alpha2, te), fr_sub(fs_mul(tb, fr_add(tt, sc->beta)), tm)), tb);
+        st->tscale = fs_mul(st->tscale, fr_inv2_m());
+        const fr c = fs_mul(tau, st->tscale);
         for (int q = 0; q < 4; ++q) tab[q] = c;
     }
     const fr u = sc->u[d - k];
-    const fr coef = fr_mul(sc->alpha1, st->C);
-    const fr cl0 = fr_mul(coef, fr_sub(one, u)), cl1 = fr_mul(coef, u);
-    const fr cl2 = fr_mul(coef, fr_sub(fr_mul(three, u), one)), cl3 = fr_mul(coef, fr_sub(fr_mul(fr_five_m(), u), two));
+    const fr coef = fs_mul(sc->alpha1, st->C);
+    const fr cl0 = fs_mul(coef, fr_sub(one, u)), cl1 = fs_mul(coef, u);
+    const fr cl2 = fs_mul(coef, fr_sub(fs_mul(three, u), one)), cl3 = fs_mul(coef, fr_sub(fs_mul(fr_five_m(), u), two));
     fr H0 = s[SLOT_H0], H1 = s[SLOT_H1];
     if (h01_one) { H0 = one; H1 = one; }
     const fr Hinf = s[SLOT_HINF], a0 = s[SLOT_A0], a1 = s[SLOT_A1], da = fr_sub(a1, a0);
+    if (derive_h1) {
+        // claim = g_{k-1}(x), x = r_{k-1}, by Lagrange on the nodes 0..3
+        const fr x = sc->r[k - 2];
+        const fr xm1 = fr_sub(x, one), xm2 = fr_sub(x, two), xm3 = fr_sub(x, three);
+        const fr xa = fs_mul(x, xm1), xb = fs_mul(xm2, xm3);
+        const fr L0 = fr_neg(fs_mul(fs_mul(xm1, xb), fr_inv6_m())), L1 = fs_mul(fs_mul(x, xb), fr_inv2_m());
+        const fr L2 = fr_neg(fs_mul(fs_mul(xa, xm3), fr_inv2_m())), L3 = fs_mul(fs_mul(xa, xm2), fr_inv6_m());
+        const fr claim = fr_add(fr_add(fs_mul(st->gprev[0], L0), fs_mul(st->gprev[1], L1)),
+                                fr_add(fs_mul(st->gprev[2], L2), fs_mul(st->gprev[3], L3)));
+        const fr rest = fr_sub(fr_sub(fr_sub(claim, fs_mul(cl0, H0)), fr_add(a0, a1)), fr_add(tab[0], tab[1]));
+        H1 = fs_mul(rest, st->inv_cl1);
+        if (fr_is_zero(cl1) && !fr_is_zero(coef)) atomicMin(miss, 0ull);
+    }
     const fr H2 = fr_add(fr_sub(fr_add(H1, H1), H0), fr_add(Hinf, Hinf));
-    const fr H3 = fr_add(fr_sub(fr_mul(three, H1), fr_add(H0, H0)), fr_mul(six, Hinf));
+    const fr H3 = fr_add(fr_sub(fs_mul(three, H1), fr_add(H0, H0)), fs_mul(six, Hinf));
     fr g[4];
-    g[0] = fr_add(fr_add(fr_mul(cl0, H0), a0), tab[0]);
-    g[1] = fr_add(fr_add(fr_mul(cl1, H1), a1), tab[1]);
-    g[2] = fr_add(fr_add(fr_mul(cl2, H2), fr_add(a0, fr_add(da, da))), tab[2]);
-    g[3] = fr_add(fr_add(fr_mul(cl3, H3), fr_add(a0, fr_mul(three, da))), tab[3]);
+    g[0] = fr_add(fr_add(fs_mul(cl0, H0), a0), tab[0]);
+    g[1] = fr_add(fr_add(fs_mul(cl1, H1), a1), tab[1]);
+    g[2] = fr_add(fr_add(fs_mul(cl2, H2), fr_add(a0, fr_add(da, da))), tab[2]);
+    g[3] = fr_add(fr_add(fs_mul(cl3, H3), fr_add(a0, fs_mul(three, da))), tab[3]);
     uint8_t msg[32 + 1 + 4 + 128];
     int p = 0;
     for (int i = 0; i < 32; ++i) msg[p++] = st->h[i];
     msg[p++] = 'g';
     for (int i = 0; i < 4; ++i) msg[p++] = (uint8_t)((uint32_t)k >> (8 * i));
     for (int t = 0; t < 4; ++t) {
-        const zkl_fr c = to_canon(g[t]);
+        st->gprev[t] = g[t];
+        const zkl_fr c = fs_canon(g[t]);
         out->evals[k - 1][t] = c;
         for (int l = 0; l < 8; ++l)
             for (int b = 0; b < 4; ++b) msg[p++] = (uint8_t)(c.w[l] >> (8 * b));
@@ -187,10 +242,10 @@ __global__ void k_fs_round(int k, int d, int n, int variant, const fr* __restric
     sha256(msg, p, st->h);
     const fr r = fs_challenge(st->h, "r", 1, (uint32_t)k);
     derived[3 + d + (k - 1)] = fs_canon_out(r);
-    const fr rm = fr_to_mont(r);
+    const fr rm = fs_mul(r, fr_r2());
     sc->r[k - 1] = rm;
     const fr l0 = fr_sub(one, u);
-    st->C = fr_mul(st->C, fr_add(l0, fr_mul(rm, fr_sub(u, l0))));
+    st->C = fs_mul(st->C, fr_add(l0, fs_mul(rm, fr_sub(u, l0))));
 }
 
 __global__ void k_fs_finish(const fr* __restrict__ fin, const fr* __restrict__ tfin, ProofOut* out) {

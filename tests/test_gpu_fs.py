@@ -25,9 +25,10 @@ def ctx():
     c.close()
 
 
-@pytest.mark.parametrize("d,n", [(1, 0), (3, 2), (10, 8), (13, 5), (14, 14), (16, 10)])
+@pytest.mark.parametrize("d,n", [(1, 0), (3, 2), (10, 8), (13, 5), (14, 14), (16, 10), (21, 10)])
 @pytest.mark.parametrize("variant", [TL.PAPER, TL.LOGUP])
 def test_fs_transcript(ctx, d, n, variant):
+    """d >= 21: rounds with >= 2^20 elements derive H(1) from the running claim (k_fs_inv on the side stream)."""
     from paper_2404_16109_b200 import zkl
     rng = random.Random(d * 131 + n + variant)
     D, N = 1 << d, 1 << n
