@@ -106,7 +106,7 @@ uint64_t zkl_ctx_launch_count(const zkl_ctx* ctx);
  * are recorded, then recording stops).  zkl_ctx_profile_read synchronizes, writes up to `cap` kernel names
  * (name_len bytes each, NUL-terminated), durations in ms, (if non-NULL) start times relative to the first
  * recorded launch and the stream of each launch (0 = the ctx stream, 1 = table-side stream, 2 = aux
- * stream), returns the count, and clears the record. */
+ * stream, 3 = the low-priority histogram stream of async mode), returns the count, and clears the record. */
 int zkl_ctx_set_profiling(zkl_ctx* ctx, int on);
 int zkl_ctx_profile_read(zkl_ctx* ctx, char* names, int name_len, float* ms, float* start_ms, int* stream_tag,
                          int cap);

@@ -92,6 +92,10 @@ int hist_rows_for(uint64_t Dp, uint64_t N) {
 }
 
 // ------------------------------------------------------------------ plan + workspace layout
+#ifndef ZKL_HIST_ASYNC_ROWS
+#define ZKL_HIST_ASYNC_ROWS 64
+#endif
+constexpr int kHistAsyncRows = ZKL_HIST_ASYNC_ROWS;   // histogram CTAs when it runs behind the proof (async mode)
 constexpr uint64_t kInvTop = 8192;   // the top level of the inversion hierarchy: one block
 
 // One hierarchical batched inversion over level-0 tiles [t0, t1) (a4).
@@ -435,6 +439,7 @@ int table_side(zkl_ctx* ctx, const Plan& p, cudaStream_t s, cudaStream_t s2, con
     const uint64_t N = p.N;
     fr* wk = at<fr>(ctx, p.o_twk);
     fr *cur = wk, *nxt = wk + 4 * N;
+    if (m_u32 && ctx->m_pending) CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_m, 0));   // async-mode histogram
     LAUNCH(ctx, k_tab_init, grid_for(N, 256), 256, 0, s, B, T, m_u32, Mf, N, sc, p.d, p.n, variant, cur, Bout);
     fr* tpart = at<fr>(ctx, p.o_tpart);
     uint64_t len = N;
@@ -578,8 +583,16 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
             LAUNCH(ctx, k_batch_invert, 1, bt, 4 * bt * sizeof(fr), sb, tX, N, (uint64_t)0, N, tB);
         }
         if (gather) LAUNCH(ctx, k_pack_tb, grid_for(N, 256), 256, 0, s, Tsrc, tB, N, at<uint4>(ctx, p.o_tBaos));
-        // B_out (if requested) is the variant's B, written by k_tab_init
-        if ((st = table_side(ctx, p, s, s2, tB, Tsrc, a.m_dev, nullptr, a.variant, sc, tsum, tfin, a.B_out.limbs)))
+        // B_out (if requested) is the variant's B, written by k_tab_init.  With the histogram still running on the
+        // low stream (async mode), the whole table side moves to the side stream, so that the D side does not wait
+        // for m
+        cudaStream_t ts = s;
+        if (ctx->m_pending) {
+            CUDA_TRY(ctx, cudaEventRecord(ctx->ev_b, s));
+            CUDA_TRY(ctx, cudaStreamWaitEvent(s2, ctx->ev_b, 0));
+            ts = s2;
+        }
+        if ((st = table_side(ctx, p, ts, s2, tB, Tsrc, a.m_dev, nullptr, a.variant, sc, tsum, tfin, a.B_out.limbs)))
             return st;
     } else {
         if ((st = table_side(ctx, p, s, s2, a.B_in.limbs, Tsrc, nullptr, a.m_fr_in.limbs, a.variant, sc, tsum, tfin,
@@ -838,6 +851,7 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
     }
     fr* wk = at<fr>(ctx, p.o_twk);
     fr *tcur = wk, *tnxt = wk + 4 * N;
+    if (ctx->m_pending) CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_m, 0));   // async-mode histogram
     LAUNCH(ctx, k_tab_init, grid_for(N, 256), 256, 0, s, tB, table->T, m_dev, (const uint32_t*)nullptr, N, sc, p.d,
            p.n, variant, tcur, B_out.limbs);
     uint64_t tlen = N;
@@ -1307,6 +1321,10 @@ static int ctx_create_common(int device, void* stream, zkl_ctx** out) {
         cudaDeviceGetStreamPriorityRange(&c->prio_lo, &c->prio_hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, c->prio_hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, c->prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&c->low, cudaStreamNonBlocking, c->prio_lo) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_keys, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_m, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fwd[0], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fwd[1], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_mid[0], cudaEventDisableTiming) != cudaSuccess ||
@@ -1460,6 +1478,10 @@ int zkl_ctx_set_async(zkl_ctx* ctx, int on) {
 
 int zkl_ctx_wait(zkl_ctx* ctx) {
     if (!ctx) return ZKL_E_ARG;
+    if (ctx->m_pending) {   // m (written on the low stream) is complete for the ctx stream from here on
+        cudaStreamWaitEvent(ctx->stream, ctx->ev_m, 0);
+        ctx->m_pending = 0;
+    }
     int st = sync_stream(ctx);
     std::vector<std::function<int()>> work;
     if (ctx->pending) work.swap(pending_of(ctx));
@@ -1484,6 +1506,10 @@ void zkl_ctx_destroy(zkl_ctx* c) {
     cudaStreamSynchronize(c->aux);
     cudaStreamDestroy(c->side);
     cudaStreamDestroy(c->aux);
+    cudaStreamDestroy(c->low);
+    cudaEventDestroy(c->ev_keys);
+    cudaEventDestroy(c->ev_m);
+    cudaEventDestroy(c->ev_b);
     for (int i = 0; i < 2; ++i) { cudaEventDestroy(c->ev_fwd[i]); cudaEventDestroy(c->ev_mid[i]); }
     cudaEventDestroy(c->ev_fork);
     cudaEventDestroy(c->ev_join);
@@ -1540,7 +1566,11 @@ int zkl_ctx_profile_read(zkl_ctx* c, char* names, int name_len, float* ms, float
         cudaEventElapsedTime(&t0, c->prof[0].a, c->prof[i].a);
         ms[n] = t;
         if (start_ms) start_ms[n] = t0;
-        if (stream_tag) stream_tag[n] = c->prof[i].stream == c->side ? 1 : (c->prof[i].stream == c->aux ? 2 : 0);
+        if (stream_tag)
+            stream_tag[n] = c->prof[i].stream == c->side ? 1
+                            : c->prof[i].stream == c->aux ? 2
+                            : c->prof[i].stream == c->low ? 3
+                                                          : 0;
         snprintf(names + (size_t)n * name_len, name_len, "%s", c->prof[i].name);
     }
     c->nprof = 0;
@@ -1784,8 +1814,23 @@ static int prepare_impl(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T,
     }
     // key bits: n (+1 for the sentinel of a partial tile when D_local < 4096)
     const int key_bits = std::max(1, p.n + (p.Dp < (uint64_t)kHistTile ? 1 : 0));
-    LAUNCH(ctx, k_hist_count, p.hist_rows, kHistThreads, 0, ctx->stream, keys, p.Dp, (uint32_t)T->N, rows, key_bits);
-    LAUNCH(ctx, k_hist_colsum, grid_for(T->N, 256), 256, 0, ctx->stream, rows, p.hist_rows, T->N, m_dev);
+    // async mode (single rank): the histogram runs on the low-priority stream, overlapping the proof that follows
+    // (which needs m only for the table side: it waits for ev_m there; zkl_ctx_wait orders the ctx stream after it)
+    const bool hist_low = ctx->async_mode && ctx->nranks == 1;
+    cudaStream_t hs = ctx->stream;
+    if (hist_low) {
+        CUDA_TRY(ctx, cudaEventRecord(ctx->ev_keys, ctx->stream));
+        CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->low, ctx->ev_keys, 0));
+        hs = ctx->low;
+    }
+    // in the background a few CTAs suffice (the proof's kernels keep the rest of the GPU)
+    const int hrows = hist_low ? std::min(p.hist_rows, kHistAsyncRows) : p.hist_rows;
+    LAUNCH(ctx, k_hist_count, hrows, kHistThreads, 0, hs, keys, p.Dp, (uint32_t)T->N, rows, key_bits);
+    LAUNCH(ctx, k_hist_colsum, grid_for(T->N, 256), 256, 0, hs, rows, hrows, T->N, m_dev);
+    if (hist_low) {
+        CUDA_TRY(ctx, cudaEventRecord(ctx->ev_m, ctx->low));
+        ctx->m_pending = 1;
+    }
     if (ctx->nranks > 1) {
         int rc = zkl_dist_allreduce_u32(ctx, m_dev, T->N);
         if (rc) return rc;

@@ -168,6 +168,10 @@ struct zkl_ctx {
     cudaStream_t stream;
     cudaStream_t side;             // table-side work overlapping the D side (high priority, one block)
     cudaStream_t aux;              // upper inversion levels (high priority, latency hidden behind the D side)
+    cudaStream_t low;              // async-mode histogram (lowest priority: fills the gaps of the proof's critical path)
+    cudaEvent_t ev_keys, ev_m;     // index keys written (main) / m written (low)
+    cudaEvent_t ev_b;              // B = 1/(beta + T) written (main), for a table side moved to the side stream
+    int m_pending;                 // ev_m recorded: the next consumer of m on the ctx stream must wait for it
     int prio_lo, prio_hi;
     cudaEvent_t ev_fork, ev_join;
     cudaEvent_t ev_fwd[2], ev_mid[2];

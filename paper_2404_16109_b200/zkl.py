@@ -282,7 +282,7 @@ class Context:
 
     def profile_read(self, with_start: bool = False):
         """[(kernel name, ms[, start ms, stream tag])] of the launches recorded since profiling was (re)enabled
-        or last read.  stream tag: 0 = ctx stream, 1 = table side, 2 = aux."""
+        or last read.  stream tag: 0 = ctx stream, 1 = table side, 2 = aux, 3 = async-mode histogram."""
         cap, nl = 256, 64
         names = ctypes.create_string_buffer(cap * nl)
         ms = (ctypes.c_float * cap)()

@@ -65,4 +65,4 @@ wall = time.perf_counter() - t0
 rec = ctx.profile_read(with_start=True)
 print(f"wall {wall*1e3:.2f} ms  launches {len(rec)}")
 for name, ms, st, tag in sorted(rec, key=lambda r: r[2]):
-    print(f"{st:9.3f} {ms:8.3f}  {'main side aux'.split()[tag]:4s} {name}")
+    print(f"{st:9.3f} {ms:8.3f}  {'main side aux low'.split()[tag]:4s} {name}")
