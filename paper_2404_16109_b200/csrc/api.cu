@@ -851,11 +851,22 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
     }
     fr* wk = at<fr>(ctx, p.o_twk);
     fr *tcur = wk, *tnxt = wk + 4 * N;
-    if (ctx->m_pending) CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_m, 0));   // async-mode histogram
-    LAUNCH(ctx, k_tab_init, grid_for(N, 256), 256, 0, s, tB, table->T, m_dev, (const uint32_t*)nullptr, N, sc, p.d,
+    // the table's round-1 work needs m: with the async histogram still running it goes to the side stream, so the
+    // D side (the gather) does not wait for m
+    cudaStream_t ts = s;
+    const bool tab_side = ctx->m_pending != 0;
+    if (tab_side) {
+        CUDA_TRY(ctx, cudaEventRecord(ctx->ev_b, s));
+        CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_b, 0));
+        CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_m, 0));
+        ts = ctx->side;
+    }
+    LAUNCH(ctx, k_tab_init, grid_for(N, 256), 256, 0, ts, tB, table->T, m_dev, (const uint32_t*)nullptr, N, sc, p.d,
            p.n, variant, tcur, B_out.limbs);
     uint64_t tlen = N;
-    if (p.n == 0) LAUNCH(ctx, k_tab_fin_copy, 1, 32, 0, s, tcur, tfin);   // the table is fully bound from the start
+    if (p.n == 0) LAUNCH(ctx, k_tab_fin_copy, 1, 32, 0, ts, tcur, tfin);   // the table is fully bound from the start
+    if (p.n >= 1) LAUNCH(ctx, k_tab_eval, p.tnb[0], 256, 0, ts, tcur, tlen, sc, variant, tpart);
+    if (tab_side) CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join, ts));
     // ---- round 1: A (gather through the prepared index, or inversion) + the round-1 sums
     uint32_t* Abuf = A_out.limbs ? A_out.limbs : at<uint32_t>(ctx, p.o_A);
     const bool gather = !p.small && !force_inversion;
@@ -890,7 +901,7 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
                arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, partials + r.part_base);
         h01 = 0;
     }
-    if (p.n >= 1) LAUNCH(ctx, k_tab_eval, p.tnb[0], 256, 0, s, tcur, tlen, sc, variant, tpart);
+    if (tab_side) CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
     {
         // round 1 has one partial row per 4096-element tile: fold them to 32 rows with 32 CTAs first, so the
         // single-CTA derivation below (on the critical path of every round) does not sum 16K rows

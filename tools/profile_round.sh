@@ -3,7 +3,7 @@
 #   plain runs first (each ncu pass only after its command exited 0 without ncu), then
 #   (1) per-kernel metrics over the launches of tools/timeline.py 26 (3 H steps: 2 warm-up + 1),
 #   (2) the bench line, (3) the launch list of the bench command itself (device time per launch),
-#   (4) one `--set full` capture of the top kernels.
+#   (4) with FULL=<kernel regex>, one `--set full` capture (3 launches) of those kernels.
 set -o pipefail
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 TAG=${1:-prof}
@@ -16,6 +16,8 @@ cat gpurun_out/${TAG}_bench.json
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches_bench.csv \
     python bench.py --steps 2 --warmup 3 > gpurun_out/${TAG}_ncu2.log 2>&1
 echo "launch list rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:"k_round|k_gather_keys|k_chunk_rounds|k_hist_count|k_import_pair_index" \
-    -s 10 -c 6 -o gpurun_out/${TAG}_full python tools/timeline.py 26 > gpurun_out/${TAG}_ncu3.log 2>&1
+if [ -n "$FULL" ]; then   # the --set full capture is large: run it in its own call (gpurun copies back <= 64 MiB)
+ncu --set full --clock-control none --import-source on -k regex:"$FULL" -c 3 \
+    -o gpurun_out/${TAG}_full python tools/timeline.py 26 > gpurun_out/${TAG}_ncu3.log 2>&1
 echo "full rc=$?"
+fi
