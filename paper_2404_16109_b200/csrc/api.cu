@@ -15,6 +15,8 @@
 #include <algorithm>
 #include <array>
 #include <functional>
+#include <initializer_list>
+#include <utility>
 #include <memory>
 #include <new>
 #include <vector>
@@ -379,6 +381,40 @@ int need_ws(zkl_ctx* ctx, const Plan& p) {
     return ZKL_OK;
 }
 
+// Small host->device transfers from the ctx's pinned staging page (challenges, plans, alpha_f) are done by one
+// kernel reading the mapped host memory (zero-copy over PCIe), not by cudaMemcpyAsync: a copy-engine transfer would
+// queue behind a large H2D copy the caller has in flight on another stream (e.g. the next step's inputs) and stall
+// the proof until it drains.
+struct CopySeg {
+    uint32_t* dst;
+    const uint32_t* src;
+    uint32_t words;
+};
+struct CopySegs {
+    CopySeg seg[4];
+    int n;
+};
+__global__ void k_copy_from_host(CopySegs c) {
+    for (int g = 0; g < c.n; ++g)
+        for (uint32_t i = threadIdx.x; i < c.seg[g].words; i += blockDim.x) c.seg[g].dst[i] = c.seg[g].src[i];
+}
+
+int h2d_small(zkl_ctx* ctx, cudaStream_t s, std::initializer_list<std::pair<void*, const void*>> dsts,
+              std::initializer_list<size_t> sizes) {
+    CopySegs c;
+    c.n = 0;
+    auto sz = sizes.begin();
+    for (const auto& d : dsts) {
+        c.seg[c.n].dst = reinterpret_cast<uint32_t*>(d.first);
+        c.seg[c.n].src = reinterpret_cast<const uint32_t*>(d.second);   // pinned (cudaMallocHost): UVA device-visible
+        c.seg[c.n].words = (uint32_t)(*sz / 4);
+        ++c.n;
+        ++sz;
+    }
+    LAUNCH(ctx, k_copy_from_host, 1, 256, 0, s, c);
+    return ZKL_OK;
+}
+
 int sync_stream(zkl_ctx* ctx) {
     cudaError_t e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) {
@@ -552,10 +588,9 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
     memcpy(hs->rounds, p.rd, sizeof(p.rd));
     memcpy(hs->jobs, p.jobs, sizeof(p.jobs));
     memcpy(hs->tnb, p.tnb, sizeof(p.tnb));
-    CUDA_TRY(ctx, cudaMemcpyAsync(chal, hs->chal, sizeof(hs->chal), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(ctx, cudaMemcpyAsync(rounds, hs->rounds, sizeof(hs->rounds), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(ctx, cudaMemcpyAsync(jobs, hs->jobs, sizeof(hs->jobs), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(ctx, cudaMemcpyAsync(at<uint32_t>(ctx, p.o_tnb), hs->tnb, sizeof(hs->tnb), cudaMemcpyHostToDevice, s));
+    if ((st = h2d_small(ctx, s, {{chal, hs->chal}, {rounds, hs->rounds}, {jobs, hs->jobs}, {at<uint32_t>(ctx, p.o_tnb), hs->tnb}},
+                        {sizeof(hs->chal), sizeof(hs->rounds), sizeof(hs->jobs), sizeof(hs->tnb)})))
+        return st;
     CUDA_TRY(ctx, cudaMemsetAsync(err, 0xff, 4 * sizeof(unsigned long long), s));
     LAUNCH(ctx, k_setup, 1, 1, 0, s, chal, p.d, p.pbits, p.rank, N, D, sc);
     LAUNCH(ctx, k_eq_fill, grid_for(p.arena, 256), 256, 0, s, jobs, p.njobs, p.arena, sc, arena);
@@ -832,9 +867,9 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
     memcpy(hs->seed, seed, 32);
     memcpy(hs->rounds, p.rd, sizeof(p.rd));
     memcpy(hs->jobs, p.jobs, sizeof(p.jobs));
-    CUDA_TRY(ctx, cudaMemcpyAsync(dseed, hs->seed, 32, cudaMemcpyHostToDevice, s));
-    CUDA_TRY(ctx, cudaMemcpyAsync(rounds, hs->rounds, sizeof(hs->rounds), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(ctx, cudaMemcpyAsync(jobs, hs->jobs, sizeof(hs->jobs), cudaMemcpyHostToDevice, s));
+    if ((st = h2d_small(ctx, s, {{dseed, hs->seed}, {rounds, hs->rounds}, {jobs, hs->jobs}},
+                        {sizeof(hs->seed), sizeof(hs->rounds), sizeof(hs->jobs)})))
+        return st;
     CUDA_TRY(ctx, cudaMemsetAsync(err, 0xff, 4 * sizeof(unsigned long long), s));
     LAUNCH(ctx, k_fs_init, 1, 1, 0, s, dseed, D, N, variant, p.d, sc, fst, dder);
     LAUNCH(ctx, k_eq_fill, grid_for(p.arena, 256), 256, 0, s, jobs, p.njobs, p.arena, sc, arena);
@@ -1637,7 +1672,7 @@ int zkl_vec_import_pair(zkl_ctx* ctx, const int32_t* x, const int32_t* y, const 
     fr* af = reinterpret_cast<fr*>(ctx->dscratch + 64);
     zkl_fr* staged = reinterpret_cast<zkl_fr*>((uint8_t*)ctx->host_out + 62000);
     *staged = *alpha_f;
-    CUDA_TRY(ctx, cudaMemcpyAsync(af, staged, sizeof(fr), cudaMemcpyHostToDevice, ctx->stream));
+    if ((st = h2d_small(ctx, ctx->stream, {{af, staged}}, {sizeof(fr)}))) return st;
     LAUNCH(ctx, k_import_canon, 1, 32, 0, ctx->stream, (const uint32_t*)af, 1, (uint32_t*)af,
            (unsigned long long*)nullptr);
     fr* consts = af + 1;
@@ -1738,7 +1773,7 @@ int zkl_table_attach_pair(zkl_ctx* ctx, zkl_table* t, const int32_t* tx, const i
     unsigned long long* bad = reinterpret_cast<unsigned long long*>(ctx->dscratch + 8);
     zkl_fr* staged = reinterpret_cast<zkl_fr*>((uint8_t*)ctx->host_out + 62000);
     *staged = *alpha_f;
-    CUDA_TRY(ctx, cudaMemcpyAsync(af, staged, sizeof(fr), cudaMemcpyHostToDevice, ctx->stream));
+    if ((st = h2d_small(ctx, ctx->stream, {{af, staged}}, {sizeof(fr)}))) return st;
     CUDA_TRY(ctx, cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), ctx->stream));
     LAUNCH(ctx, k_import_canon, 1, 32, 0, ctx->stream, (const uint32_t*)af, 1, (uint32_t*)af,
            (unsigned long long*)nullptr);
@@ -1808,7 +1843,7 @@ static int prepare_impl(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T,
         fr* af = reinterpret_cast<fr*>(ctx->dscratch + 64);
         zkl_fr* staged = reinterpret_cast<zkl_fr*>((uint8_t*)ctx->host_out + 62000);
         *staged = *pair->alpha_f;
-        CUDA_TRY(ctx, cudaMemcpyAsync(af, staged, sizeof(fr), cudaMemcpyHostToDevice, ctx->stream));
+        if ((st = h2d_small(ctx, ctx->stream, {{af, staged}}, {sizeof(fr)}))) return st;
         LAUNCH(ctx, k_import_canon, 1, 32, 0, ctx->stream, (const uint32_t*)af, 1, (uint32_t*)af,
                (unsigned long long*)nullptr);
         LAUNCH(ctx, k_pair_consts, 1, 32, 0, ctx->stream, af, af + 1);
