@@ -103,3 +103,49 @@ def test_loopback_not_in_table_smallest_global_index():
     [t.join(timeout=300) for t in th]
     group.close()
     assert all(r == ("ZKL_E_NOT_IN_TABLE", 3000) for r in res), res
+
+
+@pytest.mark.parametrize("bad", [False, True])
+def test_loopback_pair_range_prepare(bad):
+    """P = 4 ranks, function lookups through the pair-range fast path (zkl_table_attach_pair): m summed over the
+    ranks equals the global histogram; with a pair off the graph on rank 2 (and another on rank 3), every rank's
+    fast path falls back to the hash index and all report NOT_IN_TABLE at the smallest global index."""
+    import torch
+    from paper_2404_16109_b200 import zkl
+    P, D, N = 4, 1 << 14, 1 << 8
+    tx = np.arange(N, dtype=np.int32) - 128
+    ty = (tx * 5 - 3).astype(np.int32)
+    rng = np.random.default_rng(9)
+    x = rng.integers(-128, 128, D).astype(np.int32)
+    y = (x * 5 - 3).astype(np.int32)
+    if bad:
+        y[9001] += 1        # rank 2
+        y[13000] += 2       # rank 3
+    group = zkl.LoopbackGroup(P, max_D_local=D // P, max_N=N)
+    res = [None] * P
+
+    def rank_main(p):
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            ctx = zkl.Context(0, stream=stream, rank=p, group=group)
+            ctx.reserve(D // P, N)
+            tab = ctx.table(ctx.import_pair(tx, ty, 4242))
+            assert ctx.table_attach_pair(tab, tx, ty, 4242)
+            sl = slice(p * D // P, (p + 1) * D // P)
+            try:
+                _, m = ctx.prepare_pair(x[sl], y[sl], 4242, D, tab)
+                res[p] = m.cpu().numpy().astype(np.int64)
+            except zkl.ZklError as e:
+                res[p] = (e.name, e.index)
+            ctx.close()
+
+    th = [threading.Thread(target=rank_main, args=(p,)) for p in range(P)]
+    [t.start() for t in th]
+    [t.join(timeout=300) for t in th]
+    group.close()
+    if bad:
+        assert all(r == ("ZKL_E_NOT_IN_TABLE", 9001) for r in res), res
+    else:
+        ref = np.bincount(x.astype(np.int64) + 128, minlength=N)
+        for r in res:
+            assert np.array_equal(r, ref)
