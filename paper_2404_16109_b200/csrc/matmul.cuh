@@ -82,24 +82,6 @@ __device__ __forceinline__ void wide_mad(Wide& a, const fr& e, uint32_t x) {
           "r"(x));
 }
 
-// a -= b (a >= b)
-__device__ __forceinline__ void wide_sub(Wide& a, const Wide& b) {
-    asm("sub.cc.u32  %0, %0, %10;\n\t"
-        "subc.cc.u32 %1, %1, %11;\n\t"
-        "subc.cc.u32 %2, %2, %12;\n\t"
-        "subc.cc.u32 %3, %3, %13;\n\t"
-        "subc.cc.u32 %4, %4, %14;\n\t"
-        "subc.cc.u32 %5, %5, %15;\n\t"
-        "subc.cc.u32 %6, %6, %16;\n\t"
-        "subc.cc.u32 %7, %7, %17;\n\t"
-        "subc.cc.u32 %8, %8, %18;\n\t"
-        "subc.u32    %9, %9, %19;"
-        : "+r"(a.w[0]), "+r"(a.w[1]), "+r"(a.w[2]), "+r"(a.w[3]), "+r"(a.w[4]), "+r"(a.w[5]), "+r"(a.w[6]),
-          "+r"(a.w[7]), "+r"(a.w[8]), "+r"(a.w[9])
-        : "r"(b.w[0]), "r"(b.w[1]), "r"(b.w[2]), "r"(b.w[3]), "r"(b.w[4]), "r"(b.w[5]), "r"(b.w[6]), "r"(b.w[7]),
-          "r"(b.w[8]), "r"(b.w[9]));
-}
-
 // w mod r, canonical: w = hi 2^256 + lo, lo mod r by two conditional subtractions (lo < 2^256 < 3r) and
 // hi 2^256 = hi R = mont(R^2, hi) mod r
 __device__ __forceinline__ fr wide_reduce(const Wide& w) {
