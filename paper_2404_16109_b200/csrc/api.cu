@@ -1264,11 +1264,10 @@ int run_hyrax_commit(zkl_ctx* ctx, const void* pp, uint64_t cols, zkl_vec S, uin
                        h.total);
     ctx->prep_S = nullptr;
     cudaStream_t s = ctx->stream;
-    const g1a* gens = reinterpret_cast<const g1a*>(pp);
+    // pp = [generators (cols + 1, affine)] [their window tables]
     const g1a* tab = reinterpret_cast<const g1a*>((const uint8_t*)pp + align_up(sizeof(g1a) * (cols + 1)));
     uint32_t* Sc = at<uint32_t>(ctx, h.o_sc);
     g1j* part = at<g1j>(ctx, h.o_part);
-    (void)gens;
     uint32_t* drho = nullptr;
     if (rho) {
         for (uint64_t j = 0; j < h.rows; ++j)
