@@ -1240,7 +1240,14 @@ void make_hx_plan(HxPlan& h, uint64_t D, uint64_t cols) {
     h.total = o;
 }
 
-size_t hx_pp_bytes(uint64_t cols) { return align_up(sizeof(g1a) * (cols + 1)) + sizeof(g1a) * (cols + 1) * kHxTab; }
+// pp = [generators G_0..G_{cols-1}, H (affine)] [their 16-entry tables] [64 x 16 window table of H]
+size_t hx_pp_bytes(uint64_t cols) {
+    return align_up(sizeof(g1a) * (cols + 1)) + align_up(sizeof(g1a) * (cols + 1) * kHxTab) + sizeof(g1a) * 64 * kHxTab;
+}
+const g1a* hx_htab(const void* pp, uint64_t cols) {
+    return reinterpret_cast<const g1a*>((const uint8_t*)pp + align_up(sizeof(g1a) * (cols + 1)) +
+                                        align_up(sizeof(g1a) * (cols + 1) * kHxTab));
+}
 
 int hx_shape(zkl_ctx* ctx, uint64_t D, uint64_t cols) {
     if (!is_pow2(D) || !is_pow2(cols) || cols > D || cols > (1ull << 24))
@@ -1283,7 +1290,7 @@ int run_hyrax_commit(zkl_ctx* ctx, const void* pp, uint64_t cols, zkl_vec S, uin
     g1j* Q = at<g1j>(ctx, h.o_q);
     LAUNCH(ctx, k_hx_reduce_slices, (unsigned)(h.rows * kHxGroups), kHxRedThreads, 0, s, part, h.nslices, Q);
     zkl_g1* dout = at<zkl_g1>(ctx, h.o_out);
-    LAUNCH(ctx, k_hx_commit_rows, (unsigned)((h.rows + 63) / 64), 64, 0, s, Q, h.rows, drho, tab + cols * kHxTab,
+    LAUNCH(ctx, k_hx_commit_rows, (unsigned)((h.rows + 63) / 64), 64, 0, s, Q, h.rows, drho, hx_htab(pp, cols),
            dout);
     CUDA_TRY(ctx, cudaMemcpyAsync(C_host, dout, sizeof(zkl_g1) * h.rows, cudaMemcpyDeviceToHost, s));
     return sync_stream(ctx);
@@ -1480,6 +1487,7 @@ int zkl_hyrax_setup(zkl_ctx* ctx, uint64_t cols, void* pp, size_t pp_bytes) {
     g1a* tab = reinterpret_cast<g1a*>((uint8_t*)pp + align_up(sizeof(g1a) * (cols + 1)));
     LAUNCH(ctx, k_hx_gens, (unsigned)((cols + 1 + 63) / 64), 64, 0, s, cols, gens);
     LAUNCH(ctx, k_hx_tables, (unsigned)(((cols + 1) * kHxTab + 127) / 128), 128, 0, s, gens, cols + 1, tab);
+    LAUNCH(ctx, k_hx_htables, (64 * kHxTab + 127) / 128, 128, 0, s, gens + cols, const_cast<g1a*>(hx_htab(pp, cols)));
     return sync_stream(ctx);
 }
 

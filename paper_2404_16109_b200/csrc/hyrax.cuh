@@ -95,6 +95,20 @@ __global__ void k_hx_tables(const g1a* __restrict__ gens, uint64_t count, g1a* t
     tab[k] = g1_to_affine(acc);
 }
 
+// hw[w][d] = d 16^w H, w = 0..63, d = 0..15 (affine): the blind rho H becomes 64 table additions, no doublings
+__global__ void k_hx_htables(const g1a* __restrict__ H, g1a* hw) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= 64 * kHxTab) return;
+    const int w = k / kHxTab, d = k % kHxTab;
+    g1j acc = g1_infinity();
+    for (int bit = 3; bit >= 0; --bit) {
+        acc = g1_dbl(acc);
+        if ((d >> bit) & 1) acc = g1_add_affine(acc, *H);
+    }
+    for (int i = 0; i < 4 * w; ++i) acc = g1_dbl(acc);
+    hw[k] = g1_to_affine(acc);
+}
+
 // canonical scalars (the digits are read from the integer value)
 __global__ void k_hx_canon(const uint32_t* __restrict__ S, uint64_t n, uint32_t* out) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
@@ -168,14 +182,11 @@ __global__ void k_hx_commit_rows(const g1j* __restrict__ Q, uint64_t rows, const
         for (int k = 0; k < 32; ++k) acc = g1_dbl(acc);
         acc = g1_add(acc, Q[j * kHxGroups + g]);
     }
-    if (rho_canon) {
-        g1j h = g1_infinity();
-        for (int w = 63; w >= 0; --w) {
-            h = g1_dbl(g1_dbl(g1_dbl(g1_dbl(h))));
+    if (rho_canon) {   // rho H = sum_w hw[w][digit_w] (htab: the 64 x 16 window table of H)
+        for (int w = 0; w < 64; ++w) {
             const uint32_t d = (rho_canon[j * 8 + (w >> 3)] >> ((w & 7) * 4)) & 15u;
-            if (d) h = g1_add_affine(h, htab[d]);
+            if (d) acc = g1_add_affine(acc, htab[w * kHxTab + d]);
         }
-        acc = g1_add(acc, h);
     }
     const g1a a = g1_to_affine(acc);
     zkl_g1 o;
