@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libzkl.so")
-SOURCES = ["api.cu"]
+SOURCES = ["api.cu", "mm_api.cu", "hx_api.cu"]   # compiled in parallel, linked into one .so
 DEPS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh", ".h")))   # every source and header
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 def _nccl_include() -> str:
@@ -28,6 +28,19 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-I", os.path.join(ROOT, "include")]
 
 
+def _includes(path, seen=None):
+    """path and every file it includes with #include "..." (transitively)."""
+    import re
+    seen = set() if seen is None else seen
+    path = os.path.normpath(path)
+    if path in seen or not os.path.exists(path):
+        return seen
+    seen.add(path)
+    for m in re.finditer(r'^#include "([^"]+)"', open(path).read(), re.M):
+        _includes(os.path.join(os.path.dirname(path), m.group(1)), seen)
+    return seen
+
+
 def needs_build() -> bool:
     if not os.path.exists(LIB):
         return True
@@ -39,16 +52,41 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
-    cmd = [NVCC, *FLAGS, "-I", _nccl_include(), "-o", LIB] + [os.path.join(CSRC, f) for f in SOURCES] + ["-ldl"]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    import concurrent.futures as cf
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    inc = ["-I", _nccl_include()]
+    cflags = [f for f in FLAGS if f != "-shared"]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        cmd = [NVCC, *cflags, *inc, "-c", "-o", obj, os.path.join(CSRC, src)]
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(
+                os.path.getmtime(f) for f in _includes(os.path.join(CSRC, src))):
+            return src, obj, cmd, subprocess.CompletedProcess(cmd, 0, "", "(up to date)\n")
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, cmd, r
+
+    with cf.ThreadPoolExecutor(len(SOURCES)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+        for src, obj, cmd, r in results:
+            f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+    for src, obj, cmd, r in results:
+        if r.returncode != 0:
+            sys.stderr.write(r.stderr[-8000:])
+            raise RuntimeError(f"nvcc failed on {src} (see {log})")
+    link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB] + [o for _, o, _, _ in results] + ["-ldl"]
+    r = subprocess.run(link, capture_output=True, text=True)
+    with open(log, "a") as f:
+        f.write(" ".join(link) + "\n" + r.stdout + r.stderr)
     if r.returncode != 0:
         sys.stderr.write(r.stderr[-8000:])
-        raise RuntimeError(f"nvcc failed (see {log})")
+        raise RuntimeError(f"link failed (see {log})")
     if verbose:
-        sys.stderr.write(r.stderr)
+        for _, _, _, rr in results:
+            sys.stderr.write(rr.stderr)
     return LIB
 
 

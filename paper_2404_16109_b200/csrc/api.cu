@@ -23,69 +23,14 @@
 
 #include "fs.cuh"
 #include "kernels.cuh"
-#include "matmul.cuh"
-#include "hyrax.cuh"
+#include "host_common.h"
 #include "nccl_loader.h"
 
 using namespace zkl;
 
 namespace {
 
-constexpr int kSMs = 148;
-
-int set_err(zkl_ctx* ctx, int st, const char* fmt, ...) {
-    if (ctx) {
-        va_list ap;
-        va_start(ap, fmt);
-        vsnprintf(ctx->last_error, sizeof(ctx->last_error), fmt, ap);
-        va_end(ap);
-    }
-    return st;
-}
-
-#define CUDA_TRY(ctx, call)                                                                         \
-    do {                                                                                            \
-        cudaError_t e_ = (call);                                                                    \
-        if (e_ != cudaSuccess) {                                                                    \
-            if (e_ != cudaErrorInvalidValue && e_ != cudaErrorMemoryAllocation) (ctx)->poisoned = 1; \
-            return set_err((ctx), ZKL_E_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_),       \
-                           __FILE__, __LINE__);                                                     \
-        }                                                                                           \
-    } while (0)
-
-// Every kernel launch goes through LAUNCH: counted, and (when profiling) bracketed by events on
-// the launching stream.
-#define LAUNCH(ctx, kern, grid, block, smem, stream, ...)                                           \
-    do {                                                                                            \
-        zkl_ctx::ProfRec* pr_ = prof_begin((ctx), #kern, (stream));                                 \
-        kern<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                                   \
-        (ctx)->launches++;                                                                          \
-        if (pr_) cudaEventRecord(pr_->b, (stream));                                                 \
-        CUDA_TRY(ctx, cudaGetLastError());                                                          \
-    } while (0)
-
-zkl_ctx::ProfRec* prof_begin(zkl_ctx* ctx, const char* name, cudaStream_t st) {
-    if (!ctx->profiling || ctx->nprof >= 256) return nullptr;
-    zkl_ctx::ProfRec* r = &ctx->prof[ctx->nprof++];
-    r->name = name;
-    r->stream = st;
-    cudaEventRecord(r->a, st);
-    return r;
-}
-
-bool is_pow2(uint64_t x) { return x && !(x & (x - 1)); }
-int ilog2(uint64_t x) { int k = 0; while ((1ull << k) < x) ++k; return k; }
-size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
-size_t soa_bytes(uint64_t n) { return align_up(8 * 4 * std::max<uint64_t>(n, 4)); }
-
-unsigned grid_for(uint64_t work, unsigned threads, unsigned cap) {
-    uint64_t g = (work + threads - 1) / threads;
-    if (g < 1) g = 1;
-    if (g > cap) g = cap;
-    return (unsigned)g;
-}
-
-unsigned grid_for(uint64_t work, unsigned threads) { return grid_for(work, threads, kSMs * 8); }
+using namespace zkl_host;
 
 int hist_rows_for(uint64_t Dp, uint64_t N) {
     uint64_t ntiles = (Dp + kHistTile - 1) / kHistTile;
@@ -108,7 +53,7 @@ struct InvPlan {
     size_t o_val[12], o_slot[12], o_topinv;
 };
 
-unsigned grid_for(uint64_t work, unsigned threads, unsigned cap);
+
 
 struct Plan {
     uint64_t D, Dp, N;
@@ -271,6 +216,9 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
     auto take = [&](size_t bytes) { size_t r = o; o += align_up(bytes); return r; };
     // the index-map keys outlive the call (prepare -> prove): first, at an offset that depends on nothing else
     p.o_keys = take(sizeof(uint32_t) * std::max<uint64_t>(p.Dp, 4));
+    // the histogram rows of an async-mode prepare are written on the low stream while the following proof runs, so
+    // they too sit at an offset that depends only on (D_local, N): never inside any plan's proof buffers
+    p.o_hist = take(sizeof(uint32_t) * (size_t)p.hist_rows * N);
     p.o_out = take(sizeof(ProofOut));
     p.o_sc = take(sizeof(ProofScalars));
     p.o_err = take(4 * sizeof(unsigned long long));
@@ -290,7 +238,6 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
     p.o_small = take(soa_bytes(std::min<uint64_t>(p.Dp, kInvTile)));
     p.o_derived = take(sizeof(zkl_fr) * (3 + 2 * kMaxRounds));
     p.o_arena = take(sizeof(fr) * p.arena);
-    p.o_hist = take(sizeof(uint32_t) * (size_t)p.hist_rows * N);
     p.o_tot = take(soa_bytes(p.ntiles));
     p.o_totinv = take(soa_bytes(p.ntiles));
     p.o_A = take(soa_bytes(p.Dp));
@@ -345,24 +292,7 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
     p.total = o;
 }
 
-template <typename T>
-T* at(zkl_ctx* ctx, size_t off) { return reinterpret_cast<T*>(ctx->ws + off); }
 
-int check_ctx(zkl_ctx* ctx) {
-    if (!ctx) return ZKL_E_ARG;
-    if (ctx->poisoned) return set_err(ctx, ZKL_E_STATE, "context poisoned by an earlier CUDA fault");
-    CUDA_TRY(ctx, cudaSetDevice(ctx->device));
-    return ZKL_OK;
-}
-
-int check_vec(zkl_ctx* ctx, const zkl_vec& v, uint64_t n, const char* name) {
-    if (!v.limbs) return set_err(ctx, ZKL_E_ARG, "%s: null", name);
-    if (v.n != n) return set_err(ctx, ZKL_E_SHAPE, "%s: length %llu, expected %llu", name,
-                                 (unsigned long long)v.n, (unsigned long long)n);
-    if (n >= 4 && ((n & 3) || ((uintptr_t)v.limbs & 15)))
-        return set_err(ctx, ZKL_E_ARG, "%s: limbs must be 16-byte aligned and n a multiple of 4", name);
-    return ZKL_OK;
-}
 
 int check_shape(zkl_ctx* ctx, uint64_t D, uint64_t N) {
     if (!is_pow2(D) || !is_pow2(N) || N > D)
@@ -373,6 +303,7 @@ int check_shape(zkl_ctx* ctx, uint64_t D, uint64_t N) {
         return set_err(ctx, ZKL_E_SHAPE, "P=%d must be a power of two dividing D", ctx->nranks);
     return ZKL_OK;
 }
+
 
 int need_ws(zkl_ctx* ctx, const Plan& p) {
     if (!ctx->ws || ctx->ws_bytes < p.total)
@@ -385,47 +316,6 @@ int need_ws(zkl_ctx* ctx, const Plan& p) {
 // kernel reading the mapped host memory (zero-copy over PCIe), not by cudaMemcpyAsync: a copy-engine transfer would
 // queue behind a large H2D copy the caller has in flight on another stream (e.g. the next step's inputs) and stall
 // the proof until it drains.
-struct CopySeg {
-    uint32_t* dst;
-    const uint32_t* src;
-    uint32_t words;
-};
-struct CopySegs {
-    CopySeg seg[4];
-    int n;
-};
-__global__ void k_copy_from_host(CopySegs c) {
-    for (int g = 0; g < c.n; ++g)
-        for (uint32_t i = threadIdx.x; i < c.seg[g].words; i += blockDim.x) c.seg[g].dst[i] = c.seg[g].src[i];
-}
-
-int h2d_small(zkl_ctx* ctx, cudaStream_t s, std::initializer_list<std::pair<void*, const void*>> dsts,
-              std::initializer_list<size_t> sizes) {
-    CopySegs c;
-    c.n = 0;
-    auto sz = sizes.begin();
-    for (const auto& d : dsts) {
-        c.seg[c.n].dst = reinterpret_cast<uint32_t*>(d.first);
-        c.seg[c.n].src = reinterpret_cast<const uint32_t*>(d.second);   // pinned (cudaMallocHost): UVA device-visible
-        c.seg[c.n].words = (uint32_t)(*sz / 4);
-        ++c.n;
-        ++sz;
-    }
-    LAUNCH(ctx, k_copy_from_host, 1, 256, 0, s, c);
-    return ZKL_OK;
-}
-
-int sync_stream(zkl_ctx* ctx) {
-    cudaError_t e = cudaStreamSynchronize(ctx->stream);
-    if (e != cudaSuccess) {
-        ctx->poisoned = 1;
-        return set_err(ctx, ZKL_E_CUDA, "asynchronous CUDA error: %s", cudaGetErrorString(e));
-    }
-    return ZKL_OK;
-}
-
-// ------------------------------------------------------------------ hierarchical batched inversion (a4)
-// Forward passes: level 0 on `s0` (the caller's stream), the levels above and the one-block top on `s1`.
 int inv_forward(zkl_ctx* ctx, const InvPlan& ip, const uint32_t* X0, uint64_t n0total, uint32_t* slots0,
                 const ProofScalars* sc, uint64_t err_off, unsigned long long* err, cudaStream_t s0, cudaStream_t s1,
                 cudaEvent_t ev) {
@@ -1046,298 +936,6 @@ int proof_fs_collect(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table
 }
 
 // ------------------------------------------------------------------ matmul sumcheck
-bool fr_ge_r_host(const zkl_fr& x) {
-    static const uint32_t rl[8] = {0x00000001u, 0xffffffffu, 0xfffe5bfeu, 0x53bda402u,
-                                   0x09a1d805u, 0x3339d808u, 0x299d7d48u, 0x73eda753u};
-    for (int i = 7; i >= 0; --i)
-        if (x.w[i] != rl[i]) return x.w[i] > rl[i];
-    return true;
-}
-
-struct MMPlan {
-    uint64_t m, n, p;
-    int lm, L, lp;
-    int kc, nr;              // chunked rounds kc .. kc+nr-1 (0 = none)
-    uint64_t chunk, nchunks; // chunk elements, number of chunks (= elements left for the tail)
-    uint32_t gridA[kMaxRounds];   // multi-block rounds 1 .. kc-1: blocks per round
-    MMRound rd[kMaxRounds];
-    uint64_t parts;          // total partial rows (fr)
-    uint64_t rowchunks;      // row chunks of the a-restriction
-    size_t o_ch, o_eu, o_ev, o_rpart, o_a, o_b, o_f1a, o_f1b, o_f2a, o_f2b, o_ca, o_cb, o_parts, o_rd, o_fin, o_out,
-        total;
-};
-
-void make_mm_plan(MMPlan& q, uint64_t m, uint64_t n, uint64_t p) {
-    memset(&q, 0, sizeof(q));
-    q.m = m; q.n = n; q.p = p;
-    q.lm = ilog2(m); q.L = ilog2(n); q.lp = ilog2(p);
-    uint64_t rows = 0;
-    int k = 1;
-    uint64_t len = n;
-    for (; k <= q.L && len > kMMChunkMaxElems; ++k, len /= 2) {
-        q.gridA[k - 1] = grid_for(len / 2, kMMThreads, kMaxBlocks);
-        q.rd[k - 1] = MMRound{3 * rows, q.gridA[k - 1]};
-        rows += q.gridA[k - 1];
-    }
-    if (k <= q.L) {
-        q.kc = k;
-        q.chunk = std::min<uint64_t>(kMMChunk, len);
-        q.nr = ilog2(q.chunk);
-        q.nchunks = len / q.chunk;
-        for (int j = 0; j < q.nr; ++j) {
-            q.rd[k + j - 1] = MMRound{3 * rows, (uint32_t)(q.nchunks * kMMChunkWarps)};
-            rows += q.nchunks * kMMChunkWarps;
-        }
-        for (int kk = k + q.nr; kk <= q.L; ++kk) {
-            q.rd[kk - 1] = MMRound{3 * rows, 1};
-            rows += 1;
-        }
-    }
-    q.parts = 3 * std::max<uint64_t>(rows, 1);
-    q.rowchunks = (m + kMMRowChunk - 1) / kMMRowChunk;
-    size_t o = 0;
-    auto take = [&](size_t bytes) { size_t r = o; o += align_up(bytes); return r; };
-    q.o_ch = take(sizeof(fr) * (q.lm + q.lp + q.L + 1));
-    q.o_eu = take(sizeof(fr) * m);
-    q.o_ev = take(sizeof(fr) * p);
-    q.o_rpart = take(sizeof(fr) * q.rowchunks * n);
-    q.o_a = take(soa_bytes(n));
-    q.o_b = take(soa_bytes(n));
-    q.o_f1a = take(soa_bytes(n / 2));
-    q.o_f1b = take(soa_bytes(n / 2));
-    q.o_f2a = take(soa_bytes(n / 4));
-    q.o_f2b = take(soa_bytes(n / 4));
-    q.o_ca = take(soa_bytes(128));
-    q.o_cb = take(soa_bytes(128));
-    q.o_parts = take(sizeof(fr) * q.parts);
-    q.o_rd = take(sizeof(MMRound) * kMaxRounds);
-    q.o_fin = take(sizeof(fr) * 2);
-    q.o_out = take(sizeof(zkl_fr) * (3 + 3 * kMaxRounds));
-    q.total = o;
-}
-
-int run_matmul(zkl_ctx* ctx, const int32_t* A, const int32_t* B, uint64_t m, uint64_t n, uint64_t p,
-               const zkl_fr* u, const zkl_fr* v, const zkl_fr* r, zkl_vec a_out, zkl_vec b_out, zkl_fr* claim,
-               zkl_fr* round_evals, zkl_fr* finals) {
-    int st;
-    if ((st = check_ctx(ctx))) return st;
-    if (ctx->async_mode) return set_err(ctx, ZKL_E_STATE, "matmul prove: synchronous calls only");
-    if (!A || !B || !claim || !finals || (n > 1 && (!r || !round_evals)) || (m > 1 && !u) || (p > 1 && !v))
-        return set_err(ctx, ZKL_E_ARG, "null argument");
-    if (!is_pow2(m) || !is_pow2(n) || !is_pow2(p) || ilog2(n) > kMaxRounds - 1 || ilog2(m) > 32 || ilog2(p) > 32)
-        return set_err(ctx, ZKL_E_SHAPE, "m=%llu n=%llu p=%llu: powers of two, n <= 2^%d", (unsigned long long)m,
-                       (unsigned long long)n, (unsigned long long)p, kMaxRounds - 1);
-    MMPlan q;
-    make_mm_plan(q, m, n, p);
-    if (!ctx->ws || ctx->ws_bytes < q.total)
-        return set_err(ctx, ZKL_E_OOM, "workspace %zu bytes < %zu required (zkl_matmul_workspace_bytes)",
-                       ctx->ws_bytes, q.total);
-    if (a_out.limbs && (st = check_vec(ctx, a_out, n, "a_out"))) return st;
-    if (b_out.limbs && (st = check_vec(ctx, b_out, n, "b_out"))) return st;
-    ctx->prep_S = nullptr;   // the workspace (and the cached index-map keys in it) is reused here
-    cudaStream_t s = ctx->stream;
-    // challenges u | v | r, canonical, through the pinned staging area
-    const int nch = q.lm + q.lp + q.L;
-    zkl_fr* hs = reinterpret_cast<zkl_fr*>((uint8_t*)ctx->host_out + 40000);
-    for (int i = 0; i < q.lm; ++i) hs[i] = u[i];
-    for (int i = 0; i < q.lp; ++i) hs[q.lm + i] = v[i];
-    for (int i = 0; i < q.L; ++i) hs[q.lm + q.lp + i] = r[i];
-    for (int i = 0; i < nch; ++i)
-        if (fr_ge_r_host(hs[i])) return set_err(ctx, ZKL_E_NONCANONICAL, "challenge %d is not canonical", i);
-    memcpy(reinterpret_cast<uint8_t*>(hs) + sizeof(zkl_fr) * (nch + 1), q.rd, sizeof(q.rd));
-    zkl_fr* dstage = at<zkl_fr>(ctx, q.o_out);   // raw challenges land in the output area first
-    fr* ch = at<fr>(ctx, q.o_ch);
-    MMRound* drd = at<MMRound>(ctx, q.o_rd);
-    if (nch) CUDA_TRY(ctx, cudaMemcpyAsync(dstage, hs, sizeof(zkl_fr) * nch, cudaMemcpyHostToDevice, s));
-    CUDA_TRY(ctx, cudaMemcpyAsync(drd, reinterpret_cast<uint8_t*>(hs) + sizeof(zkl_fr) * (nch + 1), sizeof(q.rd),
-                                  cudaMemcpyHostToDevice, s));
-    if (nch) LAUNCH(ctx, k_mm_consts, (nch + 63) / 64, 64, 0, s, dstage, nch, ch);
-    const fr *cu = ch, *cv = ch + q.lm, *cr = ch + q.lm + q.lp;
-    fr* Eu = at<fr>(ctx, q.o_eu);
-    fr* Ev = at<fr>(ctx, q.o_ev);
-    LAUNCH(ctx, k_mm_eq, grid_for(m, 256), 256, 0, s, cu, q.lm, m, Eu);
-    LAUNCH(ctx, k_mm_eq, grid_for(p, 256), 256, 0, s, cv, q.lp, p, Ev);
-    // restrictions a = A~(u, .), b = B~(., v)
-    uint32_t* a = a_out.limbs ? a_out.limbs : at<uint32_t>(ctx, q.o_a);
-    uint32_t* b = b_out.limbs ? b_out.limbs : at<uint32_t>(ctx, q.o_b);
-    fr* rpart = at<fr>(ctx, q.o_rpart);
-    {
-        dim3 grid((unsigned)((n + kMMThreads - 1) / kMMThreads), (unsigned)q.rowchunks);
-        LAUNCH(ctx, k_mm_restrict_rows, grid, kMMThreads, 0, s, A, m, n, Eu, rpart);
-        LAUNCH(ctx, k_mm_sum_chunks, grid_for(n, 256), 256, 0, s, rpart, q.rowchunks, n, a);
-        if (n % kMMColRows == 0)
-            LAUNCH(ctx, k_mm_restrict_cols_tiled, (unsigned)(n / kMMColRows), kMMThreads, 0, s, B, n, p, Ev, b);
-        else
-            LAUNCH(ctx, k_mm_restrict_cols, (unsigned)((n + kMMThreads / 32 - 1) / (kMMThreads / 32)), kMMThreads, 0,
-                   s, B, n, p, Ev, b);
-    }
-    // the degree-2 sumcheck on (a, b)
-    fr* parts = at<fr>(ctx, q.o_parts);
-    fr* fin = at<fr>(ctx, q.o_fin);
-    const uint32_t *ca = a, *cb = b;
-    uint64_t len = n;
-    for (int k = 1; k < (q.kc ? q.kc : q.L + 1) && q.gridA[k - 1]; ++k) {
-        uint32_t* na = at<uint32_t>(ctx, (k & 1) == 0 ? q.o_f1a : q.o_f2a);   // k = 2 writes n/2 elements
-        uint32_t* nb = at<uint32_t>(ctx, (k & 1) == 0 ? q.o_f1b : q.o_f2b);
-        const int fold = k > 1;
-        LAUNCH(ctx, k_mm_round, q.gridA[k - 1], kMMThreads, 0, s, ca, cb, len, fold, cr, k, na, nb,
-               parts + q.rd[k - 1].base, q.rd[k - 1].rows);
-        if (fold) {
-            ca = na; cb = nb;
-            len /= 2;
-        }
-    }
-    uint32_t* ta = at<uint32_t>(ctx, q.o_ca);
-    uint32_t* tb = at<uint32_t>(ctx, q.o_cb);
-    uint64_t tlen;
-    int k0;
-    if (q.kc) {
-        const int fold = q.kc > 1;
-        LAUNCH(ctx, k_mm_chunk, (unsigned)q.nchunks, kMMChunk / 2, 2 * kMMChunk * sizeof(fr), s, ca, cb, len, fold,
-               (int)q.chunk, q.nr, cr, q.kc, drd, parts, ta, tb);
-        tlen = q.nchunks;
-        k0 = q.kc + q.nr;
-    } else {   // n = 1: no rounds
-        ta = a; tb = b;
-        tlen = 1;
-        k0 = 1;
-    }
-    LAUNCH(ctx, k_mm_tail, 1, 32, 0, s, ta, tb, tlen, cr, k0, q.L, drd, parts, fin);
-    zkl_fr* dout = at<zkl_fr>(ctx, q.o_out);
-    LAUNCH(ctx, k_mm_finish, q.L + 1, 256, 0, s, parts, drd, q.L, fin, dout);
-    zkl_fr* hout = reinterpret_cast<zkl_fr*>((uint8_t*)ctx->host_out + 45000);
-    CUDA_TRY(ctx, cudaMemcpyAsync(hout, dout, sizeof(zkl_fr) * (3 + 3 * q.L), cudaMemcpyDeviceToHost, s));
-    if ((st = sync_stream(ctx))) return st;
-    *claim = hout[0];
-    finals[0] = hout[1];
-    finals[1] = hout[2];
-    if (q.L) memcpy(round_evals, hout + 3, sizeof(zkl_fr) * 3 * q.L);
-    return ZKL_OK;
-}
-
-// ------------------------------------------------------------------ Hyrax commitments
-struct HxPlan {
-    uint64_t D, cols, rows, nslices;
-    size_t o_sc, o_part, o_q, o_rho, o_out, o_v, o_er, o_ec, o_ypart, o_y, total;
-};
-
-void make_hx_plan(HxPlan& h, uint64_t D, uint64_t cols) {
-    memset(&h, 0, sizeof(h));
-    h.D = D; h.cols = cols; h.rows = D / cols;
-    h.nslices = (cols + kHxSlice - 1) / kHxSlice;
-    size_t o = 0;
-    auto take = [&](size_t bytes) { size_t r = o; o += align_up(bytes); return r; };
-    h.o_sc = take(soa_bytes(D));
-    h.o_part = take(sizeof(g1j) * h.rows * h.nslices * kHxGroups);
-    h.o_q = take(sizeof(g1j) * h.rows * kHxGroups);
-    h.o_rho = take(sizeof(zkl_fr) * h.rows);
-    h.o_out = take(sizeof(zkl_g1) * h.rows);
-    h.o_v = take(sizeof(fr) * 64);
-    h.o_er = take(sizeof(fr) * h.rows);
-    h.o_ec = take(sizeof(fr) * cols);
-    h.o_ypart = take(sizeof(fr) * 256);
-    h.o_y = take(sizeof(zkl_fr));
-    h.total = o;
-}
-
-// pp = [generators G_0..G_{cols-1}, H (affine)] [their 16-entry tables] [64 x 16 window table of H]
-size_t hx_pp_bytes(uint64_t cols) {
-    return align_up(sizeof(g1a) * (cols + 1)) + align_up(sizeof(g1a) * (cols + 1) * kHxTab) + sizeof(g1a) * 64 * kHxTab;
-}
-const g1a* hx_htab(const void* pp, uint64_t cols) {
-    return reinterpret_cast<const g1a*>((const uint8_t*)pp + align_up(sizeof(g1a) * (cols + 1)) +
-                                        align_up(sizeof(g1a) * (cols + 1) * kHxTab));
-}
-
-int hx_shape(zkl_ctx* ctx, uint64_t D, uint64_t cols) {
-    if (!is_pow2(D) || !is_pow2(cols) || cols > D || cols > (1ull << 24))
-        return set_err(ctx, ZKL_E_SHAPE, "Hyrax: D=%llu cols=%llu must be powers of two with cols <= D, 2^24",
-                       (unsigned long long)D, (unsigned long long)cols);
-    return ZKL_OK;
-}
-
-int run_hyrax_commit(zkl_ctx* ctx, const void* pp, uint64_t cols, zkl_vec S, uint64_t D, const zkl_fr* rho,
-                     zkl_g1* C_host) {
-    int st;
-    if ((st = check_ctx(ctx))) return st;
-    if (ctx->async_mode) return set_err(ctx, ZKL_E_STATE, "Hyrax: synchronous calls only");
-    if (!pp || !C_host) return set_err(ctx, ZKL_E_ARG, "null argument");
-    if ((st = hx_shape(ctx, D, cols))) return st;
-    if ((st = check_vec(ctx, S, D, "S"))) return st;
-    HxPlan h;
-    make_hx_plan(h, D, cols);
-    if (!ctx->ws || ctx->ws_bytes < h.total)
-        return set_err(ctx, ZKL_E_OOM, "workspace %zu bytes < %zu required (zkl_hyrax_workspace_bytes)", ctx->ws_bytes,
-                       h.total);
-    ctx->prep_S = nullptr;
-    cudaStream_t s = ctx->stream;
-    // pp = [generators (cols + 1, affine)] [their window tables]
-    const g1a* tab = reinterpret_cast<const g1a*>((const uint8_t*)pp + align_up(sizeof(g1a) * (cols + 1)));
-    uint32_t* Sc = at<uint32_t>(ctx, h.o_sc);
-    g1j* part = at<g1j>(ctx, h.o_part);
-    uint32_t* drho = nullptr;
-    if (rho) {
-        for (uint64_t j = 0; j < h.rows; ++j)
-            if (fr_ge_r_host(rho[j])) return set_err(ctx, ZKL_E_NONCANONICAL, "rho_%llu is not canonical",
-                                                     (unsigned long long)j);
-        drho = at<uint32_t>(ctx, h.o_rho);
-        CUDA_TRY(ctx, cudaMemcpyAsync(drho, rho, sizeof(zkl_fr) * h.rows, cudaMemcpyHostToDevice, s));
-    }
-    LAUNCH(ctx, k_hx_canon, grid_for(D, 256), 256, 0, s, S.limbs, D, Sc);
-    const uint64_t nthreads = h.rows * h.nslices * kHxGroups;
-    LAUNCH(ctx, k_hx_commit_partial, (unsigned)((nthreads + kHxThreads - 1) / kHxThreads), kHxThreads, 0, s, Sc, D,
-           cols, tab, h.nslices, part);
-    g1j* Q = at<g1j>(ctx, h.o_q);
-    LAUNCH(ctx, k_hx_reduce_slices, (unsigned)(h.rows * kHxGroups), kHxRedThreads, 0, s, part, h.nslices, Q);
-    zkl_g1* dout = at<zkl_g1>(ctx, h.o_out);
-    LAUNCH(ctx, k_hx_commit_rows, (unsigned)((h.rows + 63) / 64), 64, 0, s, Q, h.rows, drho, hx_htab(pp, cols),
-           dout);
-    CUDA_TRY(ctx, cudaMemcpyAsync(C_host, dout, sizeof(zkl_g1) * h.rows, cudaMemcpyDeviceToHost, s));
-    return sync_stream(ctx);
-}
-
-int run_hyrax_eval(zkl_ctx* ctx, zkl_vec S, uint64_t D, uint64_t cols, const zkl_fr* v, zkl_vec w_out,
-                   zkl_fr* y_host) {
-    int st;
-    if ((st = check_ctx(ctx))) return st;
-    if (ctx->async_mode) return set_err(ctx, ZKL_E_STATE, "Hyrax: synchronous calls only");
-    if (!v || !y_host || !w_out.limbs) return set_err(ctx, ZKL_E_ARG, "null argument");
-    if ((st = hx_shape(ctx, D, cols))) return st;
-    if ((st = check_vec(ctx, S, D, "S")) || (st = check_vec(ctx, w_out, cols, "w_out"))) return st;
-    HxPlan h;
-    make_hx_plan(h, D, cols);
-    if (!ctx->ws || ctx->ws_bytes < h.total)
-        return set_err(ctx, ZKL_E_OOM, "workspace %zu bytes < %zu required (zkl_hyrax_workspace_bytes)", ctx->ws_bytes,
-                       h.total);
-    ctx->prep_S = nullptr;
-    const int d = ilog2(D), lr = ilog2(h.rows), lc = ilog2(cols);
-    for (int i = 0; i < d; ++i)
-        if (fr_ge_r_host(v[i])) return set_err(ctx, ZKL_E_NONCANONICAL, "v_%d is not canonical", i);
-    cudaStream_t s = ctx->stream;
-    zkl_fr* hs = reinterpret_cast<zkl_fr*>((uint8_t*)ctx->host_out + 40000);
-    memcpy(hs, v, sizeof(zkl_fr) * d);
-    zkl_fr* dstage = at<zkl_fr>(ctx, h.o_rho);
-    fr* dv = at<fr>(ctx, h.o_v);
-    if (d) {
-        CUDA_TRY(ctx, cudaMemcpyAsync(dstage, hs, sizeof(zkl_fr) * d, cudaMemcpyHostToDevice, s));
-        LAUNCH(ctx, k_mm_consts, 1, 64, 0, s, dstage, d, dv);
-    }
-    fr* Er = at<fr>(ctx, h.o_er);
-    fr* Ec = at<fr>(ctx, h.o_ec);
-    LAUNCH(ctx, k_hx_eq, grid_for(h.rows, 256), 256, 0, s, dv, lr, h.rows, Er);
-    LAUNCH(ctx, k_hx_eq, grid_for(cols, 256), 256, 0, s, dv + lr, lc, cols, Ec);
-    LAUNCH(ctx, k_hx_eval_w, (unsigned)((cols + 127) / 128), 128, 0, s, S.limbs, D, cols, Er, w_out.limbs);
-    const unsigned nb = grid_for(cols, 256, 256);
-    LAUNCH(ctx, k_hx_eval_y, nb, 256, 0, s, w_out.limbs, cols, Ec, at<fr>(ctx, h.o_ypart));
-    zkl_fr* dy = at<zkl_fr>(ctx, h.o_y);
-    LAUNCH(ctx, k_hx_eval_y_final, 1, 256, 0, s, at<fr>(ctx, h.o_ypart), (int)nb, dy);
-    zkl_fr* hy = reinterpret_cast<zkl_fr*>((uint8_t*)ctx->host_out + 45000);
-    CUDA_TRY(ctx, cudaMemcpyAsync(hy, dy, sizeof(zkl_fr), cudaMemcpyDeviceToHost, s));
-    if ((st = sync_stream(ctx))) return st;
-    *y_host = *hy;
-    return ZKL_OK;
-}
-
 }  // namespace
 
 // ====================================================================== ABI
@@ -1398,7 +996,6 @@ static int ctx_create_common(int device, void* stream, zkl_ctx** out) {
     cudaFuncSetAttribute(k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tail_smem);
     cudaFuncSetAttribute(k_batch_invert, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 1024 * (int)sizeof(fr));
     cudaFuncSetAttribute(k_tab_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kTabChunk * (int)sizeof(fr));
-    cudaFuncSetAttribute(k_mm_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kMMChunk * (int)sizeof(fr));
     cudaFuncSetAttribute(k_chunk_rounds, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(2 * kChunk * sizeof(fr)));
     *out = c;
@@ -1459,66 +1056,6 @@ int zkl_ctx_create_loopback(int device, void* cuda_stream, zkl_group* group, int
     (*out)->rank = rank;
     (*out)->nranks = group->nranks;
     return ZKL_OK;
-}
-
-size_t zkl_matmul_workspace_bytes(uint64_t m, uint64_t n, uint64_t p) {
-    if (!is_pow2(m) || !is_pow2(n) || !is_pow2(p)) return 0;
-    MMPlan q;
-    make_mm_plan(q, m, n, p);
-    return q.total;
-}
-
-int zkl_matmul_prove(zkl_ctx* ctx, const int32_t* A, const int32_t* B, uint64_t m, uint64_t n, uint64_t p,
-                     const zkl_fr* u, const zkl_fr* v, const zkl_fr* r, zkl_vec a_out, zkl_vec b_out, zkl_fr* claim,
-                     zkl_fr* round_evals, zkl_fr* finals) {
-    return run_matmul(ctx, A, B, m, n, p, u, v, r, a_out, b_out, claim, round_evals, finals);
-}
-
-size_t zkl_hyrax_pp_bytes(uint64_t cols) { return is_pow2(cols) ? hx_pp_bytes(cols) : 0; }
-
-int zkl_hyrax_setup(zkl_ctx* ctx, uint64_t cols, void* pp, size_t pp_bytes) {
-    int st;
-    if ((st = check_ctx(ctx))) return st;
-    if (!pp) return set_err(ctx, ZKL_E_ARG, "null argument");
-    if (!is_pow2(cols) || cols > (1ull << 24)) return set_err(ctx, ZKL_E_SHAPE, "cols must be a power of two <= 2^24");
-    if (pp_bytes < hx_pp_bytes(cols)) return set_err(ctx, ZKL_E_OOM, "pp %zu bytes < %zu", pp_bytes, hx_pp_bytes(cols));
-    cudaStream_t s = ctx->stream;
-    g1a* gens = reinterpret_cast<g1a*>(pp);
-    g1a* tab = reinterpret_cast<g1a*>((uint8_t*)pp + align_up(sizeof(g1a) * (cols + 1)));
-    LAUNCH(ctx, k_hx_gens, (unsigned)((cols + 1 + 63) / 64), 64, 0, s, cols, gens);
-    LAUNCH(ctx, k_hx_tables, (unsigned)(((cols + 1) * kHxTab + 127) / 128), 128, 0, s, gens, cols + 1, tab);
-    LAUNCH(ctx, k_hx_htables, (64 * kHxTab + 127) / 128, 128, 0, s, gens + cols, const_cast<g1a*>(hx_htab(pp, cols)));
-    return sync_stream(ctx);
-}
-
-int zkl_hyrax_export_generators(zkl_ctx* ctx, const void* pp, uint64_t cols, zkl_g1* out_host) {
-    int st;
-    if ((st = check_ctx(ctx))) return st;
-    if (!pp || !out_host) return set_err(ctx, ZKL_E_ARG, "null argument");
-    if (!is_pow2(cols)) return set_err(ctx, ZKL_E_SHAPE, "cols must be a power of two");
-    zkl_g1* d = nullptr;
-    CUDA_TRY(ctx, cudaMallocAsync((void**)&d, sizeof(zkl_g1) * (cols + 1), ctx->stream));
-    LAUNCH(ctx, k_hx_export, (unsigned)((cols + 1 + 127) / 128), 128, 0, ctx->stream, (const g1a*)pp, cols + 1, d);
-    CUDA_TRY(ctx, cudaMemcpyAsync(out_host, d, sizeof(zkl_g1) * (cols + 1), cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(ctx, cudaFreeAsync(d, ctx->stream));
-    return sync_stream(ctx);
-}
-
-size_t zkl_hyrax_workspace_bytes(uint64_t D, uint64_t cols) {
-    if (!is_pow2(D) || !is_pow2(cols) || cols > D) return 0;
-    HxPlan h;
-    make_hx_plan(h, D, cols);
-    return h.total;
-}
-
-int zkl_hyrax_commit(zkl_ctx* ctx, const void* pp, uint64_t cols, zkl_vec S, uint64_t D, const zkl_fr* rho,
-                     zkl_g1* C_host) {
-    return run_hyrax_commit(ctx, pp, cols, S, D, rho, C_host);
-}
-
-int zkl_hyrax_prove_eval(zkl_ctx* ctx, zkl_vec S, uint64_t D, uint64_t cols, const zkl_fr* v, zkl_vec w_out,
-                         zkl_fr* y_host) {
-    return run_hyrax_eval(ctx, S, D, cols, v, w_out, y_host);
 }
 
 int zkl_ctx_set_async(zkl_ctx* ctx, int on) {
@@ -1634,6 +1171,7 @@ int zkl_ctx_profile_read(zkl_ctx* c, char* names, int name_len, float* ms, float
 int zkl_vec_import(zkl_ctx* ctx, const void* canon, int src_on_device, zkl_vec dst, int64_t* err_index) {
     int st;
     if ((st = check_ctx(ctx))) return st;
+    if ((st = check_idle(ctx))) return st;
     if (err_index) *err_index = -1;
     if (!canon) return set_err(ctx, ZKL_E_ARG, "null source");
     if ((st = check_vec(ctx, dst, dst.n, "dst"))) return st;
@@ -1672,6 +1210,7 @@ int zkl_vec_import_i64(zkl_ctx* ctx, const int64_t* x, zkl_vec dst) {
 int zkl_vec_import_pair(zkl_ctx* ctx, const int32_t* x, const int32_t* y, const zkl_fr* alpha_f, zkl_vec dst) {
     int st;
     if ((st = check_ctx(ctx))) return st;
+    if ((st = check_idle(ctx))) return st;
     if (!x || !y || !alpha_f) return set_err(ctx, ZKL_E_ARG, "null argument");
     if ((st = check_vec(ctx, dst, dst.n, "dst"))) return st;
     if (dst.n == 0) return ZKL_OK;
@@ -1721,6 +1260,7 @@ int zkl_table_create(zkl_ctx* ctx, zkl_vec T, void* mem, size_t mem_bytes, zkl_t
     if (!out) return ZKL_E_ARG;
     *out = nullptr;
     if ((st = check_ctx(ctx))) return st;
+    if ((st = check_idle(ctx))) return st;
     if (!is_pow2(T.n)) return set_err(ctx, ZKL_E_SHAPE, "N=%llu is not a power of two", (unsigned long long)T.n);
     if ((st = check_vec(ctx, T, T.n, "T"))) return st;
     const uint64_t N = T.n;
@@ -1772,6 +1312,7 @@ void zkl_table_destroy(zkl_table* t) { free(t); }
 int zkl_table_attach_pair(zkl_ctx* ctx, zkl_table* t, const int32_t* tx, const int32_t* ty, const zkl_fr* alpha_f) {
     int st;
     if ((st = check_ctx(ctx))) return st;
+    if ((st = check_idle(ctx))) return st;
     if (!t || !tx || !ty || !alpha_f) return set_err(ctx, ZKL_E_ARG, "null argument");
     if (fr_ge_r_host(*alpha_f)) return set_err(ctx, ZKL_E_NONCANONICAL, "alpha_f is not canonical");
     t->has_pair = 0;

@@ -116,6 +116,19 @@ __device__ __forceinline__ void atomic_min_i64(unsigned long long* p, uint64_t v
     atomicMin(p, (unsigned long long)v);
 }
 
+__device__ __forceinline__ fr fr_small(uint32_t v) {
+    fr x = fr_zero();
+    x.v[0] = v;
+    return fr_to_mont(x);
+}
+
+__device__ __forceinline__ zkl_fr to_canon(const fr& m) {
+    fr c = fr_from_mont(m);
+    zkl_fr z;
+    for (int l = 0; l < 8; ++l) z.w[l] = c.v[l];
+    return z;
+}
+
 // ------------------------------------------------------------------ device-side proof state
 // Scalars of one proof, Montgomery form, in the workspace.
 struct RoundDesc {

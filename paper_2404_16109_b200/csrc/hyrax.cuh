@@ -6,13 +6,22 @@
 // cols <= 2^13): one thread per (row, slice of 16 columns, 32-bit scalar chunk) keeps one Jacobian accumulator,
 // multiplies it by 16 per window and adds T_i[digit] for every column of its slice (64 mixed additions per scalar
 // in all, no buckets, no sort, no atomics); the partial sums are tree-reduced per (row, chunk), the chunks combined
-// by Horner (2^32 steps) and each row normalised once.  Included by api.cu.
+// by Horner (2^32 steps) and each row normalised once.  Included by hx_api.cu.
 #pragma once
 #include "g1.cuh"
-#include "kernels.cuh"
+#include "common.cuh"
 #include "sha256.cuh"
 
 namespace zkl {
+
+// canonical -> Montgomery for the evaluation point
+__global__ void k_hx_consts(const zkl_fr* __restrict__ in, int count, fr* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    fr x;
+    for (int l = 0; l < 8; ++l) x.v[l] = in[i].w[l];
+    out[i] = fr_to_mont(x);
+}
 
 constexpr int kHxThreads = 128;
 constexpr int kHxSlice = 16;     // columns per thread in the commit kernel

@@ -1246,19 +1246,6 @@ __global__ void k_reduce_rounds(const fr* __restrict__ partials, const RoundDesc
     }
 }
 
-__device__ __forceinline__ fr fr_small(uint32_t v) {
-    fr x = fr_zero();
-    x.v[0] = v;
-    return fr_to_mont(x);
-}
-
-__device__ __forceinline__ zkl_fr to_canon(const fr& m) {
-    fr c = fr_from_mont(m);
-    zkl_fr z;
-    for (int l = 0; l < 8; ++l) z.w[l] = c.v[l];
-    return z;
-}
-
 // Per-round constants that depend only on the challenges (a7), computed on the side stream at the start
 // of a proof: C_k = prod_{j<k} l_{d-j}(r_j), cl_t = alpha1 C_k l_c(t) (c = d - k), the inverse of
 // cl_1 = alpha1 C_k u_c (one batch inversion, one Fermat), the Lagrange basis L_t(r_k) on {0,1,2,3},

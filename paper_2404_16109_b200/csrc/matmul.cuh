@@ -6,9 +6,9 @@
 // multiply-adds, no modular reduction) and reduced once per column chunk -- about 10x cheaper than an Fr
 // multiplication, so the restrictions run near the HBM rate of reading A and B (4 B per entry).  The
 // log2(n)-round degree-2 sumcheck on (a, b) reuses the chunked-round scheme of the tlookup path.
-// Included by api.cu (one translation unit).
+// Included by mm_api.cu.
 #pragma once
-#include "kernels.cuh"
+#include "common.cuh"
 
 namespace zkl {
 

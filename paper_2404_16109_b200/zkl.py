@@ -261,9 +261,11 @@ class Context:
         self._check(lib().zkl_ctx_set_async(self.h, 1 if on else 0))
         self._async = bool(on)
 
-    def _defer(self, err, make=None):
+    def _defer(self, err, make=None, keep=None):
+        """`keep`: device buffers the library still reads at completion (e.g. prepare_pair's x, y for the range-miss
+        fallback inside zkl_ctx_wait) -- referenced here until wait() so that temporaries are not freed early."""
         dfr = Deferred(make) if make is not None else None
-        self._pending.append((err, dfr))
+        self._pending.append((err, dfr, keep))
         return dfr
 
     def wait(self):
@@ -271,9 +273,9 @@ class Context:
         st = lib().zkl_ctx_wait(self.h)
         pend, self._pending = self._pending, []
         if st:
-            idx = next((e.value for e, _ in pend if e is not None and e.value != -1), -1)
+            idx = next((e.value for e, _, _ in pend if e is not None and e.value != -1), -1)
             raise ZklError(st, idx, lib().zkl_last_error(self.h).decode(errors="replace"))
-        for _, dfr in pend:
+        for _, dfr, _ in pend:
             if dfr is not None:
                 dfr._resolve()
 
@@ -411,7 +413,7 @@ class Context:
                                             ctypes.byref(err))
         self._check(st, err.value)
         if self._async:
-            self._defer(err)
+            self._defer(err, keep=(tx, ty))
         return S, m
 
     # -- a4..a9

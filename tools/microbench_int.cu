@@ -1,0 +1,238 @@
+// Throughput-bound integer-pipe microbenchmark: the IMAD family, IADD3 and
+// the Fr multiplication of csrc/fr.cuh, each with many independent chains per thread and 16+ warps per SMSP so that
+// no result is waited on before ~32 other instructions have issued.  The loop bodies are checked in SASS
+// (tools/sass_count.py) before the numbers are trusted: one IMAD / IMAD.WIDE / IMAD.HI / IADD3 per asm statement.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o microbench_int tools/microbench_int.cu && ./microbench_int
+//
+// Output: one JSON line per kernel: lane-operations per second and per SM-clock (with the SM clock measured inside
+// the kernel from clock64 / globaltimer), and a final MEASURED_INT_PEAKS line.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../paper_2404_16109_b200/csrc/fr.cuh"
+
+using namespace zkl;
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); return 1; } } while (0)
+
+__device__ __forceinline__ uint64_t gtimer() { uint64_t t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }
+__device__ unsigned long long g_clk[4];
+
+#define CLK_BEGIN unsigned long long c0 = clock64(), t0 = gtimer();
+#define CLK_END                                                                                \
+    unsigned long long c1 = clock64(), t1 = gtimer();                                          \
+    if (blockIdx.x == 0 && threadIdx.x == 0) { g_clk[0] = c0; g_clk[1] = c1; g_clk[2] = t0; g_clk[3] = t1; }
+
+constexpr int kChains = 16;
+
+// 32-bit IMAD (mad.lo): 16 independent accumulators, multiplier/addend in registers
+__global__ void k_imad(uint32_t* out, int iters, uint32_t b, uint32_t c) {
+    uint32_t a[kChains];
+#pragma unroll
+    for (int k = 0; k < kChains; ++k) a[k] = threadIdx.x * 31 + k;
+    CLK_BEGIN
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < kChains; ++k) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[k]) : "r"(b), "r"(c));
+    }
+    CLK_END
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kChains; ++k) s += a[k];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// IMAD.HI (mad.hi): acc = hi(acc * b) + x
+__global__ void k_imadhi(uint32_t* out, int iters, uint32_t b, uint32_t c) {
+    uint32_t a[kChains];
+    const uint32_t x = threadIdx.x * 977u + c;
+#pragma unroll
+    for (int k = 0; k < kChains; ++k) a[k] = threadIdx.x * 31 + k;
+    CLK_BEGIN
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < kChains; ++k) asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(a[k]) : "r"(b), "r"(x));
+    }
+    CLK_END
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kChains; ++k) s += a[k];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// IMAD.WIDE.U32: 64-bit acc = lo(acc) * b + acc (one 32x32->64 product and a 64-bit add per instruction)
+__global__ void k_imadwide(unsigned long long* out, int iters, uint32_t b, uint32_t c) {
+    unsigned long long acc[kChains];
+#pragma unroll
+    for (int k = 0; k < kChains; ++k) acc[k] = threadIdx.x * 31 + k;
+    CLK_BEGIN
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < kChains; ++k)
+            asm volatile("{\n\t.reg .u32 lo, hi;\n\tmov.b64 {lo, hi}, %0;\n\tmad.wide.u32 %0, lo, %1, %0;\n\t}"
+                         : "+l"(acc[k]) : "r"(b));
+    }
+    CLK_END
+    unsigned long long s = 0;
+#pragma unroll
+    for (int k = 0; k < kChains; ++k) s += acc[k];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// the carry-chained lo/hi pair fr_mul is built from: (lo, hi) += x * b with carries (IMAD.WIDE.U32.X in SASS)
+__global__ void k_madc(uint32_t* out, int iters, uint32_t b, uint32_t c) {
+    uint32_t a[kChains];
+    const uint32_t x = threadIdx.x * 977u + c;
+#pragma unroll
+    for (int k = 0; k < kChains; ++k) a[k] = threadIdx.x * 31 + k;
+    CLK_BEGIN
+    for (int it = 0; it < iters; ++it) {
+        // 8 independent 2-word accumulators, each updated by one carry-chained mad.lo.cc / madc.hi pair
+#pragma unroll
+        for (int k = 0; k < kChains; k += 2)
+            asm volatile("mad.lo.cc.u32 %0, %2, %3, %0;\n\tmadc.hi.u32 %1, %2, %3, %1;"
+                         : "+r"(a[k]), "+r"(a[k + 1]) : "r"(x), "r"(b));
+    }
+    CLK_END
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kChains; ++k) s += a[k];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// IADD3 (alu pipe)
+__global__ void k_iadd3(uint32_t* out, int iters, uint32_t b, uint32_t c) {
+    uint32_t a[kChains];
+#pragma unroll
+    for (int k = 0; k < kChains; ++k) a[k] = threadIdx.x * 31 + k;
+    CLK_BEGIN
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < kChains; ++k) asm volatile("add.u32 %0, %0, %1;\n\tadd.u32 %0, %0, %2;" : "+r"(a[k]) : "r"(b), "r"(c));
+    }
+    CLK_END
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kChains; ++k) s ^= a[k];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// IMAD and IADD3 interleaved 1:1 (do the fma and alu pipes issue concurrently?)
+__global__ void k_mix(uint32_t* out, int iters, uint32_t b, uint32_t c) {
+    uint32_t a[kChains], z[kChains];
+#pragma unroll
+    for (int k = 0; k < kChains; ++k) { a[k] = threadIdx.x * 31 + k; z[k] = k; }
+    CLK_BEGIN
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < kChains; ++k) {
+            asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[k]) : "r"(b), "r"(c));
+            asm volatile("add.u32 %0, %0, %1;\n\tadd.u32 %0, %0, %2;" : "+r"(z[k]) : "r"(b), "r"(c));
+        }
+    }
+    CLK_END
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kChains; ++k) s += a[k] ^ z[k];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// FP64 FMA (DFMA), for reference
+__global__ void k_dfma(double* out, int iters, uint32_t b, uint32_t c) {
+    double a[kChains];
+    const double x = 1.0 + 1e-9 * b, y = 1e-12 * c;
+#pragma unroll
+    for (int k = 0; k < kChains; ++k) a[k] = threadIdx.x + k;
+    CLK_BEGIN
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < kChains; ++k) asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(a[k]) : "d"(x), "d"(y));
+    }
+    CLK_END
+    double s = 0;
+#pragma unroll
+    for (int k = 0; k < kChains; ++k) s += a[k];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// Fr multiplication throughput (csrc/fr.cuh): ILP independent products per thread
+template <int ILP>
+__global__ void k_frmul(fr* out, int iters, uint32_t b, uint32_t c) {
+    fr x[ILP];
+    fr y = fr_one();
+    y.v[0] ^= threadIdx.x ^ b;
+#pragma unroll
+    for (int k = 0; k < ILP; ++k) { x[k] = fr_r2(); x[k].v[1] ^= blockIdx.x * 977 + k + c; }
+    CLK_BEGIN
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < ILP; ++k) x[k] = fr_mul(x[k], y);
+    }
+    CLK_END
+    fr acc = x[0];
+#pragma unroll
+    for (int k = 1; k < ILP; ++k) acc = fr_add(acc, x[k]);
+    out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
+static double g_mhz;
+
+template <typename K, typename T>
+static int timeit(const char* name, K kern, T* buf, int blocks, int threads, int iters, double ops_per_iter_thread,
+                  double* gops_out) {
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+    kern<<<blocks, threads>>>(buf, iters / 10 + 1, 3u, 5u);   // warm-up (clocks up)
+    CK(cudaDeviceSynchronize());
+    float best = 1e30f;
+    for (int rep = 0; rep < 3; ++rep) {
+        CK(cudaEventRecord(e0));
+        kern<<<blocks, threads>>>(buf, iters, 3u, 5u);
+        CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        if (ms < best) best = ms;
+    }
+    unsigned long long h[4];
+    CK(cudaMemcpyFromSymbol(h, g_clk, sizeof(h)));
+    const double mhz = double(h[1] - h[0]) / double(h[3] - h[2]) * 1e3;
+    const double ops = (double)blocks * threads * iters * ops_per_iter_thread;
+    const double gops = ops / (best * 1e-3) / 1e9;
+    const double per_clk_sm = ops / (best * 1e-3) / (mhz * 1e6) / 148.0;
+    printf("{\"bench\": \"%s\", \"blocks\": %d, \"threads\": %d, \"ms\": %.3f, \"Gops\": %.2f, \"sm_mhz_in_kernel\": %.0f, "
+           "\"lane_ops_per_clk_per_sm\": %.2f}\n",
+           name, blocks, threads, best, gops, mhz, per_clk_sm);
+    if (gops_out) *gops_out = per_clk_sm;
+    g_mhz = mhz;
+    return 0;
+}
+
+int main() {
+    cudaDeviceProp pr;
+    CK(cudaGetDeviceProperties(&pr, 0));
+    printf("{\"device\": \"%s\", \"sm\": %d, \"cc\": \"%d.%d\"}\n", pr.name, pr.multiProcessorCount, pr.major, pr.minor);
+    void* buf;
+    CK(cudaMalloc(&buf, 64 << 20));
+    const int B = 148 * 8, T = 256, IT = 4096;
+    double imad, imadhi, imadw, madc, iadd, mix, dfma, fr1, fr2, fr4;
+    if (timeit("imad_lo", k_imad, (uint32_t*)buf, B, T, IT, kChains, &imad)) return 1;
+    if (timeit("imad_hi", k_imadhi, (uint32_t*)buf, B, T, IT, kChains, &imadhi)) return 1;
+    if (timeit("imad_wide", k_imadwide, (unsigned long long*)buf, B, T, IT, kChains, &imadw)) return 1;
+    if (timeit("madc_lo_hi_pair", k_madc, (uint32_t*)buf, B, T, IT, kChains / 2, &madc)) return 1;
+    if (timeit("iadd3", k_iadd3, (uint32_t*)buf, B, T, IT, 2 * kChains, &iadd)) return 1;
+    if (timeit("imad_plus_2iadd_mix(counting imad)", k_mix, (uint32_t*)buf, B, T, IT, kChains, &mix)) return 1;
+    if (timeit("dfma", k_dfma, (double*)buf, B, T, IT / 4, kChains, &dfma)) return 1;
+    if (timeit("frmul_ilp1", k_frmul<1>, (fr*)buf, 148 * 8, 256, 512, 1, &fr1)) return 1;
+    if (timeit("frmul_ilp2", k_frmul<2>, (fr*)buf, 148 * 8, 128, 512, 2, &fr2)) return 1;
+    if (timeit("frmul_ilp4", k_frmul<4>, (fr*)buf, 148 * 4, 128, 512, 4, &fr4)) return 1;
+    double frbest = fr1 > fr2 ? fr1 : fr2;
+    frbest = frbest > fr4 ? frbest : fr4;
+    printf("{\"MEASURED_INT_PEAKS\": {\"imad_lo_per_clk_sm\": %.2f, \"imad_hi_per_clk_sm\": %.2f, "
+           "\"imad_wide_per_clk_sm\": %.2f, \"madc_pair_per_clk_sm\": %.2f, \"iadd3_per_clk_sm\": %.2f, "
+           "\"dfma_per_clk_sm\": %.2f, \"frmul_per_clk_sm\": %.4f, \"frmul_G_per_s_at_1965MHz\": %.2f, "
+           "\"imad_wide_G_per_s_at_1965MHz\": %.1f}}\n",
+           imad, imadhi, imadw, madc, iadd, dfma, frbest, frbest * 148 * 1965e6 / 1e9, imadw * 148 * 1965e6 / 1e9);
+    return 0;
+}
