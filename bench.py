@@ -234,7 +234,6 @@ def main():
     ch = wl.chal
     chal = zkl.Context.challenges(ch.beta, ch.alpha1, ch.alpha2, ch.u, ch.r)
     xd, yd, txd, tyd = (t.to(dev) for t in (x, y, tx, ty))
-    S = ctx.vec(Dp)
     T = ctx.vec(N)
     tmem = ctx.table_mem(N)
     m = torch.empty(N, dtype=torch.int32, device=dev)
@@ -246,12 +245,13 @@ def main():
         ctx.import_pair(txs, tys, ch.alpha_f, T)
         tab = ctx.table(T, tmem)
         ctx.table_attach_pair(tab, txs, tys, ch.alpha_f)   # pair-range fast path of prepare_pair
+        # S stays virtual (only the table keys are kept, S_i = T_key)
         if not use_async:
-            ctx.prepare_pair(xs, ys, ch.alpha_f, D, tab, S, m)
-            return ctx.prove(S, D, tab, m, chal, args.variant)
+            ctx.prepare_pair(xs, ys, ch.alpha_f, D, tab, m=m, virtual_s=True)
+            return ctx.prove(None, D, tab, m, chal, args.variant)
         ctx.set_async(True)
-        ctx.prepare_pair(xs, ys, ch.alpha_f, D, tab, S, m)
-        pending = ctx.prove(S, D, tab, m, chal, args.variant)
+        ctx.prepare_pair(xs, ys, ch.alpha_f, D, tab, m=m, virtual_s=True)
+        pending = ctx.prove(None, D, tab, m, chal, args.variant)
         ctx.wait()
         ctx.set_async(False)
         return pending.result()
@@ -303,8 +303,8 @@ def main():
             ctx.import_pair(txd, tyd, ch.alpha_f, T)
             tab = ctx.table(T, tmem)
             ctx.table_attach_pair(tab, txd, tyd, ch.alpha_f)   # pair-range fast path of prepare_pair
-            ctx.prepare_pair(xd, yd, ch.alpha_f, D, tab, S, m)   # synchronous: the FS rounds are latency-bound,
-            return ctx.prove_fs(S, D, tab, m, seed, args.variant)   # a background histogram only slows them
+            ctx.prepare_pair(xd, yd, ch.alpha_f, D, tab, m=m, virtual_s=True)   # synchronous: a background
+            return ctx.prove_fs(None, D, tab, m, seed, args.variant)   # histogram only slows the FS rounds
 
         step_fs()
         torch.cuda.synchronize(dev)
@@ -408,7 +408,7 @@ def main():
            "vs_baseline": None, "dtype": "u32x8 (Fr, exact)", "data": "synthetic",
            "config": {"workload": WORKLOAD, "D": D, "N": N, "P": world, "D_local": Dp, "variant":
                       "paper" if args.variant == 0 else "logup", "parallelism": f"hypercube-top{world}",
-                      "l2": "inputs larger than L2 (X,Y int32 512 MiB; S 2 GiB)"},
+                      "l2": "inputs larger than L2 (X,Y int32 512 MiB; S virtual, keys 256 MiB, folded A,S 2 GiB)"},
            "e2e": {"value": D / (ms_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
            "gpu_launches": launches, "roofline": roofline, "clocks": clk.summary(),
            "kernel_ms_per_step": kernels, "kernel_ms_sum": step_ms_sum,

@@ -23,6 +23,15 @@
  *     2^(d-k) * (N/D) * tau = tau / 2^(k-n) to every g_k(t).  Cross-checked against
  *     the D-repeated Python tier in tests/test_oracle_c.py.
  *
+ * zko_tlookup_pair_stream (below) is the same computation for function / range lookups given as int32 pairs
+ * (S_i = x_i + alpha_f y_i, T_j = tx_j + alpha_f ty_j), in memory bounded for D = 2^30 (SURVEY.md §7 step 8,
+ * §8(d)): S is formed from (x_i, y_i) where it is used instead of being stored, A_i = 1/(beta + S_i) is
+ * recomputed per block of 2^s consecutive elements (Montgomery batch inversion per batch of blocks), and the first
+ * s rounds are evaluated block by block -- the pairs of round k inside an aligned block of 2^s elements fold into
+ * the same block, so each block's contribution to g_1..g_s is computed from its own elements alone, exactly as the
+ * unblocked loop computes it.  Vectors are materialised from round s+1 (D / 2^s elements).  Equality with
+ * zko_tlookup for every s is checked in tests/test_oracle_c.py.
+ *
  * Conventions: DESIGN.md §2 readings (coordinate 0 = MSB, j = x mod N, LSB-first
  * binding, g_k given at t = 0..3, weights (1, alpha1, alpha2)).
  * Threads: OpenMP over independent elements / pairs (sums reduced exactly mod r).
@@ -438,5 +447,283 @@ int zko_tlookup(uint64_t D, uint64_t N, const fe *S, const fe *T, const fe *chal
 done:
     free(m); free(A); free(Sv); free(E); free(B); free(Tv); free(Mv); free(E2); free(um); free(ks);
     free(A2); free(S2); free(Ed2);
+    return status;
+}
+
+/* ------------------------------------------------------------------ streaming tier (pair inputs) */
+
+/* canonical x + alpha_f y for int32 x, y (af_m: alpha_f in Montgomery form) -- as zko_pair_inputs */
+static fe pair_value(int32_t x, int32_t y, const fe *af_m) {
+    return fadd(fe_from_i64(x), from_m(fmul(*af_m, to_m(fe_from_i64(y)))));
+}
+
+/* the summand of Eq. tlookup-sumcheck at one point of the line, D side: A (alpha1 e (S + beta) + 1) */
+static fe d_term(fe a, fe sv, fe e, fe a1, fe beta) { return fmul(a, fadd(fmul(fmul(a1, e), fadd(sv, beta)), ONE_M)); }
+
+/* table side at one point of the line (PAPER variant / LOGUP variant) */
+static fe t_term(fe b, fe t, fe m, fe e, fe a2, fe beta, int variant) {
+    if (variant == 0) return fmul(b, fsub(fmul(fmul(a2, e), fadd(t, beta)), m));
+    return fsub(fmul(fmul(a2, e), fsub(fmul(b, fadd(t, beta)), m)), b);
+}
+
+/* one round on `len` materialised elements of A, S, E: direct sums at t = 0..3 into g, fold with rk into the
+ * first len/2 entries of the out arrays */
+static void d_round(const fe *A, const fe *S, const fe *E, uint64_t len, fe *An, fe *Sn, fe *En, fe rk, fe a1,
+                    fe beta, fe g[4]) {
+    uint64_t halfn = len / 2;
+    int nt = zko_num_threads();
+    fe *part = (fe *)calloc((size_t)nt * 4, sizeof(fe));
+    #pragma omp parallel
+    {
+        int tid = 0;
+#ifdef _OPENMP
+        tid = omp_get_thread_num();
+#endif
+        fe acc[4] = {fe_from_u64(0), fe_from_u64(0), fe_from_u64(0), fe_from_u64(0)};
+        #pragma omp for schedule(static)
+        for (int64_t y = 0; y < (int64_t)halfn; ++y) {
+            fe a0 = A[2 * y], s0 = S[2 * y], e0 = E[2 * y];
+            fe da = fsub(A[2 * y + 1], a0), ds = fsub(S[2 * y + 1], s0), de = fsub(E[2 * y + 1], e0);
+            fe at = a0, st = s0, et = e0;
+            for (int t = 0; t < 4; ++t) {
+                if (t > 0) { at = fadd(at, da); st = fadd(st, ds); et = fadd(et, de); }
+                acc[t] = fadd(acc[t], d_term(at, st, et, a1, beta));
+            }
+        }
+        for (int t = 0; t < 4; ++t) part[tid * 4 + t] = acc[t];
+    }
+    for (int q = 0; q < nt; ++q) for (int t = 0; t < 4; ++t) g[t] = fadd(g[t], part[q * 4 + t]);
+    free(part);
+    #pragma omp parallel for schedule(static)
+    for (int64_t y = 0; y < (int64_t)halfn; ++y) {
+        An[y] = fadd(A[2 * y], fmul(rk, fsub(A[2 * y + 1], A[2 * y])));
+        Sn[y] = fadd(S[2 * y], fmul(rk, fsub(S[2 * y + 1], S[2 * y])));
+        En[y] = fadd(E[2 * y], fmul(rk, fsub(E[2 * y + 1], E[2 * y])));
+    }
+}
+
+/*
+ * x, y: D int32 (S_i = x_i + alpha_f y_i); tx, ty: N int32 (T_j = tx_j + alpha_f ty_j); alpha_f, chal canonical
+ * (chal as in zko_tlookup).  s: rounds streamed block by block (0 <= s <= log2 D).  Outputs as zko_tlookup
+ * (m_out, B_out may be NULL).  Errors: E_SHAPE, E_DUP_TABLE(j), E_NOT_IN_TABLE(smallest i), E_DIV_ZERO_T(j),
+ * E_DIV_ZERO_S(smallest i), E_OOM.
+ */
+int zko_tlookup_pair_stream(uint64_t D, uint64_t N, const int32_t *x, const int32_t *y, const int32_t *tx,
+                            const int32_t *ty, const fe *alpha_f, const fe *chal, int variant, int s,
+                            uint32_t *m_out, fe *B_out, fe *evals, fe *finals, int64_t *err_index) {
+    init();
+    *err_index = -1;
+    if (!is_pow2(D) || !is_pow2(N) || N > D) return ZKO_E_SHAPE;
+    int d = log2u(D), n = log2u(N);
+    if (s < 0 || s > d) return ZKO_E_SHAPE;
+    fe beta = to_m(chal[0]), a1 = to_m(chal[1]), a2 = to_m(chal[2]);
+    const fe *u = chal + 3, *r = chal + 3 + d;
+    fe af = to_m(*alpha_f);
+    int nt = zko_num_threads();
+    int status = ZKO_OK;
+    uint64_t Ds = D >> s;                       /* materialised length after the streamed rounds */
+    fe *T = malloc(N * sizeof(fe)), *B = malloc(N * sizeof(fe)), *Tv = malloc(N * sizeof(fe));
+    fe *Mv = malloc(N * sizeof(fe)), *E2 = malloc(N * sizeof(fe)), *um = malloc((d + 1) * sizeof(fe));
+    keyed *ks = malloc(N * sizeof(keyed));
+    uint32_t *m = calloc(N, sizeof(uint32_t)), *mth = calloc((size_t)nt * N, sizeof(uint32_t));
+    fe *dg = calloc((size_t)d * 4, sizeof(fe)), *tg = calloc((size_t)d * 4, sizeof(fe));
+    int h = d / 2;                              /* e~(u, x) = e~(u[0:d-h], x >> h) e~(u[d-h:], x mod 2^h) */
+    fe *Ehi = malloc(((size_t)1 << (d - h)) * sizeof(fe)), *Elo = malloc(((size_t)1 << h) * sizeof(fe));
+    fe *A3 = malloc(Ds * sizeof(fe)), *S3 = malloc(Ds * sizeof(fe)), *E3 = malloc(Ds * sizeof(fe));
+    fe *A4 = malloc((Ds / 2 + 1) * sizeof(fe)), *S4 = malloc((Ds / 2 + 1) * sizeof(fe)), *E4 = malloc((Ds / 2 + 1) * sizeof(fe));
+    int64_t *miss_th = malloc(nt * sizeof(int64_t)), *zero_th = malloc(nt * sizeof(int64_t));
+    fe *gth = calloc((size_t)nt * (s + 1) * 4, sizeof(fe));
+    if (!T || !B || !Tv || !Mv || !E2 || !um || !ks || !m || !mth || !dg || !tg || !Ehi || !Elo || !A3 || !S3 || !E3 ||
+        !A4 || !S4 || !E4 || !miss_th || !zero_th || !gth) { status = ZKO_E_OOM; goto done; }
+
+    /* T, distinctness (smallest later duplicate index), as zko_tlookup */
+    for (uint64_t j = 0; j < N; ++j) { T[j] = pair_value(tx[j], ty[j], &af); ks[j].v = T[j]; ks[j].idx = (uint32_t)j; }
+    qsort(ks, N, sizeof(keyed), cmp_keyed);
+    {
+        int64_t dup = -1;
+        for (uint64_t j = 1; j < N; ++j)
+            if (fe_eq(ks[j].v, ks[j - 1].v) && (dup < 0 || ks[j].idx < dup)) dup = ks[j].idx;
+        if (dup >= 0) { *err_index = dup; status = ZKO_E_DUP_TABLE; goto done; }
+    }
+    /* m_j = #{i : S_i = T_j} (Eq. hab22-coefs), binary search in the sorted table; per-thread counts */
+    for (int t = 0; t < nt; ++t) miss_th[t] = -1;
+    #pragma omp parallel
+    {
+        int tid = 0;
+#ifdef _OPENMP
+        tid = omp_get_thread_num();
+#endif
+        uint32_t *mc = mth + (size_t)tid * N;
+        #pragma omp for schedule(static)
+        for (int64_t i = 0; i < (int64_t)D; ++i) {
+            fe sv = pair_value(x[i], y[i], &af);
+            uint64_t lo = 0, hi = N;
+            while (lo < hi) {
+                uint64_t mid = (lo + hi) / 2;
+                if (cmp_fe(&ks[mid].v, &sv) < 0) lo = mid + 1; else hi = mid;
+            }
+            if (lo < N && fe_eq(ks[lo].v, sv)) mc[ks[lo].idx]++;
+            else if (miss_th[tid] < 0) miss_th[tid] = i;   /* static schedule: increasing i per thread */
+        }
+    }
+    {
+        int64_t miss = -1;
+        for (int t = 0; t < nt; ++t) if (miss_th[t] >= 0 && (miss < 0 || miss_th[t] < miss)) miss = miss_th[t];
+        if (miss >= 0) { *err_index = miss; status = ZKO_E_NOT_IN_TABLE; goto done; }
+    }
+    for (int t = 0; t < nt; ++t) for (uint64_t j = 0; j < N; ++j) m[j] += mth[(size_t)t * N + j];
+    if (m_out) memcpy(m_out, m, N * sizeof(uint32_t));
+    /* B (Eq. hab22-invs); beta + T_j = 0 first */
+    for (uint64_t j = 0; j < N; ++j) {
+        Tv[j] = fadd(beta, to_m(T[j]));
+        if (fe_is_zero(Tv[j])) { *err_index = (int64_t)j; status = ZKO_E_DIV_ZERO_T; goto done; }
+    }
+    batch_inverse(B, Tv, N);
+    if (variant == 1) for (uint64_t j = 0; j < N; ++j) B[j] = fmul(B[j], to_m(fe_from_u64(m[j])));
+    if (B_out) for (uint64_t j = 0; j < N; ++j) B_out[j] = from_m(B[j]);
+
+    /* ---- table side, every round (N-sized vectors, weight rule of DESIGN.md §5 a8) */
+    for (uint64_t j = 0; j < N; ++j) { Tv[j] = to_m(T[j]); Mv[j] = to_m(fe_from_u64(m[j])); }
+    for (int c = 0; c < d; ++c) um[c] = to_m(u[c]);
+    eq_table(E2, um + (d - n), n);
+    {
+        fe half = finv(to_m(fe_from_u64(2)));
+        fe tau = fe_from_u64(0), tau_scale = ONE_M;
+        uint64_t tlen = N;
+        if (n == 0) tau = t_term(B[0], Tv[0], Mv[0], E2[0], a2, beta, variant);
+        for (int k = 1; k <= d; ++k) {
+            fe *g = tg + (size_t)(k - 1) * 4;
+            if (k <= n) {
+                uint64_t th = tlen / 2;
+                for (uint64_t yy = 0; yy < th; ++yy) {
+                    fe b0 = B[2 * yy], t0 = Tv[2 * yy], m0 = Mv[2 * yy], e0 = E2[2 * yy];
+                    fe db = fsub(B[2 * yy + 1], b0), dt = fsub(Tv[2 * yy + 1], t0);
+                    fe dm = fsub(Mv[2 * yy + 1], m0), de = fsub(E2[2 * yy + 1], e0);
+                    fe bt = b0, ttv = t0, mt = m0, et = e0;
+                    for (int t = 0; t < 4; ++t) {
+                        if (t > 0) { bt = fadd(bt, db); ttv = fadd(ttv, dt); mt = fadd(mt, dm); et = fadd(et, de); }
+                        g[t] = fadd(g[t], t_term(bt, ttv, mt, et, a2, beta, variant));
+                    }
+                }
+                fe rk = to_m(r[k - 1]);
+                for (uint64_t yy = 0; yy < th; ++yy) {
+                    B[yy] = fadd(B[2 * yy], fmul(rk, fsub(B[2 * yy + 1], B[2 * yy])));
+                    Tv[yy] = fadd(Tv[2 * yy], fmul(rk, fsub(Tv[2 * yy + 1], Tv[2 * yy])));
+                    Mv[yy] = fadd(Mv[2 * yy], fmul(rk, fsub(Mv[2 * yy + 1], Mv[2 * yy])));
+                    E2[yy] = fadd(E2[2 * yy], fmul(rk, fsub(E2[2 * yy + 1], E2[2 * yy])));
+                }
+                tlen = th;
+                if (k == n) tau = t_term(B[0], Tv[0], Mv[0], E2[0], a2, beta, variant);
+            } else {
+                tau_scale = fmul(tau_scale, half);
+                fe c = fmul(tau, tau_scale);
+                for (int t = 0; t < 4; ++t) g[t] = c;
+            }
+        }
+    }
+
+    /* ---- D side: rounds 1..s block by block, A recomputed per batch of blocks */
+    eq_table(Ehi, um, d - h);
+    eq_table(Elo, um + (d - h), h);
+    for (int t = 0; t < nt; ++t) zero_th[t] = -1;
+    {
+        const uint64_t bs = 1ULL << s;                                   /* block length */
+        const uint64_t nb = Ds;                                          /* blocks */
+        const uint64_t per = bs >= 4096 ? 1 : 4096 / bs;                 /* blocks per inversion batch */
+        const uint64_t nbatch = (nb + per - 1) / per;
+        fe rkm[64];
+        for (int k = 1; k <= s; ++k) rkm[k] = to_m(r[k - 1]);
+        #pragma omp parallel
+        {
+            int tid = 0;
+#ifdef _OPENMP
+            tid = omp_get_thread_num();
+#endif
+            fe *acc = gth + (size_t)tid * (s + 1) * 4;
+            uint64_t blen = per * bs;
+            fe *xs = malloc(blen * sizeof(fe)), *sv = malloc(blen * sizeof(fe)), *av = malloc(blen * sizeof(fe));
+            fe *ev = malloc(bs * sizeof(fe));
+            #pragma omp for schedule(static)
+            for (int64_t q = 0; q < (int64_t)nbatch; ++q) {
+                uint64_t b0 = (uint64_t)q * per, b1 = b0 + per < nb ? b0 + per : nb;
+                uint64_t i0 = b0 * bs, cnt = (b1 - b0) * bs;
+                for (uint64_t k = 0; k < cnt; ++k) {
+                    sv[k] = to_m(pair_value(x[i0 + k], y[i0 + k], &af));
+                    xs[k] = fadd(beta, sv[k]);
+                    if (fe_is_zero(xs[k]) && zero_th[tid] < 0) zero_th[tid] = (int64_t)(i0 + k);
+                }
+                /* A = 1/(beta + S) for the batch: prefix products, one Fermat inversion, backward pass */
+                fe p = ONE_M;
+                for (uint64_t k = 0; k < cnt; ++k) { av[k] = p; if (!fe_is_zero(xs[k])) p = fmul(p, xs[k]); }
+                fe iv = finv(p);
+                for (uint64_t k = cnt; k-- > 0;) {
+                    if (fe_is_zero(xs[k])) { av[k] = fe_from_u64(0); continue; }
+                    av[k] = fmul(av[k], iv);
+                    iv = fmul(iv, xs[k]);
+                }
+                for (uint64_t b = b0; b < b1; ++b) {
+                    fe *ab = av + (b - b0) * bs, *sb = sv + (b - b0) * bs;
+                    for (uint64_t k = 0; k < bs; ++k) {
+                        uint64_t i = b * bs + k;
+                        ev[k] = fmul(Ehi[i >> h], Elo[i & ((1ULL << h) - 1)]);
+                    }
+                    uint64_t len = bs;
+                    for (int k = 1; k <= s; ++k) {
+                        fe *g = acc + (size_t)k * 4;
+                        for (uint64_t yy = 0; yy < len / 2; ++yy) {
+                            fe a0 = ab[2 * yy], s0 = sb[2 * yy], e0 = ev[2 * yy];
+                            fe da = fsub(ab[2 * yy + 1], a0), ds = fsub(sb[2 * yy + 1], s0), de = fsub(ev[2 * yy + 1], e0);
+                            fe at = a0, st = s0, et = e0;
+                            for (int t = 0; t < 4; ++t) {
+                                if (t > 0) { at = fadd(at, da); st = fadd(st, ds); et = fadd(et, de); }
+                                g[t] = fadd(g[t], d_term(at, st, et, a1, beta));
+                            }
+                        }
+                        for (uint64_t yy = 0; yy < len / 2; ++yy) {
+                            ab[yy] = fadd(ab[2 * yy], fmul(rkm[k], fsub(ab[2 * yy + 1], ab[2 * yy])));
+                            sb[yy] = fadd(sb[2 * yy], fmul(rkm[k], fsub(sb[2 * yy + 1], sb[2 * yy])));
+                            ev[yy] = fadd(ev[2 * yy], fmul(rkm[k], fsub(ev[2 * yy + 1], ev[2 * yy])));
+                        }
+                        len /= 2;
+                    }
+                    A3[b] = ab[0];
+                    S3[b] = sb[0];
+                    E3[b] = ev[0];
+                }
+            }
+            free(xs); free(sv); free(av); free(ev);
+        }
+    }
+    {
+        int64_t z = -1;
+        for (int t = 0; t < nt; ++t) if (zero_th[t] >= 0 && (z < 0 || zero_th[t] < z)) z = zero_th[t];
+        if (z >= 0) { *err_index = z; status = ZKO_E_DIV_ZERO_S; goto done; }
+    }
+    for (int k = 1; k <= s; ++k)
+        for (int t = 0; t < nt; ++t)
+            for (int q = 0; q < 4; ++q) dg[(k - 1) * 4 + q] = fadd(dg[(k - 1) * 4 + q], gth[((size_t)t * (s + 1) + k) * 4 + q]);
+    /* ---- rounds s+1..d on the materialised vectors */
+    {
+        fe *Ac = A3, *Sc = S3, *Ec = E3, *An = A4, *Sn = S4, *En = E4;
+        uint64_t len = Ds;
+        for (int k = s + 1; k <= d; ++k) {
+            d_round(Ac, Sc, Ec, len, An, Sn, En, to_m(r[k - 1]), a1, beta, dg + (size_t)(k - 1) * 4);
+            fe *t0 = Ac; Ac = An; An = t0;
+            t0 = Sc; Sc = Sn; Sn = t0;
+            t0 = Ec; Ec = En; En = t0;
+            len /= 2;
+        }
+        finals[0] = from_m(Ac[0]);
+        finals[1] = from_m(Sc[0]);
+    }
+    finals[2] = from_m(B[0]);
+    finals[3] = from_m(Tv[0]);
+    finals[4] = from_m(Mv[0]);
+    for (int k = 0; k < d; ++k)
+        for (int t = 0; t < 4; ++t) evals[k * 4 + t] = from_m(fadd(dg[k * 4 + t], tg[k * 4 + t]));
+done:
+    free(T); free(B); free(Tv); free(Mv); free(E2); free(um); free(ks); free(m); free(mth); free(dg); free(tg);
+    free(Ehi); free(Elo); free(A3); free(S3); free(E3); free(A4); free(S4); free(E4); free(miss_th); free(zero_th);
+    free(gth);
     return status;
 }

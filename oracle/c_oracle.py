@@ -45,6 +45,9 @@ def lib():
                                      P, P, P, P, P, P, P, P, P]
         _lib.zko_tlookup.restype = ctypes.c_int
         _lib.zko_pair_inputs.argtypes = [ctypes.c_uint64, P, P, P, P]
+        _lib.zko_tlookup_pair_stream.argtypes = [ctypes.c_uint64, ctypes.c_uint64, P, P, P, P, P, P, ctypes.c_int,
+                                                 ctypes.c_int, P, P, P, P, P]
+        _lib.zko_tlookup_pair_stream.restype = ctypes.c_int
         _lib.zko_int_inputs.argtypes = [ctypes.c_uint64, P, P]
         for f in ("zko_fr_mul", "zko_fr_add", "zko_fr_sub"):
             getattr(_lib, f).argtypes = [P, P, P]
@@ -164,3 +167,26 @@ def sumcheck(A: np.ndarray, S: np.ndarray, B: np.ndarray, T: np.ndarray, m: np.n
     if st:
         raise OracleError(st, err.value)
     return Result(m, None, None, ev[:d * 4], fin)
+
+
+def prove_pair_stream(x, y, tx, ty, alpha_f: int, chal: np.ndarray, variant: int = 0, s: int = 4,
+                      want_B: bool = True) -> Result:
+    """The streaming tier (zko_tlookup_pair_stream): S_i = x_i + alpha_f y_i, T_j = tx_j + alpha_f ty_j (int32),
+    first s rounds evaluated per aligned block of 2^s elements, memory ~ (D / 2^s) * 192 B + 8 B per lookup."""
+    x = np.ascontiguousarray(x, dtype=np.int32)
+    y = np.ascontiguousarray(y, dtype=np.int32)
+    tx = np.ascontiguousarray(tx, dtype=np.int32)
+    ty = np.ascontiguousarray(ty, dtype=np.int32)
+    D, N = x.shape[0], tx.shape[0]
+    d = D.bit_length() - 1
+    af = ints_to_limbs([alpha_f % R])
+    m = np.zeros(N, dtype=np.uint32)
+    B = np.zeros((N, 4), dtype=np.uint64) if want_B else None
+    ev = np.zeros((max(d, 1) * 4, 4), dtype=np.uint64)
+    fin = np.zeros((5, 4), dtype=np.uint64)
+    err = ctypes.c_int64(-1)
+    st = lib().zko_tlookup_pair_stream(D, N, _p(x), _p(y), _p(tx), _p(ty), _p(af), _p(chal), variant, s, _p(m),
+                                       _p(B), _p(ev), _p(fin), ctypes.byref(err))
+    if st:
+        raise OracleError(st, err.value)
+    return Result(m, None, B, ev[:d * 4], fin)

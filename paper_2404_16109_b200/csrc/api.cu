@@ -79,7 +79,7 @@ struct Plan {
     int hist_rows;
     // workspace offsets
     size_t o_out, o_sc, o_err, o_rounds, o_jobs, o_chal, o_part, o_tpart, o_tnb, o_rank, o_gath, o_repl, o_tsum,
-        o_fin, o_tfin, o_gfin, o_rc, o_fs, o_small, o_derived, o_arena, o_hist, o_keys, o_tot, o_totinv, o_A, o_A1, o_S1, o_A2, o_S2, o_tB, o_tX, o_tM,
+        o_fin, o_tfin, o_gfin, o_rc, o_fs, o_small, o_Sv, o_derived, o_arena, o_hist, o_keys, o_tot, o_totinv, o_A, o_A1, o_S1, o_A2, o_S2, o_tB, o_tX, o_tM,
         o_tE, o_twk, o_tBaos, o_chA, o_chS, total;
 };
 
@@ -236,6 +236,8 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
     p.o_rc = take(sizeof(RoundConst) * kMaxRounds);
     p.o_fs = take(sizeof(FsState));
     p.o_small = take(soa_bytes(std::min<uint64_t>(p.Dp, kInvTile)));
+    // a virtual S materialised from the keys where a kernel reads the vector itself (D_local <= 2^18, see run_proof)
+    p.o_Sv = take(soa_bytes(p.Dp <= 2 * kChunkMaxElems ? p.Dp : 4));
     p.o_derived = take(sizeof(zkl_fr) * (3 + 2 * kMaxRounds));
     p.o_arena = take(sizeof(fr) * p.arena);
     p.o_tot = take(soa_bytes(p.ntiles));
@@ -435,7 +437,15 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
     Plan p;
     make_plan(p, D, N, ctx->nranks, ctx->rank, a.prove_mode, a.ch->u);
     if ((st = need_ws(ctx, p))) return st;
-    if ((st = check_vec(ctx, a.S, p.Dp, "S_local"))) return st;
+    // keys of the preceding prepare on this S (or virtual S) and table: A_i = B_key, S_i = T_key by gathers
+    const bool virt = a.prove_mode && a.S.limbs == nullptr;
+    const bool keys_ok = a.prove_mode && ctx->prep_valid && ctx->prep_S == a.S.limbs && ctx->prep_n == p.Dp &&
+                         ctx->prep_table == a.table;
+    if (virt && !keys_ok)
+        return set_err(ctx, ZKL_E_ARG, "S_local is virtual (NULL): it needs the keys of the preceding "
+                                       "zkl_tlookup_prepare_pair on this context, table and D");
+    if (!virt && (st = check_vec(ctx, a.S, p.Dp, "S_local"))) return st;
+    if (virt && a.force_inversion) return set_err(ctx, ZKL_E_STATE, "internal: inversion fallback on a virtual S");
     if (!a.prove_mode) {
         if ((st = check_vec(ctx, a.A_in, p.Dp, "A_local"))) return st;
         if ((st = check_vec(ctx, a.B_in, N, "B"))) return st;
@@ -530,6 +540,16 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
     uint32_t* Abuf = a.prove_mode ? (a.A_out.limbs ? a.A_out.limbs : at<uint32_t>(ctx, p.o_A)) : nullptr;
     const uint32_t* A1in = a.prove_mode ? Abuf : a.A_in.limbs;
     const uint32_t* S1in = a.S.limbs;
+    const int kend_rounds = p.kc ? p.kc : p.k0;   // k_round launches for rounds < kend_rounds
+    // round 2 gathers A and S from the keys again (neither is materialised) when it is a multi-block k_round launch
+    const bool r2_gather = gather && keys_ok && kend_rounds > 2;
+    if (virt && !r2_gather) {
+        // D_local <= 2^18 (the one-CTA prove or the chunked rounds read the vectors themselves): S_i = T_key
+        uint32_t* Sv = at<uint32_t>(ctx, p.o_Sv);
+        LAUNCH(ctx, k_s_from_keys, grid_for(p.Dp, 256), 256, 0, s, at<uint32_t>(ctx, p.o_keys), p.Dp, N,
+               a.table->Taos, Sv);
+        S1in = Sv;
+    }
     const uint64_t errS_off = (uint64_t)p.rank * p.Dp;
     const size_t tail_smem = (2 * kTailMax + 4 * kTailThreads) * sizeof(fr) + 5 * (kTailThreads / 32) * sizeof(fr);
     int rounds_nb0 = -1;   // round-1 partial rows written by the inversion (prove mode)
@@ -541,12 +561,28 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
         if (gather) {
             // a4 + a5 through the table: A_i = B_j(i), one block per 4096-element tile (partial row = tile)
             TableView tv{a.table->T, a.table->Taos, a.table->slots, a.table->Skeys, a.table->N, a.table->slot_mask};
-            if (ctx->prep_S == a.S.limbs && ctx->prep_n == p.Dp && ctx->prep_table == a.table) {
-                // keys from the preceding prepare on this S (each still verified against T)
-                LAUNCH(ctx, k_gather_keys_round1, (unsigned)p.ntiles, kInvThreads, 0, s, a.S.limbs, p.Dp,
-                       at<uint32_t>(ctx, p.o_keys), N, at<uint4>(ctx, p.o_tBaos), Abuf,
-                       arena + p.rd[0].elo_off, arena + p.rd[0].ehi_off, partials + p.rd[0].part_base,
-                       (int)p.ntiles, err + 2);
+            if (keys_ok) {
+                // keys from the preceding prepare: A_i = B_key, S_i = T_key from the (B, T) records; a materialised S
+                // is verified against T_key.  A is written only if the caller wants it or round 2 reads it.
+                uint32_t* Aw = a.A_out.limbs ? a.A_out.limbs : (r2_gather ? nullptr : Abuf);
+                const bool verify = !virt;
+                const uint32_t* keys = at<uint32_t>(ctx, p.o_keys);
+                const uint4* TB = at<uint4>(ctx, p.o_tBaos);
+                const fr *elo1 = arena + p.rd[0].elo_off, *ehi1 = arena + p.rd[0].ehi_off;
+                fr* part1 = partials + p.rd[0].part_base;
+                const unsigned nb1 = (unsigned)p.ntiles;
+                if (verify && Aw)
+                    LAUNCH(ctx, (k_round1_keys<true, true>), nb1, kInvThreads, 0, s, a.S.limbs, p.Dp, keys, N, TB, Aw,
+                           elo1, ehi1, part1, (int)p.ntiles, err + 2);
+                else if (verify)
+                    LAUNCH(ctx, (k_round1_keys<true, false>), nb1, kInvThreads, 0, s, a.S.limbs, p.Dp, keys, N, TB,
+                           Aw, elo1, ehi1, part1, (int)p.ntiles, err + 2);
+                else if (Aw)
+                    LAUNCH(ctx, (k_round1_keys<false, true>), nb1, kInvThreads, 0, s, S1in, p.Dp, keys, N, TB, Aw,
+                           elo1, ehi1, part1, (int)p.ntiles, err + 2);
+                else
+                    LAUNCH(ctx, (k_round1_keys<false, false>), nb1, kInvThreads, 0, s, S1in, p.Dp, keys, N, TB, Aw,
+                           elo1, ehi1, part1, (int)p.ntiles, err + 2);
             } else {
                 LAUNCH(ctx, k_gather_round1, (unsigned)p.ntiles, kInvThreads, 0, s, a.S.limbs, p.Dp, tv,
                        at<uint4>(ctx, p.o_tBaos), Abuf, arena + p.rd[0].elo_off, arena + p.rd[0].ehi_off,
@@ -585,7 +621,6 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
         }
         const uint32_t *cA = A1in, *cS = S1in;
         uint64_t len = p.Dp;
-        const int kend_rounds = p.kc ? p.kc : p.k0;   // k_round launches for rounds < kend_rounds
         for (int k = a.prove_mode ? 2 : 1; k < kend_rounds; ++k) {
             const RoundDesc& r = p.rd[k - 1];
             fr* part = partials + r.part_base;
@@ -596,7 +631,16 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
                 const bool odd = (k & 1) == 0;   // k = 2 -> buffers 1
                 uint32_t* nA = at<uint32_t>(ctx, odd ? p.o_A1 : p.o_A2);
                 uint32_t* nS = at<uint32_t>(ctx, odd ? p.o_S1 : p.o_S2);
-                if (r.direct_h1)
+                if (k == 2 && r2_gather) {
+                    const uint32_t* keys = at<uint32_t>(ctx, p.o_keys);
+                    const uint4* TB = at<uint4>(ctx, p.o_tBaos);
+                    if (r.direct_h1)
+                        LAUNCH(ctx, (k_round<true, true, true>), r.nblocks, kRoundThreads, 0, s, nullptr, nullptr, len,
+                               nA, nS, sc, k, arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, part, keys, TB);
+                    else
+                        LAUNCH(ctx, (k_round<true, false, true>), r.nblocks, kRoundThreads, 0, s, nullptr, nullptr,
+                               len, nA, nS, sc, k, arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, part, keys, TB);
+                } else if (r.direct_h1)
                     LAUNCH(ctx, (k_round<true, true>), r.nblocks, kRoundThreads, 0, s, cA, cS, len, nA, nS, sc, k,
                            arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, part);
                 else
@@ -731,7 +775,13 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
     Plan p;
     make_plan(p, D, N, 1, 0, true, u1.data(), true);
     if ((st = need_ws(ctx, p))) return st;
-    if ((st = check_vec(ctx, S, p.Dp, "S_local"))) return st;
+    const bool virt = S.limbs == nullptr;
+    const bool keys_ok = ctx->prep_valid && ctx->prep_S == S.limbs && ctx->prep_n == p.Dp && ctx->prep_table == table;
+    if (virt && !keys_ok)
+        return set_err(ctx, ZKL_E_ARG, "S_local is virtual (NULL): it needs the keys of the preceding "
+                                       "zkl_tlookup_prepare_pair on this context, table and D");
+    if (virt && force_inversion) return set_err(ctx, ZKL_E_STATE, "internal: inversion fallback on a virtual S");
+    if (!virt && (st = check_vec(ctx, S, p.Dp, "S_local"))) return st;
     if (A_out.limbs && (st = check_vec(ctx, A_out, p.Dp, "A_local_out"))) return st;
     if (B_out.limbs && (st = check_vec(ctx, B_out, N, "B_out"))) return st;
     cudaStream_t s = ctx->stream;
@@ -795,16 +845,38 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
     // ---- round 1: A (gather through the prepared index, or inversion) + the round-1 sums
     uint32_t* Abuf = A_out.limbs ? A_out.limbs : at<uint32_t>(ctx, p.o_A);
     const bool gather = !p.small && !force_inversion;
+    const bool r2_gather = gather && keys_ok && p.d >= 2;   // round 2 gathers A, S from the keys again
+    const uint32_t* Sin = S.limbs;
+    if (virt && !r2_gather) {   // D_local < 4096: the small path reads S itself
+        uint32_t* Sv = at<uint32_t>(ctx, p.o_Sv);
+        LAUNCH(ctx, k_s_from_keys, grid_for(p.Dp, 256), 256, 0, s, at<uint32_t>(ctx, p.o_keys), p.Dp, N, table->Taos,
+               Sv);
+        Sin = Sv;
+    }
     int h01 = 1;
     if (gather) {
         LAUNCH(ctx, k_pack_tb, grid_for(N, 256), 256, 0, s, table->T, tB, N, at<uint4>(ctx, p.o_tBaos));
         TableView tv{table->T, table->Taos, table->slots, table->Skeys, table->N, table->slot_mask};
-        if (ctx->prep_S == S.limbs && ctx->prep_n == p.Dp && ctx->prep_table == table)
-            LAUNCH(ctx, k_gather_keys_round1, (unsigned)p.ntiles, kInvThreads, 0, s, S.limbs, p.Dp,
-                   at<uint32_t>(ctx, p.o_keys), N, at<uint4>(ctx, p.o_tBaos), Abuf,
-                   arena + p.rd[0].elo_off, arena + p.rd[0].ehi_off, partials + p.rd[0].part_base, (int)p.ntiles,
-                   err + 2);
-        else
+        if (keys_ok) {
+            uint32_t* Aw = A_out.limbs ? A_out.limbs : (r2_gather ? nullptr : Abuf);
+            const uint32_t* keys = at<uint32_t>(ctx, p.o_keys);
+            const uint4* TB = at<uint4>(ctx, p.o_tBaos);
+            const fr *elo1 = arena + p.rd[0].elo_off, *ehi1 = arena + p.rd[0].ehi_off;
+            fr* part1 = partials + p.rd[0].part_base;
+            const unsigned nb1 = (unsigned)p.ntiles;
+            if (!virt && Aw)
+                LAUNCH(ctx, (k_round1_keys<true, true>), nb1, kInvThreads, 0, s, S.limbs, p.Dp, keys, N, TB, Aw, elo1,
+                       ehi1, part1, (int)p.ntiles, err + 2);
+            else if (!virt)
+                LAUNCH(ctx, (k_round1_keys<true, false>), nb1, kInvThreads, 0, s, S.limbs, p.Dp, keys, N, TB, Aw, elo1,
+                       ehi1, part1, (int)p.ntiles, err + 2);
+            else if (Aw)
+                LAUNCH(ctx, (k_round1_keys<false, true>), nb1, kInvThreads, 0, s, Sin, p.Dp, keys, N, TB, Aw, elo1,
+                       ehi1, part1, (int)p.ntiles, err + 2);
+            else
+                LAUNCH(ctx, (k_round1_keys<false, false>), nb1, kInvThreads, 0, s, Sin, p.Dp, keys, N, TB, Aw, elo1,
+                       ehi1, part1, (int)p.ntiles, err + 2);
+        } else
             LAUNCH(ctx, k_gather_round1, (unsigned)p.ntiles, kInvThreads, 0, s, S.limbs, p.Dp, tv,
                    at<uint4>(ctx, p.o_tBaos), Abuf, arena + p.rd[0].elo_off, arena + p.rd[0].ehi_off,
                    partials + p.rd[0].part_base, (int)p.ntiles, err + 2);
@@ -817,12 +889,12 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
                 return st;
     } else {
         // small D: A by one batch inversion, round 1 summed directly from A and S
-        LAUNCH(ctx, k_add_beta, grid_for(p.Dp, 256), 256, 0, s, S.limbs, p.Dp, sc, at<uint32_t>(ctx, p.o_small), err);
+        LAUNCH(ctx, k_add_beta, grid_for(p.Dp, 256), 256, 0, s, Sin, p.Dp, sc, at<uint32_t>(ctx, p.o_small), err);
         const unsigned bt = (unsigned)std::min<uint64_t>(1024, std::max<uint64_t>(32, p.Dp));
         LAUNCH(ctx, k_batch_invert, 1, bt, 4 * bt * sizeof(fr), s, at<uint32_t>(ctx, p.o_small), p.Dp, (uint64_t)0,
                p.Dp, Abuf);
         const RoundDesc& r = p.rd[0];
-        LAUNCH(ctx, (k_round<false, true>), r.nblocks, kRoundThreads, 0, s, Abuf, S.limbs, p.Dp, nullptr, nullptr, sc, 1,
+        LAUNCH(ctx, (k_round<false, true>), r.nblocks, kRoundThreads, 0, s, Abuf, Sin, p.Dp, nullptr, nullptr, sc, 1,
                arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, partials + r.part_base);
         h01 = 0;
     }
@@ -842,7 +914,7 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
                p.n >= 1 ? p.tnb[0] : 0u, tfin, sc, fst, out, dder, 0, err + 2);
     }
     // ---- rounds 2..d
-    const uint32_t *cA = Abuf, *cS = S.limbs;
+    const uint32_t *cA = Abuf, *cS = Sin;
     uint64_t len = p.Dp;
     for (int k = 2; k <= p.d; ++k) {
         const RoundDesc& r = p.rd[k - 1];
@@ -865,7 +937,16 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
             if (k <= p.n) LAUNCH(ctx, k_tab_eval, p.tnb[k - 1], 256, 0, ctx->side, tcur, tlen, sc, variant, tpart);
             CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join, ctx->side));
         }
-        if (derive)
+        if (k == 2 && r2_gather) {
+            const uint32_t* keys = at<uint32_t>(ctx, p.o_keys);
+            const uint4* TB = at<uint4>(ctx, p.o_tBaos);
+            if (derive)
+                LAUNCH(ctx, (k_round<true, false, true>), r.nblocks, kRoundThreads, 0, s, nullptr, nullptr, len, nA,
+                       nS, sc, k, arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, partials + r.part_base, keys, TB);
+            else
+                LAUNCH(ctx, (k_round<true, true, true>), r.nblocks, kRoundThreads, 0, s, nullptr, nullptr, len, nA,
+                       nS, sc, k, arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, partials + r.part_base, keys, TB);
+        } else if (derive)
             LAUNCH(ctx, (k_round<true, false>), r.nblocks, kRoundThreads, 0, s, cA, cS, len, nA, nS, sc, k,
                    arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, partials + r.part_base);
         else
@@ -1080,7 +1161,7 @@ int zkl_ctx_wait(zkl_ctx* ctx) {
             st = f();
         } else {   // an earlier completion failed: later results are not delivered
             ctx->pend_prepare = ctx->pend_prove = 0;
-            ctx->prep_S = nullptr;
+            ctx->prep_valid = 0;
         }
     }
     return st;
@@ -1126,7 +1207,7 @@ int zkl_ctx_set_workspace(zkl_ctx* c, void* ptr, size_t bytes) {
     if (((uintptr_t)ptr) & 255) return set_err(c, ZKL_E_ARG, "workspace must be 256-byte aligned");
     c->ws = (uint8_t*)ptr;
     c->ws_bytes = bytes;
-    c->prep_S = nullptr;   // the cached index-map keys lived in the old workspace
+    c->prep_valid = 0;   // the cached index-map keys lived in the old workspace
     return ZKL_OK;
 }
 
@@ -1379,7 +1460,9 @@ static int prepare_impl(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T,
     for (auto& x : u) { memset(&x, 0, sizeof(x)); x.w[0] = 1; }
     make_plan(p, D, T->N, ctx->nranks, ctx->rank, true, u.data());
     if ((st = need_ws(ctx, p))) return st;
-    if ((st = check_vec(ctx, S, p.Dp, "S_local"))) return st;
+    // prepare_pair may leave S virtual (S_local_out.limbs == NULL): only the keys are kept, S_i = T_key(i)
+    if ((!pair || S.limbs) && (st = check_vec(ctx, S, p.Dp, "S_local"))) return st;
+    ctx->prep_valid = 0;
     unsigned long long* err = at<unsigned long long>(ctx, p.o_err);
     uint32_t* rows = at<uint32_t>(ctx, p.o_hist);
     CUDA_TRY(ctx, cudaMemsetAsync(err, 0xff, 2 * sizeof(unsigned long long), ctx->stream));   // [0] NOT_IN, [1] range miss
@@ -1442,6 +1525,7 @@ static int prepare_impl(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T,
     }
     if (ctx->async_mode) {
         // the keys are valid for a proof enqueued after this (the completion below clears them on error)
+        ctx->prep_valid = 1;
         ctx->prep_S = S.limbs;
         ctx->prep_n = p.Dp;
         ctx->prep_table = T;
@@ -1481,10 +1565,11 @@ static int prepare_collect(zkl_ctx* ctx, const PrepArgs& a, uint64_t Dp, bool ra
     int64_t* err_index = a.err_index;
     if (e != ~0ull) {
         if (err_index) *err_index = (int64_t)e;
-        ctx->prep_S = nullptr;
+        ctx->prep_valid = 0;
         return set_err(ctx, ZKL_E_NOT_IN_TABLE, "S_%llu is not in T", e);
     }
-    ctx->prep_S = S.limbs;   // the index-map keys in the workspace belong to this S and table
+    ctx->prep_valid = 1;
+    ctx->prep_S = S.limbs;   // the index-map keys in the workspace belong to this S (or a virtual S) and table
     ctx->prep_n = Dp;
     ctx->prep_table = T;
     return ZKL_OK;

@@ -198,7 +198,8 @@ struct zkl_ctx {
     int poisoned;
     uint64_t launches;
     // keys of the last successful zkl_tlookup_prepare (in the workspace): valid for this S / table
-    const uint32_t* prep_S;
+    int prep_valid;                // the workspace keys belong to (prep_S, prep_n, prep_table)
+    const uint32_t* prep_S;        // nullptr: S is virtual (prepare_pair without S_local_out; S_i = T_key)
     uint64_t prep_n;
     const zkl_table* prep_table;
     char last_error[512];

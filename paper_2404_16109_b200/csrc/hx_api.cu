@@ -67,7 +67,7 @@ int run_hyrax_commit(zkl_ctx* ctx, const void* pp, uint64_t cols, zkl_vec S, uin
     if (!ctx->ws || ctx->ws_bytes < h.total)
         return set_err(ctx, ZKL_E_OOM, "workspace %zu bytes < %zu required (zkl_hyrax_workspace_bytes)", ctx->ws_bytes,
                        h.total);
-    ctx->prep_S = nullptr;
+    ctx->prep_valid = 0;
     cudaStream_t s = ctx->stream;
     // pp = [generators (cols + 1, affine)] [their window tables]
     const g1a* tab = reinterpret_cast<const g1a*>((const uint8_t*)pp + align_up(sizeof(g1a) * (cols + 1)));
@@ -108,7 +108,7 @@ int run_hyrax_eval(zkl_ctx* ctx, zkl_vec S, uint64_t D, uint64_t cols, const zkl
     if (!ctx->ws || ctx->ws_bytes < h.total)
         return set_err(ctx, ZKL_E_OOM, "workspace %zu bytes < %zu required (zkl_hyrax_workspace_bytes)", ctx->ws_bytes,
                        h.total);
-    ctx->prep_S = nullptr;
+    ctx->prep_valid = 0;
     const int d = ilog2(D), lr = ilog2(h.rows), lc = ilog2(cols);
     for (int i = 0; i < d; ++i)
         if (fr_ge_r_host(v[i])) return set_err(ctx, ZKL_E_NONCANONICAL, "v_%d is not canonical", i);

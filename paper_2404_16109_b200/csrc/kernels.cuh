@@ -210,7 +210,8 @@ k_index_map(const uint32_t* __restrict__ S, uint64_t n, uint64_t global_offset, 
 // alpha ty_j, tx_j = x0 + j), the index of (x, y) is j = x - x0, valid iff 0 <= j < N and ty[j] == y (then
 // S = T_j exactly; T is duplicate-free).  No hash probe: a 4-byte gather from the L2-resident ty column.  A pair
 // that fails this test may still equal another entry for a special alpha, so a miss only raises `miss`, and the
-// caller redoes the prepare with the exact hash index.
+// caller redoes the prepare with the exact hash index.  dst == nullptr: S stays virtual (keys only; S_i = T_key,
+// S is committed homomorphically as [X] + alpha [Y] and never needs to exist in HBM).
 __global__ void __launch_bounds__(256, 4)
 k_import_pair_range(const int32_t* __restrict__ x, const int32_t* __restrict__ y, uint64_t n,
                     const fr* __restrict__ consts, uint32_t* __restrict__ dst, int32_t x0,
@@ -234,9 +235,9 @@ k_import_pair_range(const int32_t* __restrict__ x, const int32_t* __restrict__ y
                 const bool ok = j >= 0 && (uint64_t)j < N && __ldg(ty + j) == ys[q];
                 missed |= !ok;
                 kk[q] = ok ? (uint32_t)j : 0u;
-                s[q] = fr_from_small_pair(xs[q], ys[q], c);
+                if (dst) s[q] = fr_from_small_pair(xs[q], ys[q], c);
             }
-            st_fr4(dst, n, i, s);
+            if (dst) st_fr4(dst, n, i, s);
             *reinterpret_cast<uint4*>(keys + i) = make_uint4(kk[0], kk[1], kk[2], kk[3]);
         }
     } else {
@@ -245,7 +246,7 @@ k_import_pair_range(const int32_t* __restrict__ x, const int32_t* __restrict__ y
             const bool ok = j >= 0 && (uint64_t)j < N && __ldg(ty + j) == y[i];
             missed |= !ok;
             keys[i] = ok ? (uint32_t)j : 0u;
-            st_fr(dst, n, i, fr_from_small_pair(x[i], y[i], c));
+            if (dst) st_fr(dst, n, i, fr_from_small_pair(x[i], y[i], c));
         }
     }
     if (__any_sync(0xffffffffu, missed) && (threadIdx.x & 31) == 0) atomicMin(miss, 0ull);
@@ -297,7 +298,7 @@ k_import_pair_index(const int32_t* __restrict__ x, const int32_t* __restrict__ y
             s[1] = fr_from_small_pair(xv.y, yv.y, c);
             s[2] = fr_from_small_pair(xv.z, yv.z, c);
             s[3] = fr_from_small_pair(xv.w, yv.w, c);
-            st_fr4(dst, n, i, s);
+            if (dst) st_fr4(dst, n, i, s);
             uint32_t h[4], slot[4], kk[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) h[q] = hash_fr(s[q]) & tv.mask;
@@ -324,7 +325,7 @@ k_import_pair_index(const int32_t* __restrict__ x, const int32_t* __restrict__ y
     }
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const fr s = fr_from_small_pair(x[i], y[i], c);
-        st_fr(dst, n, i, s);
+        if (dst) st_fr(dst, n, i, s);
         const int64_t f = table_find(tv, s);
         uint32_t key = 0;
         if (f < 0) atomic_min_i64(err, global_offset + i);
@@ -636,6 +637,67 @@ k_gather_keys_round1(const uint32_t* __restrict__ S, uint64_t n, const uint32_t*
     }
 }
 
+// Round 1 from the keys of the preceding prepare (a4 + a5 through the table, no D-sized inversion and no D-sized
+// read of S): A_i = B_key(i) and S_i = T_key(i) both come from the 64-byte (B, T) record of the key, so the kernel
+// reads 4 B per lookup from HBM and gathers the records from L2.  VERIFY: S was materialised and may have been
+// rewritten since the prepare -- each S_i is compared with T_key (a mismatch sets *miss, the host redoes the proof
+// by inversion).  WRITE_A: A is written for the caller (A is an output of Prove); otherwise A is
+// never materialised: round 2 gathers it again (k_round<..., GATHER>).  Same tile / pair layout and partial rows as
+// k_inv_bwd<true>: tile = 2048 pairs, thread t owns pairs 256 g + t (g = 0..7), W = E_hi[tile] E_lo[256 g + t].
+template <bool VERIFY, bool WRITE_A>
+__global__ void __launch_bounds__(kInvThreads, 3)
+k_round1_keys(const uint32_t* __restrict__ S, uint64_t n, const uint32_t* __restrict__ keys, uint64_t N,
+              const uint4* __restrict__ TB, uint32_t* __restrict__ Aout, const fr* __restrict__ elo,
+              const fr* __restrict__ ehi, fr* partials, int rows, unsigned long long* miss) {
+    fr acc = fr_zero();
+    fr_acc a0 = fr_acc_zero(), a1 = fr_acc_zero();
+    const uint64_t tile = blockIdx.x;
+    const uint64_t base = tile * kInvTile + 2 * threadIdx.x;
+    uint2 kn = __ldg(reinterpret_cast<const uint2*>(keys + base));
+#pragma unroll 1
+    for (int g = 0; g < 8; ++g) {
+        const uint64_t i0 = base + 512 * g;
+        uint2 k = kn;
+        if (g < 7) kn = __ldg(reinterpret_cast<const uint2*>(keys + i0 + 512));   // the next pair's keys
+        if (k.x >= N || k.y >= N) {
+            atomic_min_i64(miss, i0);
+            k.x = k.x >= N ? 0 : k.x;
+            k.y = k.y >= N ? 0 : k.y;
+        }
+        const uint4* r0 = TB + 4 * (uint64_t)k.x;
+        const uint4* r1 = TB + 4 * (uint64_t)k.y;
+        const fr A0 = ld_fr_256(r0), A1 = ld_fr_256(r1);
+        const fr S0 = ld_fr_256(r0 + 2), S1 = ld_fr_256(r1 + 2);
+        if (VERIFY) {
+            fr x[2];
+            ld_fr2(S, n, i0, x);
+            if (!fr_eq(x[0], S0) || !fr_eq(x[1], S1)) atomic_min_i64(miss, i0);
+        }
+        if (WRITE_A) st_fr2(Aout, n, i0, A0, A1);
+        const fr dA = fr_sub(A1, A0), dS = fr_sub_lazy(S1, S0);
+        acc = fr_add(acc, fr_mul(ld_fr_256(elo + 256 * g + threadIdx.x), fr_mul(dA, dS)));
+        fr_acc_add(a0, A0);
+        fr_acc_add(a1, A1);
+    }
+    fr v[3] = {fr_mul(ehi[tile], acc), fr_acc_final(a0), fr_acc_final(a1)};
+    __shared__ fr scratch[3 * (kInvThreads / 32)];
+    block_sum_fr<3>(v, scratch);
+    if (threadIdx.x == 0) {
+        partials[SLOT_HINF * rows + tile] = v[0];
+        partials[SLOT_A0 * rows + tile] = v[1];
+        partials[SLOT_A1 * rows + tile] = v[2];
+    }
+}
+
+// a virtual S materialised where a kernel needs the vector itself: S_i = T_key(i) (AoS table copy -> SoA)
+__global__ void k_s_from_keys(const uint32_t* __restrict__ keys, uint64_t n, uint64_t N, const uint4* __restrict__ Taos,
+                              uint32_t* __restrict__ dst) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = keys[i];
+        st_fr(dst, n, i, ld_fr_256(Taos + 2 * (uint64_t)(k < N ? k : 0)));
+    }
+}
+
 // (B_j, T_j) packed as one 64-byte record per entry: the gather reads both from one L2 line
 __global__ void k_pack_tb(const uint32_t* __restrict__ T, const uint32_t* __restrict__ B, uint64_t n,
                           uint4* __restrict__ dst) {
@@ -655,11 +717,14 @@ __global__ void k_pack_tb(const uint32_t* __restrict__ T, const uint32_t* __rest
 // each thread G/256 of them, accumulating E_lo-weighted sums that are scaled by E_hi once per group.
 constexpr int kRoundThreads = 256;
 
-template <bool FOLD, bool DIRECT>
+// GATHER (round 2 after k_round1_keys): the four old elements of A and S are the (B, T) records of keys[4y..4y+3]
+// (A_i = B_key, S_i = T_key): 16 B of keys from HBM and four 64-byte records from L2 replace 256 B of A and S.
+template <bool FOLD, bool DIRECT, bool GATHER = false>
 __global__ void __launch_bounds__(kRoundThreads, 2)
 k_round(const uint32_t* __restrict__ Aold, const uint32_t* __restrict__ Sold, uint64_t nold,
         uint32_t* __restrict__ Anew, uint32_t* __restrict__ Snew, const ProofScalars* __restrict__ sc, int k,
-        const fr* __restrict__ elo, const fr* __restrict__ ehi, int gbits, fr* partials) {
+        const fr* __restrict__ elo, const fr* __restrict__ ehi, int gbits, fr* partials,
+        const uint32_t* __restrict__ keys = nullptr, const uint4* __restrict__ TB = nullptr) {
     constexpr bool direct_h1 = DIRECT;
     const fr beta = sc->beta;
     const fr rk = FOLD ? sc->r[k - 2] : fr_zero();
@@ -674,7 +739,24 @@ k_round(const uint32_t* __restrict__ Aold, const uint32_t* __restrict__ Sold, ui
         for (uint32_t yl = threadIdx.x; yl < G; yl += blockDim.x) {
             const uint64_t y = (grp << gbits) + yl;
             fr A0, A1, S0, S1;
-            if (FOLD) {
+            if (FOLD && GATHER) {
+                const uint4 kq = __ldg(reinterpret_cast<const uint4*>(keys + 4 * y));
+                const uint4 *p0 = TB + 4 * (uint64_t)kq.x, *p1 = TB + 4 * (uint64_t)kq.y;
+                const uint4 *p2 = TB + 4 * (uint64_t)kq.z, *p3 = TB + 4 * (uint64_t)kq.w;
+                {
+                    const fr a0 = ld_fr_256(p0), a1 = ld_fr_256(p1), a2 = ld_fr_256(p2), a3 = ld_fr_256(p3);
+                    A0 = fr_add(a0, fr_mul(rk, fr_sub_lazy(a1, a0)));
+                    A1 = fr_add(a2, fr_mul(rk, fr_sub_lazy(a3, a2)));
+                }
+                st_fr2(Anew, nnew, 2 * y, A0, A1);
+                {
+                    const fr s0 = ld_fr_256(p0 + 2), s1 = ld_fr_256(p1 + 2), s2 = ld_fr_256(p2 + 2),
+                             s3 = ld_fr_256(p3 + 2);
+                    S0 = fr_add(s0, fr_mul(rk, fr_sub_lazy(s1, s0)));
+                    S1 = fr_add(s2, fr_mul(rk, fr_sub_lazy(s3, s2)));
+                }
+                st_fr2(Snew, nnew, 2 * y, S0, S1);
+            } else if (FOLD) {
                 {
                     fr a[4];
                     ld_fr4(Aold, nold, 4 * y, a);

@@ -96,7 +96,7 @@ int run_matmul(zkl_ctx* ctx, const int32_t* A, const int32_t* B, uint64_t m, uin
                        ctx->ws_bytes, q.total);
     if (a_out.limbs && (st = check_vec(ctx, a_out, n, "a_out"))) return st;
     if (b_out.limbs && (st = check_vec(ctx, b_out, n, "b_out"))) return st;
-    ctx->prep_S = nullptr;   // the workspace (and the cached index-map keys in it) is reused here
+    ctx->prep_valid = 0;   // the workspace (and the cached index-map keys in it) is reused here
     cudaStream_t s = ctx->stream;
     // challenges u | v | r, canonical, through the pinned staging area
     const int nch = q.lm + q.lp + q.L;

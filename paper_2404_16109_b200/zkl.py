@@ -400,11 +400,14 @@ class Context:
             self._defer(err)
         return m
 
-    def prepare_pair(self, x, y, alpha_f: int, D: int, tab: "Table", S: Optional[Vec] = None, m=None):
-        """a1 + a3 fused for function lookups: S = x + alpha_f y is written to S and counted into m."""
+    def prepare_pair(self, x, y, alpha_f: int, D: int, tab: "Table", S: Optional[Vec] = None, m=None,
+                     virtual_s: bool = False):
+        """a1 + a3 fused for function lookups: S = x + alpha_f y is written to S and counted into m.
+        virtual_s: S is not materialised (only the table keys are kept; prove(None, ...) gathers S_i = T_key);
+        returns (None, m)."""
         tx = x if hasattr(x, "data_ptr") else self.torch.as_tensor(np.asarray(x, np.int32)).to(self.device)
         ty = y if hasattr(y, "data_ptr") else self.torch.as_tensor(np.asarray(y, np.int32)).to(self.device)
-        S = S or self.vec(tx.numel())
+        S = Vec(None, tx.numel()) if virtual_s else (S or self.vec(tx.numel()))
         m = m if m is not None else self.torch.empty(tab.N, dtype=self.torch.int32, device=self.device)
         af = fr_from_int(alpha_f % R_MODULUS)
         err = ctypes.c_int64(-1)
@@ -414,7 +417,7 @@ class Context:
         self._check(st, err.value)
         if self._async:
             self._defer(err, keep=(tx, ty))
-        return S, m
+        return (None if virtual_s else S), m
 
     # -- a4..a9
     @staticmethod
@@ -427,8 +430,10 @@ class Context:
         ch._keep = (U, Rr)
         return ch
 
-    def prove(self, S: Vec, D: int, tab: "Table", m, ch, variant: int = PAPER, want_A: bool = False,
+    def prove(self, S: Optional[Vec], D: int, tab: "Table", m, ch, variant: int = PAPER, want_A: bool = False,
               want_B: bool = False) -> Proof:
+        """S None: the virtual S of the preceding prepare_pair(..., virtual_s=True) on this context."""
+        S = S if S is not None else Vec(None, D // self.nranks)
         d = D.bit_length() - 1
         A = self.vec(S.n) if want_A else Vec(None, S.n)
         B = self.vec(tab.N) if want_B else Vec(None, tab.N)
@@ -449,6 +454,7 @@ class Context:
         Returns (Proof, derived) with derived = dict(beta, alpha1, alpha2, u, r) (canonical ints)."""
         if len(seed) != 32:
             raise ValueError("seed must be 32 bytes")
+        S = S if S is not None else Vec(None, D // self.nranks)
         d = D.bit_length() - 1
         A = self.vec(S.n) if want_A else Vec(None, S.n)
         B = self.vec(tab.N) if want_B else Vec(None, tab.N)

@@ -101,3 +101,47 @@ def test_c_errors():
     with pytest.raises(C.OracleError) as e:
         C.prove(C.ints_to_limbs([1] * 8), C.ints_to_limbs([1, R, 3, 4]), ch)
     assert e.value.name == "E_NONCANONICAL" and e.value.index == 1
+
+
+@pytest.mark.parametrize("variant", [TL.PAPER, TL.LOGUP])
+@pytest.mark.parametrize("d,n,s", [(1, 0, 0), (1, 1, 1), (3, 3, 2), (5, 2, 0), (5, 2, 3), (5, 2, 5), (8, 4, 4),
+                                   (12, 8, 1), (12, 8, 6), (13, 13, 4)])
+def test_stream_tier_equals_c_tier(d, n, s, variant):
+    """The bounded-memory streaming tier (pair inputs, first s rounds per block of 2^s) against zko_tlookup."""
+    rng = np.random.default_rng(d * 100 + n * 10 + s + variant)
+    D, N = 1 << d, 1 << n
+    tx = (np.arange(N) - N // 2).astype(np.int32)              # a range X column, as the activation tables
+    ty = rng.integers(-2 ** 31, 2 ** 31, N, dtype=np.int64).astype(np.int32)
+    pick = rng.integers(0, N, D)
+    x, y = tx[pick], ty[pick]
+    ch = W.challenges(f"stream{d}.{n}.{s}", d)
+    chal = _chal(ch)
+    wl = W.Workload("t", D, N, "pair", ch, x=x, y=y, tx=tx, ty=ty)
+    S, T = C.inputs_from_workload(wl)
+    ref = C.prove(S, T, chal, variant, want_A=False)
+    got = C.prove_pair_stream(x, y, tx, ty, ch.alpha_f, chal, variant, s)
+    assert np.array_equal(got.m, ref.m)
+    assert C.limbs_to_ints(got.B) == C.limbs_to_ints(ref.B)
+    assert got.evals == ref.evals
+    assert got.finals == ref.finals
+
+
+def test_stream_tier_errors():
+    tx = np.arange(8, dtype=np.int32)
+    ty = np.zeros(8, dtype=np.int32)
+    ch = W.challenges("stream-err", 4)
+    chal = _chal(ch)
+    x = np.array([1, 2, 3, 4, 5, 6, 7, 9, 0, 1, 2, 3, 9, 5, 6, 7], dtype=np.int32)   # 9 is not in T (first at 7)
+    with pytest.raises(C.OracleError) as e:
+        C.prove_pair_stream(x, np.zeros(16, np.int32), tx, ty, ch.alpha_f, chal, 0, 2)
+    assert e.value.name == "E_NOT_IN_TABLE" and e.value.index == 7
+    txd = tx.copy()
+    txd[5] = 2                                                                      # T_5 = T_2: duplicate 5
+    with pytest.raises(C.OracleError) as e:
+        C.prove_pair_stream(np.zeros(16, np.int32), np.zeros(16, np.int32), txd, ty, ch.alpha_f, chal, 0, 2)
+    assert e.value.name == "E_DUP_TABLE" and e.value.index == 5
+    # beta = -T_3: DIV_ZERO_T(3) (checked before S)
+    bad = C.chal_array((-3) % R, ch.alpha1, ch.alpha2, ch.u, ch.r)
+    with pytest.raises(C.OracleError) as e:
+        C.prove_pair_stream(np.zeros(16, np.int32), np.zeros(16, np.int32), tx, ty, ch.alpha_f, bad, 0, 2)
+    assert e.value.name == "E_DIV_ZERO_T" and e.value.index == 3

@@ -43,15 +43,16 @@ def step():
         ctx.import_pair(txd, tyd, ch.alpha_f, T)
         tab = ctx.table(T, tmem)
         ctx.table_attach_pair(tab, txd, tyd, ch.alpha_f)   # pair-range fast path of prepare_pair
-        ctx.prepare_pair(xd, yd, ch.alpha_f, D, tab, S, m)
+        ctx.prepare_pair(xd, yd, ch.alpha_f, D, tab, m=m, virtual_s=True)   # the bench step: S virtual
     else:
         ctx.import_ints(td, T)
         tab = ctx.table(T, tmem)
         ctx.import_ints(sd, S)
         ctx.prepare(S, D, tab, m)
+    Sx = None if wl.kind == "pair" else S
     if fs:
-        return ctx.prove_fs(S, D, tab, m, bytes(range(32)), zkl.PAPER)
-    return ctx.prove(S, D, tab, m, chal)
+        return ctx.prove_fs(Sx, D, tab, m, bytes(range(32)), zkl.PAPER)
+    return ctx.prove(Sx, D, tab, m, chal)
 
 
 for _ in range(2):
