@@ -21,6 +21,7 @@
 #include <new>
 #include <vector>
 
+#include "coop.cuh"
 #include "fs.cuh"
 #include "kernels.cuh"
 #include "host_common.h"
@@ -63,6 +64,7 @@ struct Plan {
     int fold_in;         // the tail folds its input on load
     int kc, nchunk_rounds;   // chunked rounds kc .. kc + nchunk_rounds - 1 (k_chunk_rounds), 0 = none
     int tkc;                 // table side: chunked rounds tkc .. tkc + kTabChunkBits - 1 (k_tab_chunk), 0 = none
+    int fs_coop;             // Fiat-Shamir: rounds kc .. d in one cooperative launch (k_fs_rounds_coop)
     uint64_t tnchunks;
     uint64_t nchunks;        // blocks of the chunk launch = elements left for the tail
     RoundDesc rd[kMaxRounds];
@@ -80,7 +82,7 @@ struct Plan {
     // workspace offsets
     size_t o_out, o_sc, o_err, o_rounds, o_jobs, o_chal, o_part, o_tpart, o_tnb, o_rank, o_gath, o_repl, o_tsum,
         o_fin, o_tfin, o_gfin, o_rc, o_fs, o_small, o_Sv, o_derived, o_arena, o_hist, o_keys, o_tot, o_totinv, o_A, o_A1, o_S1, o_A2, o_S2, o_tB, o_tX, o_tM,
-        o_tE, o_twk, o_tBaos, o_chA, o_chS, total;
+        o_tE, o_twk, o_tBaos, o_chA, o_chS, o_coop, total;
 };
 
 void choose_round(Plan& p, int k, uint64_t npairs, int gbits, int nblocks) {
@@ -129,6 +131,24 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
             p.rd[k - 1].direct_h1 = (k == 1 || (p.Dp >> (k - 1)) < (1ull << 20) || !prove_mode) ? 1 : 0;
         p.k0 = p.dl + 1;
         p.fold_in = 0;
+        // the small rounds in one cooperative launch (single rank): from the first round with <= 2^17 elements, if the
+        // table entering it is small enough for one CTA's shared memory
+        if (!p.small && P == 1 && prove_mode) {
+            int k = 2;
+            while (k <= p.dl && (p.Dp >> (k - 1)) > kChunkMaxElems) ++k;
+            const uint64_t nk = p.Dp >> (k - 1);
+            const uint64_t tl_in = (k - 2 <= p.n) ? (N >> (k - 2)) : 1;
+            if (k <= p.dl && nk >= (uint64_t)kChunk && tl_in <= (uint64_t)kCoopTabMax) {
+                p.fs_coop = 1;
+                p.kc = k;
+                p.nchunks = nk / kChunk;
+                for (int kk = k; kk <= p.dl; ++kk) {   // E_hi of the one-warp rounds must be a single entry
+                    RoundDesc& r = p.rd[kk - 1];
+                    r.gbits = kk < k + kChunkBits ? std::min(10, p.dl - kk) : p.dl - kk;
+                    r.direct_h1 = 1;
+                }
+            }
+        }
     } else if (p.small) {
         p.k0 = 1;
         p.fold_in = 0;
@@ -269,6 +289,8 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
     p.o_tBaos = take(64 * std::max<uint64_t>(N, 4));   // (B_j, T_j) records
     p.o_chA = take(soa_bytes(std::max<uint64_t>(p.nchunks, 1)));
     p.o_chS = take(soa_bytes(std::max<uint64_t>(p.nchunks, 1)));
+    // k_fs_rounds_coop: partial rows (10 rounds x 5 x #chunks), table terms, the chunks' last values, the grid barrier
+    p.o_coop = take(sizeof(fr) * (kChunkBits * 5 * 128 + 4 * kMaxRounds + 2 * 128) + sizeof(GridBar));
     auto inv_levels = [&](InvPlan& ip, uint64_t n0) {
         ip.n[0] = n0;
         int L = 0;
@@ -845,7 +867,8 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
     // ---- round 1: A (gather through the prepared index, or inversion) + the round-1 sums
     uint32_t* Abuf = A_out.limbs ? A_out.limbs : at<uint32_t>(ctx, p.o_A);
     const bool gather = !p.small && !force_inversion;
-    const bool r2_gather = gather && keys_ok && p.d >= 2;   // round 2 gathers A, S from the keys again
+    // round 2 gathers A, S from the keys again (unless the cooperative rounds start at round 2 and read round 1's)
+    const bool r2_gather = gather && keys_ok && p.d >= 2 && !(p.fs_coop && p.kc == 2);
     const uint32_t* Sin = S.limbs;
     if (virt && !r2_gather) {   // D_local < 4096: the small path reads S itself
         uint32_t* Sv = at<uint32_t>(ctx, p.o_Sv);
@@ -916,7 +939,26 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
     // ---- rounds 2..d
     const uint32_t *cA = Abuf, *cS = Sin;
     uint64_t len = p.Dp;
+    bool coop_done = false;
     for (int k = 2; k <= p.d; ++k) {
+        if (p.fs_coop && k == p.kc) {
+            // rounds kc .. d: one cooperative launch, a grid barrier per round (csrc/coop.cuh)
+            fr* cb = at<fr>(ctx, p.o_coop);
+            GridBar* bar = reinterpret_cast<GridBar*>(cb + kChunkBits * 5 * 128 + 4 * kMaxRounds + 2 * 128);
+            CUDA_TRY(ctx, cudaMemsetAsync(bar, 0, sizeof(GridBar), s));
+            CoopFsArgs ca;
+            ca.Ain = cA; ca.Sin = cS; ca.nin = len;
+            ca.kc = p.kc; ca.d = p.d; ca.n = p.n; ca.variant = variant;
+            ca.rounds = rounds; ca.arena = arena;
+            ca.rows = cb; ca.tabbuf = cb + kChunkBits * 5 * 128; ca.chA = ca.tabbuf + 4 * kMaxRounds;
+            ca.chS = ca.chA + 128;
+            ca.tcur = tcur; ca.tlen = (int)tlen; ca.tfin = tfin; ca.fin = fin;
+            ca.sc = sc; ca.st = fst; ca.out = out; ca.derived = dder; ca.bar = bar;
+            const size_t smem = (2 * kChunk + 4 * kCoopTabMax) * sizeof(fr);
+            LAUNCH_COOP(ctx, k_fs_rounds_coop, (unsigned)p.nchunks, kChunkThreads, smem, s, ca);
+            coop_done = true;
+            break;
+        }
         const RoundDesc& r = p.rd[k - 1];
         const bool derive = !force_inversion && !r.direct_h1;
         uint32_t* nA = at<uint32_t>(ctx, (k & 1) == 0 ? p.o_A1 : p.o_A2);
@@ -958,8 +1000,10 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
         LAUNCH(ctx, k_fs_round, 1, 256, 0, s, k, p.d, p.n, variant, partials + r.part_base, r.nblocks, 0, tpart,
                k <= p.n ? p.tnb[k - 1] : 0u, tfin, sc, fst, out, dder, derive ? 1 : 0, err + 2);
     }
-    LAUNCH(ctx, k_fold_final, 1, 32, 0, s, cA, cS, len, sc, p.d, fin);
-    if (p.n == p.d) LAUNCH(ctx, k_tab_fold, 1, 32, 0, s, tcur, tlen, tnxt, sc, p.d, tfin);
+    if (!coop_done) {
+        LAUNCH(ctx, k_fold_final, 1, 32, 0, s, cA, cS, len, sc, p.d, fin);
+        if (p.n == p.d) LAUNCH(ctx, k_tab_fold, 1, 32, 0, s, tcur, tlen, tnxt, sc, p.d, tfin);
+    }
     LAUNCH(ctx, k_fs_finish, 1, 32, 0, s, fin, tfin, out);
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->host_out, out, sizeof(ProofOut), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(ctx, cudaMemcpyAsync((uint8_t*)ctx->host_out + offsetof(ProofOut, err_index), err,
@@ -1077,6 +1121,8 @@ static int ctx_create_common(int device, void* stream, zkl_ctx** out) {
     cudaFuncSetAttribute(k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tail_smem);
     cudaFuncSetAttribute(k_batch_invert, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 1024 * (int)sizeof(fr));
     cudaFuncSetAttribute(k_tab_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kTabChunk * (int)sizeof(fr));
+    cudaFuncSetAttribute(k_fs_rounds_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)((2 * kChunk + 4 * kCoopTabMax) * sizeof(fr)));
     cudaFuncSetAttribute(k_chunk_rounds, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(2 * kChunk * sizeof(fr)));
     *out = c;

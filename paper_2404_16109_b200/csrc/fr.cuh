@@ -275,31 +275,39 @@ __device__ __forceinline__ fr fr_mul(const fr& a, const fr& b) {
     // ---- iteration 0: plain products (T = 0)
     {
         const uint32_t bi = b.v[0];
-        asm("mul.lo.u32 %0, %9, %13;\n\t"  "mul.hi.u32 %1, %9, %13;\n\t"
-            "mul.lo.u32 %2, %10, %13;\n\t" "mul.hi.u32 %3, %10, %13;\n\t"
-            "mul.lo.u32 %4, %11, %13;\n\t" "mul.hi.u32 %5, %11, %13;\n\t"
-            "mul.lo.u32 %6, %12, %13;\n\t" "mul.hi.u32 %7, %12, %13;\n\t"
-            "mov.u32 %8, 0;"
+        // one IMAD.WIDE.U32 per product (a lo/hi pair of mul.lo / mul.hi would cost an extra half-rate IMAD.HI)
+        asm("{\n\t.reg .u64 p0, p1, p2, p3;\n\t"
+            "mul.wide.u32 p0, %9, %13;\n\t"  "mul.wide.u32 p1, %10, %13;\n\t"
+            "mul.wide.u32 p2, %11, %13;\n\t" "mul.wide.u32 p3, %12, %13;\n\t"
+            "mov.b64 {%0, %1}, p0;\n\t" "mov.b64 {%2, %3}, p1;\n\t"
+            "mov.b64 {%4, %5}, p2;\n\t" "mov.b64 {%6, %7}, p3;\n\t"
+            "mov.u32 %8, 0;\n\t}"
             : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3), "=r"(x4), "=r"(x5), "=r"(x6), "=r"(x7), "=r"(x8)
             : "r"(a.v[0]), "r"(a.v[2]), "r"(a.v[4]), "r"(a.v[6]), "r"(bi));
-        asm("mul.lo.u32 %0, %8, %12;\n\t"  "mul.hi.u32 %1, %8, %12;\n\t"
-            "mul.lo.u32 %2, %9, %12;\n\t"  "mul.hi.u32 %3, %9, %12;\n\t"
-            "mul.lo.u32 %4, %10, %12;\n\t" "mul.hi.u32 %5, %10, %12;\n\t"
-            "mul.lo.u32 %6, %11, %12;\n\t" "mul.hi.u32 %7, %11, %12;"
+        asm("{\n\t.reg .u64 p0, p1, p2, p3;\n\t"
+            "mul.wide.u32 p0, %8, %12;\n\t"  "mul.wide.u32 p1, %9, %12;\n\t"
+            "mul.wide.u32 p2, %10, %12;\n\t" "mul.wide.u32 p3, %11, %12;\n\t"
+            "mov.b64 {%0, %1}, p0;\n\t" "mov.b64 {%2, %3}, p1;\n\t"
+            "mov.b64 {%4, %5}, p2;\n\t" "mov.b64 {%6, %7}, p3;\n\t}"
             : "=r"(y0), "=r"(y1), "=r"(y2), "=r"(y3), "=r"(y4), "=r"(y5), "=r"(y6), "=r"(y7)
             : "r"(a.v[1]), "r"(a.v[3]), "r"(a.v[5]), "r"(a.v[7]), "r"(bi));
     }
+// q r1 with r1 = 2^32 - 1 is not multiplied: q r1 = (q - 1) 2^32 + (2^32 - q) for q = -x0 != 0, so lo = x0 and
+// hi = q - [x0 != 0] = ~x0 + [x0 == 0] (also right for q = 0): one borrow chain instead of a half-rate IMAD.HI
+// (SURVEY.md §8(d) "224 slots"; tools/sim_fr_mul.py checks the chain).
 #define ZKL_REDUCE_STEP()                                                                        \
-    asm("{\n\t.reg .u32 q;\n\t"                                                                  \
-        "sub.u32 q, 0, %0;\n\t"                                                                  \
+    asm("{\n\t.reg .u32 q, xo, hi;\n\t"                                                          \
+        "mov.u32 xo, %0;\n\t"                                                                    \
+        "sub.cc.u32 q, 0, %0;\n\t"              /* borrow = [x0 != 0] */                         \
+        "subc.u32 hi, q, 0;\n\t"                /* hi = q - [x0 != 0] = ~x0 + [x0 == 0] */       \
         "add.cc.u32 %0, %0, q;\n\t"                                                              \
         "addc.cc.u32 %1, %1, 0;\n\t"                                                             \
         ZKL_MADPAIR("%2", "%3", "q", "%18", "%2", "%3")                                          \
         ZKL_MADPAIR("%4", "%5", "q", "%20", "%4", "%5")                                          \
         ZKL_MADPAIR("%6", "%7", "q", "%22", "%6", "%7")                                          \
         "addc.u32 %8, %8, 0;\n\t"                                                                \
-        "mad.lo.cc.u32  %9,  q, %17, %9;\n\t"                                                    \
-        "madc.hi.cc.u32 %10, q, %17, %10;\n\t"                                                   \
+        "add.cc.u32  %9,  %9, xo;\n\t"                                                           \
+        "addc.cc.u32 %10, %10, hi;\n\t"                                                          \
         ZKL_MADPAIR("%11", "%12", "q", "%19", "%11", "%12")                                      \
         ZKL_MADPAIR("%13", "%14", "q", "%21", "%13", "%14")                                      \
         "madc.lo.cc.u32 %15, q, %23, %15;\n\t"                                                   \

@@ -49,6 +49,17 @@ inline int set_err(zkl_ctx* ctx, int st, const char* fmt, ...) {
         CUDA_TRY(ctx, cudaGetLastError());                                                          \
     } while (0)
 
+// A cooperative launch (all CTAs co-resident: the kernel synchronises its grid, csrc/coop.cuh), counted and profiled
+// like LAUNCH.  One by-value argument struct.
+#define LAUNCH_COOP(ctx, kern, grid, block, smem, stream, arg)                                      \
+    do {                                                                                            \
+        zkl_ctx::ProfRec* pr_ = prof_begin((ctx), #kern, (stream));                                 \
+        void* args_[] = {(void*)&(arg)};                                                            \
+        CUDA_TRY(ctx, cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(block), args_, (smem), (stream))); \
+        (ctx)->launches++;                                                                          \
+        if (pr_) cudaEventRecord(pr_->b, (stream));                                                 \
+    } while (0)
+
 inline zkl_ctx::ProfRec* prof_begin(zkl_ctx* ctx, const char* name, cudaStream_t st) {
     if (!ctx->profiling || ctx->nprof >= 256) return nullptr;
     zkl_ctx::ProfRec* r = &ctx->prof[ctx->nprof++];

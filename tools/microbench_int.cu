@@ -176,6 +176,67 @@ __global__ void k_frmul(fr* out, int iters, uint32_t b, uint32_t c) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
+// textbook SOS Montgomery in 64-bit arithmetic (no carry-chain tricks): the reference fr_mul is checked against
+__device__ fr ref_mont(const fr& a, const fr& b) {
+    const uint32_t rl[8] = {ZKL_R0, ZKL_R1, ZKL_R2, ZKL_R3, ZKL_R4, ZKL_R5, ZKL_R6, ZKL_R7};
+    uint32_t t[17] = {0};
+    for (int i = 0; i < 8; ++i) {
+        uint64_t c = 0;
+        for (int j = 0; j < 8; ++j) {
+            c += (uint64_t)a.v[i] * b.v[j] + t[i + j];
+            t[i + j] = (uint32_t)c;
+            c >>= 32;
+        }
+        for (int k = i + 8; k < 17 && c; ++k) { c += t[k]; t[k] = (uint32_t)c; c >>= 32; }
+    }
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t q = 0u - t[i];   // r' = -r^{-1} = -1 mod 2^32
+        uint64_t c = 0;
+        for (int j = 0; j < 8; ++j) {
+            c += (uint64_t)q * rl[j] + t[i + j];
+            t[i + j] = (uint32_t)c;
+            c >>= 32;
+        }
+        for (int k = i + 8; k < 17 && c; ++k) { c += t[k]; t[k] = (uint32_t)c; c >>= 32; }
+    }
+    fr r;
+    for (int i = 0; i < 8; ++i) r.v[i] = t[8 + i];
+    if (t[16] || !(r.v[7] < rl[7] || (r.v[7] == rl[7] && !u256_geq(r, fr_modulus())))) {
+        uint64_t bw = 0;
+        for (int i = 0; i < 8; ++i) {
+            const uint64_t d = (uint64_t)r.v[i] - rl[i] - bw;
+            r.v[i] = (uint32_t)d;
+            bw = (d >> 63) & 1;
+        }
+    }
+    return r;
+}
+
+__device__ uint32_t mix32(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return (uint32_t)(z ^ (z >> 31));
+}
+
+// canonical a, b < r from a counter (every third thread: limb extremes); counts mismatches of fr_mul vs ref_mont
+__global__ void k_frmul_check(unsigned long long* bad, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        fr a, b;
+        for (int l = 0; l < 8; ++l) {
+            a.v[l] = mix32(i * 16 + l);
+            b.v[l] = mix32(i * 16 + 8 + l);
+        }
+        if (i % 3 == 1) for (int l = 0; l < 8; ++l) a.v[l] = (mix32(i) >> l) & 1 ? 0xffffffffu : 0u;
+        if (i % 5 == 2) a.v[0] = 0;
+        a.v[7] &= 0x3fffffffu;   // < 2^254 < r
+        b.v[7] &= 0x3fffffffu;
+        if (i == 0) { a = fr_modulus(); a.v[0] -= 1; b = a; }   // (r-1)^2
+        const fr x = fr_mul(a, b), y = ref_mont(a, b);
+        if (!fr_eq(x, y)) atomicAdd(bad, 1ull);
+    }
+}
+
 static double g_mhz;
 
 template <typename K, typename T>
@@ -227,6 +288,17 @@ int main() {
     if (timeit("frmul_ilp1", k_frmul<1>, (fr*)buf, 148 * 8, 256, 512, 1, &fr1)) return 1;
     if (timeit("frmul_ilp2", k_frmul<2>, (fr*)buf, 148 * 8, 128, 512, 2, &fr2)) return 1;
     if (timeit("frmul_ilp4", k_frmul<4>, (fr*)buf, 148 * 4, 128, 512, 4, &fr4)) return 1;
+    {
+        unsigned long long* dbad;
+        CK(cudaMalloc(&dbad, 8));
+        CK(cudaMemset(dbad, 0, 8));
+        const uint64_t n = 1ull << 24;
+        k_frmul_check<<<148 * 4, 256>>>(dbad, n);
+        unsigned long long hb = 0;
+        CK(cudaMemcpy(&hb, dbad, 8, cudaMemcpyDeviceToHost));
+        printf("{\"frmul_check\": {\"products\": %llu, \"mismatches\": %llu}}\n", (unsigned long long)n, hb);
+        if (hb) return 2;
+    }
     double frbest = fr1 > fr2 ? fr1 : fr2;
     frbest = frbest > fr4 ? frbest : fr4;
     printf("{\"MEASURED_INT_PEAKS\": {\"imad_lo_per_clk_sm\": %.2f, \"imad_hi_per_clk_sm\": %.2f, "

@@ -1,5 +1,8 @@
 """Word-level simulation of the aligned-pair CIOS schedule used by csrc/fr.cuh (dev check).
 
+The q r1 product of each reduction step is not multiplied: r1 = 2^32 - 1, so q r1 = (q - 1) 2^32 + (2^32 - q) with
+q = -x0, i.e. lo = x0 and hi = ~x0 + [x0 == 0] (three ALU instructions instead of an IMAD.HI pair).
+
 Models every PTX carry chain with explicit 32-bit words and a carry flag, asserting that
 the chains whose carry-out is dropped (Y chains) never produce a carry, for random and
 extreme operands.  Not part of the oracle; a design check of the schedule only.
@@ -64,6 +67,9 @@ def mul(aw, bw):
                 X[j + 1] = ch.madc(a[j], b, Xin[j + 1], True)
             X[8] = ch.add(0, 0, cc_out=False)
         q = (-X[0]) & M
+        xo = X[0]
+        hi1 = ((~xo) + (1 if xo == 0 else 0)) & M   # hi(q r1) for r1 = 2^32 - 1 (lo(q r1) = xo): no multiply
+        assert (hi1 << 32) + xo == q * rl[1]
         ch = Chain()
         X[0] = ch.add(X[0], q, cc_in=False)
         assert X[0] == 0
@@ -73,8 +79,10 @@ def mul(aw, bw):
             X[j + 1] = ch.madc(q, rl[j], X[j + 1], True)
         X[8] = ch.add(X[8], 0, cc_out=False)
         ch = Chain()
-        for j in range(1, 8, 2):
-            Y[j - 1] = ch.madc(q, rl[j], Y[j - 1], False, cc_in=(j != 1))
+        Y[0] = ch.add(Y[0], xo, cc_in=False)
+        Y[1] = ch.add(Y[1], hi1)
+        for j in range(3, 8, 2):
+            Y[j - 1] = ch.madc(q, rl[j], Y[j - 1], False)
             Y[j] = ch.madc(q, rl[j], Y[j], True, cc_out=(j != 7))
         x, y = X, Y
     ch = Chain()
