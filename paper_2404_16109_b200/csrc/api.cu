@@ -85,6 +85,16 @@ struct Plan {
         o_tE, o_twk, o_tBaos, o_chA, o_chS, o_coop, total;
 };
 
+// k_round: one CTA per group of 2^gbits pairs (grid = #groups = partial rows).  2^12 pairs (16 per thread) by default,
+// fewer while that leaves < 2 CTAs per SM, more (<= 2^14: the wide accumulators take <= 64 terms) beyond 65536 groups
+int round_gbits(uint64_t np) {
+    int gbits = 12;
+    while (gbits > 8 && (np >> gbits) < (uint64_t)(2 * kSMs)) --gbits;
+    while (gbits < 14 && (np >> gbits) > 65536) ++gbits;
+    if ((1ull << gbits) > np) gbits = ilog2(np);
+    return gbits;
+}
+
 void choose_round(Plan& p, int k, uint64_t npairs, int gbits, int nblocks) {
     RoundDesc& r = p.rd[k - 1];
     r.gbits = gbits;
@@ -120,10 +130,8 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
                 choose_round(p, 1, np, 11, (int)p.ntiles);
                 continue;
             }
-            int gbits = 12;
-            while (gbits > 8 && (np >> gbits) < (uint64_t)kSMs) --gbits;
-            if ((1ull << gbits) > np) gbits = ilog2(np);
-            choose_round(p, k, np, gbits, (int)std::max<uint64_t>(1, std::min<uint64_t>(np >> gbits, kMaxBlocks)));
+            const int gbits = round_gbits(np);
+            choose_round(p, k, np, gbits, (int)std::max<uint64_t>(1, np >> gbits));
         }
         // H(1) summed directly, except in the big rounds (>= 2^20 elements), whose k_round hides the one inversion
         // per round that deriving H(1) from the running claim needs (k_fs_inv on the side stream)
@@ -164,11 +172,8 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
             if (k >= 2 && nk <= kChunkMaxElems && nk >= (uint64_t)kChunk) break;   // chunked rounds from here
             if (k == 1 && prove_mode) continue;
             const uint64_t np = nk / 2;
-            int gbits = 12;
-            while (gbits > 8 && (np >> gbits) < (uint64_t)kSMs) --gbits;
-            if ((1ull << gbits) > np) gbits = ilog2(np);
-            const int nb = (int)std::min<uint64_t>(np >> gbits, (uint64_t)kMaxBlocks);
-            choose_round(p, k, np, gbits, nb);
+            const int gbits = round_gbits(np);
+            choose_round(p, k, np, gbits, (int)std::max<uint64_t>(1, np >> gbits));
         }
         p.k0 = k;
         p.fold_in = 1;
@@ -677,8 +682,10 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
             uint32_t* chA = at<uint32_t>(ctx, p.o_chA);
             uint32_t* chS = at<uint32_t>(ctx, p.o_chS);
             const size_t chunk_smem = 2 * kChunk * sizeof(fr);
-            LAUNCH(ctx, k_chunk_rounds, (unsigned)p.nchunks, kChunkThreads, chunk_smem, s, cA, cS, len, sc, p.kc,
-                   p.nchunk_rounds, rounds, arena, partials, chA, chS);
+            GridBar* bar = reinterpret_cast<GridBar*>(at<fr>(ctx, p.o_coop) + kChunkBits * 5 * 128 + 4 * kMaxRounds + 2 * 128);
+            CUDA_TRY(ctx, cudaMemsetAsync(bar, 0, sizeof(GridBar), s));
+            ChunkArgs ka{cA, cS, len, sc, p.kc, p.nchunk_rounds, rounds, arena, partials, chA, chS, bar};
+            LAUNCH_COOP(ctx, k_chunk_rounds_coop, (unsigned)p.nchunks, kChunkThreads, chunk_smem, s, ka);
             cA = chA; cS = chS;
             len = p.nchunks;
         }
@@ -1123,7 +1130,7 @@ static int ctx_create_common(int device, void* stream, zkl_ctx** out) {
     cudaFuncSetAttribute(k_tab_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kTabChunk * (int)sizeof(fr));
     cudaFuncSetAttribute(k_fs_rounds_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)((2 * kChunk + 4 * kCoopTabMax) * sizeof(fr)));
-    cudaFuncSetAttribute(k_chunk_rounds, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_chunk_rounds_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(2 * kChunk * sizeof(fr)));
     *out = c;
     return ZKL_OK;

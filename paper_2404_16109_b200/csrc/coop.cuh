@@ -15,31 +15,6 @@
 
 namespace zkl {
 
-// Sense-counting grid barrier for a cooperative launch (all CTAs co-resident, guaranteed by
-// cudaLaunchCooperativeKernel).  count returns to 0 after each barrier; gen only increases.
-struct GridBar {
-    unsigned int count;
-    unsigned int gen;
-};
-
-__device__ __forceinline__ void grid_sync(GridBar* b) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        volatile unsigned int* vgen = &b->gen;
-        const unsigned int g = *vgen;
-        __threadfence();
-        if (atomicAdd(&b->count, 1u) == gridDim.x - 1) {
-            b->count = 0;
-            __threadfence();
-            atomicAdd(&b->gen, 1u);
-        } else {
-            while (*vgen == g) __nanosleep(32);
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
-
 // Transcript state one CTA carries through the rounds (a copy of FsState)
 struct FsLocal {
     uint8_t h[32];

@@ -523,6 +523,102 @@ static __device__ __noinline__ fr fr_inv_fermat(const fr a) {
     return acc;
 }
 
+// ---------------------------------------------------------------------------------------
+// Lazy (wide) accumulation of an eq-weighted sum  c = sum_y e_y X_y R^{-1} (mod r):
+// the 512-bit products e_y X_y are summed without reduction (product scanning, 64 IMAD.WIDE and a carry word per
+// column, against 112 IMAD.WIDE for a Montgomery product) and the sum is reduced once.  Bounds: e_y, X_y < 2r, so
+// with at most 16 terms W < 64 r^2 < 2^516 fits 17 words; fr_wide_redc first brings the high half W_hi < 2^260
+// below r by conditional subtractions of 16r, 8r, 4r, 2r, r (it changes W by multiples of r 2^256), then
+// W < r 2^256 and one Montgomery reduction gives W R^{-1} mod r < 2r, made canonical.
+struct fr_wide {
+    uint32_t v[17];
+};
+
+__device__ __forceinline__ fr_wide fr_wide_zero() {
+    fr_wide w;
+#pragma unroll
+    for (int i = 0; i < 17; ++i) w.v[i] = 0;
+    return w;
+}
+
+// W += a * b
+__device__ __forceinline__ void fr_wide_mac(fr_wide& W, const fr& a, const fr& b) {
+    uint32_t t0 = 0, t1 = 0, t2 = 0;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+        asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, 0;" : "+r"(t0), "+r"(t1) : "r"(W.v[c]));
+#pragma unroll
+        for (int j = (c > 7 ? c - 7 : 0); j <= (c < 7 ? c : 7); ++j)
+            asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\tmadc.hi.cc.u32 %1, %3, %4, %1;\n\taddc.u32 %2, %2, 0;"
+                : "+r"(t0), "+r"(t1), "+r"(t2) : "r"(a.v[j]), "r"(b.v[c - j]));
+        W.v[c] = t0;
+        t0 = t1;
+        t1 = t2;
+        t2 = 0;
+    }
+    W.v[16] += t0;   // t1 = 0: the sum stays below 2^544
+}
+
+// H = W[8..16] (9 words) -= m 2^s r  if  H >= m 2^s r
+__device__ __forceinline__ void fr_wide_hi_sub_if(fr_wide& W, int s) {
+    const uint32_t rl[8] = {ZKL_R0, ZKL_R1, ZKL_R2, ZKL_R3, ZKL_R4, ZKL_R5, ZKL_R6, ZKL_R7};
+    uint32_t mr[9], d[9];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) mr[k] = (rl[k] << s) | (k && s ? rl[k - 1] >> (32 - s) : 0u);
+    mr[8] = s ? rl[7] >> (32 - s) : 0u;
+    uint32_t borrow;
+    asm("sub.cc.u32  %0, %10, %19;\n\t"
+        "subc.cc.u32 %1, %11, %20;\n\t"
+        "subc.cc.u32 %2, %12, %21;\n\t"
+        "subc.cc.u32 %3, %13, %22;\n\t"
+        "subc.cc.u32 %4, %14, %23;\n\t"
+        "subc.cc.u32 %5, %15, %24;\n\t"
+        "subc.cc.u32 %6, %16, %25;\n\t"
+        "subc.cc.u32 %7, %17, %26;\n\t"
+        "subc.cc.u32 %8, %18, %27;\n\t"
+        "subc.u32    %9, 0, 0;"
+        : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]), "=r"(d[8]),
+          "=r"(borrow)
+        : "r"(W.v[8]), "r"(W.v[9]), "r"(W.v[10]), "r"(W.v[11]), "r"(W.v[12]), "r"(W.v[13]), "r"(W.v[14]),
+          "r"(W.v[15]), "r"(W.v[16]), "r"(mr[0]), "r"(mr[1]), "r"(mr[2]), "r"(mr[3]), "r"(mr[4]), "r"(mr[5]),
+          "r"(mr[6]), "r"(mr[7]), "r"(mr[8]));
+#pragma unroll
+    for (int k = 0; k < 9; ++k) W.v[8 + k] = borrow ? W.v[8 + k] : d[k];
+}
+
+// W R^{-1} mod r, canonical (W destroyed)
+__device__ __forceinline__ fr fr_wide_redc(fr_wide& W) {
+    fr_wide_hi_sub_if(W, 4);
+    fr_wide_hi_sub_if(W, 3);
+    fr_wide_hi_sub_if(W, 2);
+    fr_wide_hi_sub_if(W, 1);
+    fr_wide_hi_sub_if(W, 0);
+    // W < r 2^256: eight Montgomery steps, q = -W[i] (r' = -1), W += q r 2^{32 i} (once per sum: plain 64-bit code)
+    const uint32_t rl[8] = {ZKL_R0, ZKL_R1, ZKL_R2, ZKL_R3, ZKL_R4, ZKL_R5, ZKL_R6, ZKL_R7};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t q = 0u - W.v[i];
+        uint64_t c = W.v[i] != 0;   // W[i] + q r0 = W[i] + q is 0 or 2^32
+#pragma unroll
+        for (int j = 1; j < 8; ++j) {
+            c += (uint64_t)q * rl[j] + W.v[i + j];
+            W.v[i + j] = (uint32_t)c;
+            c >>= 32;
+        }
+#pragma unroll
+        for (int k = i + 8; k < 17; ++k) {
+            c += W.v[k];
+            W.v[k] = (uint32_t)c;
+            c >>= 32;
+        }
+    }
+    fr o;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o.v[k] = W.v[8 + k];
+    fr_reduce_once(o);
+    return o;
+}
+
 // Canonical (non-Montgomery) a >= r ?
 __device__ __forceinline__ bool fr_geq_modulus(const fr& x) {
     uint32_t borrow;

@@ -644,12 +644,15 @@ k_gather_keys_round1(const uint32_t* __restrict__ S, uint64_t n, const uint32_t*
 // by inversion).  WRITE_A: A is written for the caller (A is an output of Prove); otherwise A is
 // never materialised: round 2 gathers it again (k_round<..., GATHER>).  Same tile / pair layout and partial rows as
 // k_inv_bwd<true>: tile = 2048 pairs, thread t owns pairs 256 g + t (g = 0..7), W = E_hi[tile] E_lo[256 g + t].
+#ifndef ZKL_R1_CTAS
+#define ZKL_R1_CTAS 2
+#endif
 template <bool VERIFY, bool WRITE_A>
-__global__ void __launch_bounds__(kInvThreads, 3)
+__global__ void __launch_bounds__(kInvThreads, ZKL_R1_CTAS)
 k_round1_keys(const uint32_t* __restrict__ S, uint64_t n, const uint32_t* __restrict__ keys, uint64_t N,
               const uint4* __restrict__ TB, uint32_t* __restrict__ Aout, const fr* __restrict__ elo,
               const fr* __restrict__ ehi, fr* partials, int rows, unsigned long long* miss) {
-    fr acc = fr_zero();
+    fr_wide acc = fr_wide_zero();   // sum of E_lo dA dS over the thread's 8 pairs, reduced once (fr_wide_*)
     fr_acc a0 = fr_acc_zero(), a1 = fr_acc_zero();
     const uint64_t tile = blockIdx.x;
     const uint64_t base = tile * kInvTile + 2 * threadIdx.x;
@@ -675,11 +678,11 @@ k_round1_keys(const uint32_t* __restrict__ S, uint64_t n, const uint32_t* __rest
         }
         if (WRITE_A) st_fr2(Aout, n, i0, A0, A1);
         const fr dA = fr_sub(A1, A0), dS = fr_sub_lazy(S1, S0);
-        acc = fr_add(acc, fr_mul(ld_fr_256(elo + 256 * g + threadIdx.x), fr_mul(dA, dS)));
+        fr_wide_mac(acc, ld_fr_256(elo + 256 * g + threadIdx.x), fr_mul(dA, dS));
         fr_acc_add(a0, A0);
         fr_acc_add(a1, A1);
     }
-    fr v[3] = {fr_mul(ehi[tile], acc), fr_acc_final(a0), fr_acc_final(a1)};
+    fr v[3] = {fr_mul(ehi[tile], fr_wide_redc(acc)), fr_acc_final(a0), fr_acc_final(a1)};
     __shared__ fr scratch[3 * (kInvThreads / 32)];
     block_sum_fr<3>(v, scratch);
     if (threadIdx.x == 0) {
@@ -726,69 +729,81 @@ k_round(const uint32_t* __restrict__ Aold, const uint32_t* __restrict__ Sold, ui
         const fr* __restrict__ elo, const fr* __restrict__ ehi, int gbits, fr* partials,
         const uint32_t* __restrict__ keys = nullptr, const uint4* __restrict__ TB = nullptr) {
     constexpr bool direct_h1 = DIRECT;
+#ifdef ZKL_ROUND_SCALARS_IN_REGS
     const fr beta = sc->beta;
     const fr rk = FOLD ? sc->r[k - 2] : fr_zero();
+#else
+    // beta and r_{k-1} are read from shared memory where they are used: 16 fewer live registers in the pair loop
+    __shared__ fr sh_beta, sh_rk;
+    if (threadIdx.x == 0) {
+        sh_beta = sc->beta;
+        sh_rk = FOLD ? sc->r[k - 2] : fr_zero();
+    }
+    __syncthreads();
+    const fr& beta = sh_beta;
+    const fr& rk = sh_rk;
+#endif
     const uint64_t npairs = FOLD ? nold / 4 : nold / 2;   // pairs of the round being evaluated
     const uint64_t nnew = nold / 2;
     const uint32_t G = 1u << gbits;
-    const uint64_t ngroups = npairs >> gbits;
-    fr H0 = fr_zero(), H1 = fr_zero(), Hinf = fr_zero();
+    // one group of G pairs per CTA (grid = #groups): each thread accumulates its G/256 <= 64 E_lo-weighted terms
+    // unreduced (fr_wide_*) and scales the reduced sums by E_hi once
+    const uint64_t grp = blockIdx.x;
+    fr_wide c0 = fr_wide_zero(), cinf = fr_wide_zero();
+    fr c1 = fr_zero();
     fr_acc a0 = fr_acc_zero(), a1 = fr_acc_zero();
-    for (uint64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-        fr c0 = fr_zero(), c1 = fr_zero(), cinf = fr_zero();
-        for (uint32_t yl = threadIdx.x; yl < G; yl += blockDim.x) {
-            const uint64_t y = (grp << gbits) + yl;
-            fr A0, A1, S0, S1;
-            if (FOLD && GATHER) {
-                const uint4 kq = __ldg(reinterpret_cast<const uint4*>(keys + 4 * y));
-                const uint4 *p0 = TB + 4 * (uint64_t)kq.x, *p1 = TB + 4 * (uint64_t)kq.y;
-                const uint4 *p2 = TB + 4 * (uint64_t)kq.z, *p3 = TB + 4 * (uint64_t)kq.w;
-                {
-                    const fr a0 = ld_fr_256(p0), a1 = ld_fr_256(p1), a2 = ld_fr_256(p2), a3 = ld_fr_256(p3);
-                    A0 = fr_add(a0, fr_mul(rk, fr_sub_lazy(a1, a0)));
-                    A1 = fr_add(a2, fr_mul(rk, fr_sub_lazy(a3, a2)));
-                }
-                st_fr2(Anew, nnew, 2 * y, A0, A1);
-                {
-                    const fr s0 = ld_fr_256(p0 + 2), s1 = ld_fr_256(p1 + 2), s2 = ld_fr_256(p2 + 2),
-                             s3 = ld_fr_256(p3 + 2);
-                    S0 = fr_add(s0, fr_mul(rk, fr_sub_lazy(s1, s0)));
-                    S1 = fr_add(s2, fr_mul(rk, fr_sub_lazy(s3, s2)));
-                }
-                st_fr2(Snew, nnew, 2 * y, S0, S1);
-            } else if (FOLD) {
-                {
-                    fr a[4];
-                    ld_fr4(Aold, nold, 4 * y, a);
-                    A0 = fr_add(a[0], fr_mul(rk, fr_sub_lazy(a[1], a[0])));
-                    A1 = fr_add(a[2], fr_mul(rk, fr_sub_lazy(a[3], a[2])));
-                }
-                st_fr2(Anew, nnew, 2 * y, A0, A1);
-                {
-                    fr s[4];
-                    ld_fr4(Sold, nold, 4 * y, s);
-                    S0 = fr_add(s[0], fr_mul(rk, fr_sub_lazy(s[1], s[0])));
-                    S1 = fr_add(s[2], fr_mul(rk, fr_sub_lazy(s[3], s[2])));
-                }
-                st_fr2(Snew, nnew, 2 * y, S0, S1);
-            } else {
-                fr a[2], s[2];
-                ld_fr2(Aold, nold, 2 * y, a);
-                ld_fr2(Sold, nold, 2 * y, s);
-                A0 = a[0]; A1 = a[1]; S0 = s[0]; S1 = s[1];
+    for (uint32_t yl = threadIdx.x; yl < G; yl += blockDim.x) {
+        const uint64_t y = (grp << gbits) + yl;
+        fr A0, A1, S0, S1;
+        if (FOLD && GATHER) {
+            const uint4 kq = __ldg(reinterpret_cast<const uint4*>(keys + 4 * y));
+            const uint4 *p0 = TB + 4 * (uint64_t)kq.x, *p1 = TB + 4 * (uint64_t)kq.y;
+            const uint4 *p2 = TB + 4 * (uint64_t)kq.z, *p3 = TB + 4 * (uint64_t)kq.w;
+            {
+                const fr a0v = ld_fr_256(p0), a1v = ld_fr_256(p1), a2v = ld_fr_256(p2), a3v = ld_fr_256(p3);
+                A0 = fr_add(a0v, fr_mul(rk, fr_sub_lazy(a1v, a0v)));
+                A1 = fr_add(a2v, fr_mul(rk, fr_sub_lazy(a3v, a2v)));
             }
-            const fr e = ld_fr_256(elo + yl);
-            c0 = fr_add(c0, fr_mul(e, fr_mul(A0, fr_add_lazy(S0, beta))));
-            cinf = fr_add(cinf, fr_mul(e, fr_mul(fr_sub(A1, A0), fr_sub_lazy(S1, S0))));
-            if (direct_h1) c1 = fr_add(c1, fr_mul(e, fr_mul(A1, fr_add_lazy(S1, beta))));
-            fr_acc_add(a0, A0);
-            fr_acc_add(a1, A1);
+            st_fr2(Anew, nnew, 2 * y, A0, A1);
+            {
+                const fr s0 = ld_fr_256(p0 + 2), s1 = ld_fr_256(p1 + 2), s2 = ld_fr_256(p2 + 2),
+                         s3 = ld_fr_256(p3 + 2);
+                S0 = fr_add(s0, fr_mul(rk, fr_sub_lazy(s1, s0)));
+                S1 = fr_add(s2, fr_mul(rk, fr_sub_lazy(s3, s2)));
+            }
+            st_fr2(Snew, nnew, 2 * y, S0, S1);
+        } else if (FOLD) {
+            {
+                fr a[4];
+                ld_fr4(Aold, nold, 4 * y, a);
+                A0 = fr_add(a[0], fr_mul(rk, fr_sub_lazy(a[1], a[0])));
+                A1 = fr_add(a[2], fr_mul(rk, fr_sub_lazy(a[3], a[2])));
+            }
+            st_fr2(Anew, nnew, 2 * y, A0, A1);
+            {
+                fr sv[4];
+                ld_fr4(Sold, nold, 4 * y, sv);
+                S0 = fr_add(sv[0], fr_mul(rk, fr_sub_lazy(sv[1], sv[0])));
+                S1 = fr_add(sv[2], fr_mul(rk, fr_sub_lazy(sv[3], sv[2])));
+            }
+            st_fr2(Snew, nnew, 2 * y, S0, S1);
+        } else {
+            fr av[2], sv[2];
+            ld_fr2(Aold, nold, 2 * y, av);
+            ld_fr2(Sold, nold, 2 * y, sv);
+            A0 = av[0]; A1 = av[1]; S0 = sv[0]; S1 = sv[1];
         }
-        const fr eh = ehi[grp];
-        H0 = fr_add(H0, fr_mul(eh, c0));
-        Hinf = fr_add(Hinf, fr_mul(eh, cinf));
-        if (direct_h1) H1 = fr_add(H1, fr_mul(eh, c1));
+        const fr e = ld_fr_256(elo + yl);
+        fr_wide_mac(c0, e, fr_mul(A0, fr_add_lazy(S0, beta)));
+        fr_wide_mac(cinf, e, fr_mul(fr_sub(A1, A0), fr_sub_lazy(S1, S0)));
+        if (direct_h1) c1 = fr_add(c1, fr_mul(e, fr_mul(A1, fr_add_lazy(S1, beta))));
+        fr_acc_add(a0, A0);
+        fr_acc_add(a1, A1);
     }
+    const fr eh = ehi[grp];
+    fr H0 = fr_mul(eh, fr_wide_redc(c0));
+    fr Hinf = fr_mul(eh, fr_wide_redc(cinf));
+    fr H1 = direct_h1 ? fr_mul(eh, c1) : fr_zero();
     __shared__ fr scratch[5 * (kRoundThreads / 32)];
     fr v[5] = {H0, H1, Hinf, fr_acc_final(a0), fr_acc_final(a1)};
     block_sum_fr<5>(v, scratch);
@@ -988,11 +1003,14 @@ constexpr int kChunkThreads = 256;
 constexpr uint64_t kChunkMaxElems = 1ull << 17;   // chunk rounds start at the first round with <= 2^17 elements
 constexpr int kChunkWarps = kChunkThreads / 32;   // partial rows per chunk and round: one per warp
 
-__global__ void __launch_bounds__(kChunkThreads, 2)
-k_chunk_rounds(const uint32_t* __restrict__ Ain, const uint32_t* __restrict__ Sin, uint64_t nin,
-               const ProofScalars* __restrict__ sc, int kc, int nrounds, const RoundDesc* __restrict__ rounds,
-               const fr* __restrict__ arena, fr* partials_base, uint32_t* __restrict__ Aout,
-               uint32_t* __restrict__ Sout) {
+// Causal: the chunks are synchronised by a grid barrier (cooperative launch) between writing a round's partial rows
+// and folding with its challenge, so r_k is never used before every CTA has finished its share of g_k (SURVEY.md
+// §8(a6); the challenges being explicit inputs does not change the order the prover commits to).
+__device__ __forceinline__ void
+chunk_rounds_body(const uint32_t* __restrict__ Ain, const uint32_t* __restrict__ Sin, uint64_t nin,
+                  const ProofScalars* __restrict__ sc, int kc, int nrounds, const RoundDesc* __restrict__ rounds,
+                  const fr* __restrict__ arena, fr* partials_base, uint32_t* __restrict__ Aout,
+                  uint32_t* __restrict__ Sout, GridBar* bar) {
     extern __shared__ fr smem_fr[];
     fr* As = smem_fr;
     fr* Ss = smem_fr + kChunk;
@@ -1050,8 +1068,9 @@ k_chunk_rounds(const uint32_t* __restrict__ Ain, const uint32_t* __restrict__ Si
             const uint64_t rows = nchunks * kChunkWarps, row = (uint64_t)blockIdx.x * kChunkWarps + (t >> 5);
 #pragma unroll
             for (int q = 0; q < 5; ++q) part[(uint64_t)q * rows + row] = v[q];
+            __threadfence();
         }
-        __syncthreads();   // every pair of this round has been read
+        grid_sync(bar);   // every chunk's share of g_k is written before any chunk folds with r_k
 #pragma unroll
         for (int c = 0; c < kPer; ++c) {
             const int yl = t + c * nt;
@@ -1067,6 +1086,26 @@ k_chunk_rounds(const uint32_t* __restrict__ Ain, const uint32_t* __restrict__ Si
         st_fr(Aout, nchunks, blockIdx.x, As[0]);
         st_fr(Sout, nchunks, blockIdx.x, Ss[0]);
     }
+}
+
+struct ChunkArgs {
+    const uint32_t* Ain;
+    const uint32_t* Sin;
+    uint64_t nin;
+    const ProofScalars* sc;
+    int kc, nrounds;
+    const RoundDesc* rounds;
+    const fr* arena;
+    fr* partials_base;
+    uint32_t* Aout;
+    uint32_t* Sout;
+    GridBar* bar;
+};
+
+// cooperative launch (the grid barrier needs every chunk CTA resident)
+__global__ void __launch_bounds__(kChunkThreads, 2) k_chunk_rounds_coop(ChunkArgs a) {
+    chunk_rounds_body(a.Ain, a.Sin, a.nin, a.sc, a.kc, a.nrounds, a.rounds, a.arena, a.partials_base, a.Aout, a.Sout,
+                      a.bar);
 }
 
 // ====================================================================== a8: table side

@@ -17,21 +17,26 @@ __device__ __constant__ uint32_t kSha256K[64] = {
 
 __device__ __forceinline__ uint32_t sha_rotr(uint32_t x, int n) { return (x >> n) | (x << (32 - n)); }
 
+// Fully unrolled: the 16-word message schedule window stays in registers and the round constants become immediates
+// (a rolled loop kept w[64] in local memory: the per-round transcript hash was ~5x slower).
 __device__ inline void sha256_block(uint32_t (&h)[8], const uint8_t* blk) {
-    uint32_t w[64];
+    uint32_t w[16];
+#pragma unroll
     for (int i = 0; i < 16; ++i)
         w[i] = ((uint32_t)blk[4 * i] << 24) | ((uint32_t)blk[4 * i + 1] << 16) | ((uint32_t)blk[4 * i + 2] << 8) |
                (uint32_t)blk[4 * i + 3];
-    for (int i = 16; i < 64; ++i) {
-        const uint32_t s0 = sha_rotr(w[i - 15], 7) ^ sha_rotr(w[i - 15], 18) ^ (w[i - 15] >> 3);
-        const uint32_t s1 = sha_rotr(w[i - 2], 17) ^ sha_rotr(w[i - 2], 19) ^ (w[i - 2] >> 10);
-        w[i] = w[i - 16] + s0 + w[i - 7] + s1;
-    }
     uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], k = h[7];
+#pragma unroll
     for (int i = 0; i < 64; ++i) {
+        if (i >= 16) {
+            const uint32_t w15 = w[(i - 15) & 15], w2 = w[(i - 2) & 15];
+            const uint32_t s0 = sha_rotr(w15, 7) ^ sha_rotr(w15, 18) ^ (w15 >> 3);
+            const uint32_t s1 = sha_rotr(w2, 17) ^ sha_rotr(w2, 19) ^ (w2 >> 10);
+            w[i & 15] = w[i & 15] + s0 + w[(i - 7) & 15] + s1;
+        }
         const uint32_t S1 = sha_rotr(e, 6) ^ sha_rotr(e, 11) ^ sha_rotr(e, 25);
         const uint32_t ch = (e & f) ^ (~e & g);
-        const uint32_t t1 = k + S1 + ch + kSha256K[i] + w[i];
+        const uint32_t t1 = k + S1 + ch + kSha256K[i] + w[i & 15];
         const uint32_t S0 = sha_rotr(a, 2) ^ sha_rotr(a, 13) ^ sha_rotr(a, 22);
         const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
         const uint32_t t2 = S0 + mj;
@@ -40,8 +45,8 @@ __device__ inline void sha256_block(uint32_t (&h)[8], const uint8_t* blk) {
     h[0] += a; h[1] += b; h[2] += c; h[3] += d; h[4] += e; h[5] += f; h[6] += g; h[7] += k;
 }
 
-// digest (32 bytes, big-endian words as in FIPS 180-4) of msg[0..len)
-__device__ inline void sha256(const uint8_t* msg, uint32_t len, uint8_t* out) {
+// digest (32 bytes, big-endian words as in FIPS 180-4) of msg[0..len); one out-of-line copy per translation unit
+static __device__ __noinline__ void sha256(const uint8_t* msg, uint32_t len, uint8_t* out) {
     uint32_t h[8] = {0x6a09e667u, 0xbb67ae85u, 0x3c6ef372u, 0xa54ff53au,
                      0x510e527fu, 0x9b05688cu, 0x1f83d9abu, 0x5be0cd19u};
     uint8_t blk[64];

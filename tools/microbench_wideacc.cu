@@ -1,4 +1,4 @@
-// Microbenchmark for the wide accumulation of k_round's eq-weighted sums: a sum of 16 terms,
+// Microbenchmark for the wide accumulation of the eq-weighted sums (csrc/fr.cuh fr_wide_*): 16 terms,
 // c = sum_y e_y X_y R^-1 (mod r), computed two ways on the same inputs:
 //   (a) as in k_round today: 16 Montgomery multiplications fr_mul(e_y, X_y) and 16 modular additions;
 //   (b) 16 schoolbook 256x256 products summed as one 544-bit value W, then the high half brought below r
@@ -15,80 +15,6 @@ using namespace zkl;
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); return 1; } } while (0)
 
 constexpr int kTerms = 16;
-__constant__ uint32_t c_r[8] = {ZKL_R0, ZKL_R1, ZKL_R2, ZKL_R3, ZKL_R4, ZKL_R5, ZKL_R6, ZKL_R7};
-
-// W (17 limbs) += a * b
-__device__ __forceinline__ void wide_mac(uint32_t* W, const fr& a, const fr& b) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        uint64_t carry = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const uint64_t t = (uint64_t)a.v[j] * b.v[i] + W[i + j] + carry;
-            W[i + j] = (uint32_t)t;
-            carry = t >> 32;
-        }
-#pragma unroll
-        for (int k = i + 8; k < 17; ++k) {
-            const uint64_t t = (uint64_t)W[k] + carry;
-            W[k] = (uint32_t)t;
-            carry = t >> 32;
-        }
-    }
-}
-
-// H (9 limbs, the high half W[8..16]) -= m r if H >= m r
-__device__ __forceinline__ void hi_sub_if(uint32_t* H, int shift) {
-    uint32_t mr[9];
-    uint32_t prev = 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        mr[k] = (c_r[k] << shift) | (shift ? prev >> (32 - shift) : 0u);
-        prev = c_r[k];
-    }
-    mr[8] = shift ? prev >> (32 - shift) : 0u;
-    uint32_t d[9];
-    int64_t borrow = 0;
-#pragma unroll
-    for (int k = 0; k < 9; ++k) {
-        const int64_t t = (int64_t)H[k] - mr[k] + borrow;
-        d[k] = (uint32_t)t;
-        borrow = t >> 32;
-    }
-    if (borrow == 0) {
-#pragma unroll
-        for (int k = 0; k < 9; ++k) H[k] = d[k];
-    }
-}
-
-// W < r 2^256 -> W R^-1 mod r (R = 2^256); r' = -r^-1 = -1 mod 2^32 since r0 = 1
-__device__ __forceinline__ fr wide_redc(uint32_t* W) {
-    hi_sub_if(W + 8, 2);
-    hi_sub_if(W + 8, 1);
-    hi_sub_if(W + 8, 0);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const uint32_t q = 0u - W[i];
-        uint64_t carry = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const uint64_t t = (uint64_t)q * c_r[j] + W[i + j] + carry;
-            W[i + j] = (uint32_t)t;
-            carry = t >> 32;
-        }
-#pragma unroll
-        for (int k = i + 8; k < 17; ++k) {
-            const uint64_t t = (uint64_t)W[k] + carry;
-            W[k] = (uint32_t)t;
-            carry = t >> 32;
-        }
-    }
-    fr o;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) o.v[k] = W[8 + k];
-    fr_reduce_once(o);
-    return o;
-}
 
 __device__ __forceinline__ fr term(int seed, int y) {
     fr x = fr_r2();
@@ -109,10 +35,10 @@ __global__ void k_sum(fr* out, int iters) {
     for (int it = 0; it < iters; ++it) {
         fr c, x = x0;
         if (WIDE) {
-            uint32_t W[17] = {0};
+            fr_wide W = fr_wide_zero();
 #pragma unroll
-            for (int y = 0; y < kTerms; ++y) { wide_mac(W, e[y], x); x = fr_add(x, step); }
-            c = wide_redc(W);
+            for (int y = 0; y < kTerms; ++y) { fr_wide_mac(W, e[y], x); x = fr_add(x, step); }
+            c = fr_wide_redc(W);
         } else {
             c = fr_zero();
 #pragma unroll
