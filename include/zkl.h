@@ -204,7 +204,11 @@ int zkl_tlookup_prepare(zkl_ctx* ctx, zkl_vec S_local, uint64_t D, const zkl_tab
 
 /* Function-lookup form of tlookup-Prep (a1 + a3 fused): S_local_out[i] =
  * x_i + alpha_f y_i (int32 device arrays of length D/P; same encoding as zkl_vec_import_pair) is written and
- * counted into m_dev in one pass over x, y.  Same errors as zkl_tlookup_prepare. */
+ * counted into m_dev in one pass over x, y.  Same errors as zkl_tlookup_prepare.
+ * S_local_out.limbs == NULL: S stays VIRTUAL -- only the table index of every lookup is kept (in the workspace);
+ * the following zkl_tlookup_prove / _prove_fs on this context, table and D takes S_local.limbs == NULL and reads
+ * S_i = T_key(i) (and A_i = B_key(i)) from the table instead of a D-sized vector (S is committed homomorphically
+ * as [X] + alpha [Y], so it need not exist in HBM). */
 int zkl_tlookup_prepare_pair(zkl_ctx* ctx, const int32_t* x_dev, const int32_t* y_dev, const zkl_fr* alpha_f,
                              uint64_t D, const zkl_table* T, zkl_vec S_local_out, uint32_t* m_dev,
                              int64_t* err_index);
@@ -217,6 +221,18 @@ int zkl_tlookup_prepare_pair(zkl_ctx* ctx, const int32_t* x_dev, const int32_t* 
 int zkl_tlookup_prove(zkl_ctx* ctx, zkl_vec S_local, uint64_t D, const zkl_table* T, const uint32_t* m_dev,
                       const zkl_challenges* ch, zkl_variant variant, zkl_vec A_local_out, zkl_vec B_out,
                       zkl_fr* round_evals, zkl_final_evals* finals, int64_t* err_index);
+
+/* The whole step from HOST buffers (the end-to-end call of a function lookup): x, y (D/P int32) and
+ * tx, ty (N int32, tx a contiguous range; T_j = tx_j + alpha_f ty_j) are copied to device buffers the context
+ * owns (allocated on first use, freed by zkl_ctx_destroy), then T is imported and indexed (zkl_table_create +
+ * zkl_table_attach_pair), prepare_pair runs with a virtual S, and zkl_tlookup_prove writes round_evals and
+ * finals (host) -- exactly the device-resident step, with the host->device copies inside the call.  Pinned host
+ * memory makes the copies run at the PCIe rate.  m_out (host, N u32) may be NULL.  Errors as the calls it makes;
+ * E_ARG if tx is not a range (use the device-buffer calls with the hash index then).  Synchronous. */
+int zkl_tlookup_prove_pair_host(zkl_ctx* ctx, const int32_t* x_host, const int32_t* y_host, uint64_t D,
+                                const int32_t* tx_host, const int32_t* ty_host, uint64_t N, const zkl_fr* alpha_f,
+                                const zkl_challenges* ch, zkl_variant variant, zkl_fr* round_evals,
+                                zkl_final_evals* finals, uint32_t* m_out, int64_t* err_index);
 
 /* Fiat-Shamir (non-interactive) tlookup-Prove: the same proof, with beta, alpha1, alpha2 = alpha1^2, u and every
  * r_k derived on the device from a SHA-256 transcript: h_0 = SHA256("zkl-fs-v1" || seed ||

@@ -1223,6 +1223,8 @@ int zkl_ctx_wait(zkl_ctx* ctx) {
 void zkl_ctx_destroy(zkl_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
+    if (c->hs.table) zkl_table_destroy(c->hs.table);
+    if (c->hs.buf) cudaFree(c->hs.buf);
     if (c->prof[0].a)
         for (int i = 0; i < 256; ++i) { cudaEventDestroy(c->prof[i].a); cudaEventDestroy(c->prof[i].b); }
     if (c->nccl_comm) zkl_nccl_destroy(c);
@@ -1656,6 +1658,56 @@ int zkl_tlookup_prove(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T, c
     a.ch = ch;
     a.variant = variant;
     return run_proof(ctx, D, a, round_evals, finals, err_index);
+}
+
+int zkl_tlookup_prove_pair_host(zkl_ctx* ctx, const int32_t* x_host, const int32_t* y_host, uint64_t D,
+                                const int32_t* tx_host, const int32_t* ty_host, uint64_t N, const zkl_fr* alpha_f,
+                                const zkl_challenges* ch, zkl_variant variant, zkl_fr* round_evals,
+                                zkl_final_evals* finals, uint32_t* m_out, int64_t* err_index) {
+    int st;
+    if (err_index) *err_index = -1;
+    if ((st = check_ctx(ctx))) return st;
+    if ((st = check_idle(ctx))) return st;
+    if (ctx->async_mode) return set_err(ctx, ZKL_E_STATE, "zkl_tlookup_prove_pair_host: synchronous calls only");
+    if (!x_host || !y_host || !tx_host || !ty_host || !alpha_f) return set_err(ctx, ZKL_E_ARG, "null argument");
+    if ((st = check_shape(ctx, D, N))) return st;
+    const uint64_t Dp = D / ctx->nranks;
+    // owned device buffers: x, y (Dp int32), tx, ty (N int32), T (SoA, N), table memory, m (N u32)
+    const size_t o_x = 0, o_y = align_up(4 * Dp), o_tx = o_y + align_up(4 * Dp), o_ty = o_tx + align_up(4 * N),
+                 o_T = o_ty + align_up(4 * N), o_tab = o_T + soa_bytes(N), o_m = o_tab + align_up(zkl_table_bytes(N)),
+                 total = o_m + align_up(4 * N);
+    if (ctx->hs.bytes < total) {
+        if (ctx->hs.table) { zkl_table_destroy(ctx->hs.table); ctx->hs.table = nullptr; }
+        if (ctx->hs.buf) { CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream)); cudaFree(ctx->hs.buf); ctx->hs.buf = nullptr; }
+        ctx->hs.bytes = 0;
+        CUDA_TRY(ctx, cudaMalloc(&ctx->hs.buf, total));
+        ctx->hs.bytes = total;
+    }
+    uint8_t* b = reinterpret_cast<uint8_t*>(ctx->hs.buf);
+    int32_t *xd = reinterpret_cast<int32_t*>(b + o_x), *yd = reinterpret_cast<int32_t*>(b + o_y);
+    int32_t *txd = reinterpret_cast<int32_t*>(b + o_tx), *tyd = reinterpret_cast<int32_t*>(b + o_ty);
+    uint32_t* md = reinterpret_cast<uint32_t*>(b + o_m);
+    CUDA_TRY(ctx, cudaMemcpyAsync(xd, x_host, 4 * Dp, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpyAsync(yd, y_host, 4 * Dp, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpyAsync(txd, tx_host, 4 * N, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpyAsync(tyd, ty_host, 4 * N, cudaMemcpyHostToDevice, ctx->stream));
+    zkl_vec T{reinterpret_cast<uint32_t*>(b + o_T), N};
+    if ((st = zkl_vec_import_pair(ctx, txd, tyd, alpha_f, T))) return st;
+    if (ctx->hs.table) { zkl_table_destroy(ctx->hs.table); ctx->hs.table = nullptr; }
+    if ((st = zkl_table_create(ctx, T, b + o_tab, zkl_table_bytes(N), &ctx->hs.table, err_index))) return st;
+    if ((st = zkl_table_attach_pair(ctx, ctx->hs.table, txd, tyd, alpha_f))) return st;
+    zkl_vec Sv{nullptr, Dp};
+    if ((st = zkl_tlookup_prepare_pair(ctx, xd, yd, alpha_f, D, ctx->hs.table, Sv, md, err_index))) return st;
+    zkl_vec none{nullptr, 0};
+    if ((st = zkl_tlookup_prove(ctx, Sv, D, ctx->hs.table, md, ch, variant, zkl_vec{nullptr, Dp}, zkl_vec{nullptr, N},
+                                round_evals, finals, err_index)))
+        return st;
+    (void)none;
+    if (m_out) {
+        CUDA_TRY(ctx, cudaMemcpyAsync(m_out, md, 4 * N, cudaMemcpyDeviceToHost, ctx->stream));
+        return sync_stream(ctx);
+    }
+    return ZKL_OK;
 }
 
 int zkl_tlookup_prove_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T, const uint32_t* m_dev,

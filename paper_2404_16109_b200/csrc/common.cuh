@@ -233,6 +233,12 @@ struct zkl_ctx {
     int async_mode;
     int pend_prepare, pend_prove;
     void* pending;                 // std::vector<std::function<int()>>*
+    // zkl_tlookup_prove_pair_host: device copies of the host inputs, the table and m (owned, grown on demand)
+    struct HostStep {
+        void* buf;           // x | y | tx | ty | T (SoA) | table memory | m
+        size_t bytes;
+        zkl_table* table;
+    } hs;
     // optional per-kernel timing (zkl_ctx_set_profiling): events around every launch
     int profiling;
     int nprof;

@@ -112,6 +112,9 @@ def lib() -> ctypes.CDLL:
             "zkl_tlookup_prove_fs": ([P, zkl_vec, U64, P, P, ctypes.c_char_p, I32, zkl_vec, zkl_vec,
                                       ctypes.POINTER(zkl_fr), ctypes.POINTER(zkl_final_evals), ctypes.POINTER(zkl_fr),
                                       I64P], I32),
+            "zkl_tlookup_prove_pair_host": ([P, P, P, U64, P, P, U64, ctypes.POINTER(zkl_fr),
+                                             ctypes.POINTER(zkl_challenges), I32, ctypes.POINTER(zkl_fr),
+                                             ctypes.POINTER(zkl_final_evals), P, I64P], I32),
             "zkl_sumcheck_prove": ([P, zkl_vec, zkl_vec, U64, zkl_vec, zkl_vec, zkl_vec,
                                     ctypes.POINTER(zkl_challenges), I32, ctypes.POINTER(zkl_fr),
                                     ctypes.POINTER(zkl_final_evals)], I32),
@@ -133,7 +136,7 @@ EXPORTED = ["zkl_strerror", "zkl_ctx_create", "zkl_nccl_unique_id", "zkl_ctx_cre
             "zkl_hyrax_commit", "zkl_hyrax_prove_eval",
             "zkl_vec_import", "zkl_vec_import_i64", "zkl_vec_import_pair", "zkl_vec_export", "zkl_table_bytes",
             "zkl_table_create", "zkl_table_destroy", "zkl_tlookup_prepare", "zkl_tlookup_prepare_pair",
-            "zkl_tlookup_prove", "zkl_tlookup_prove_fs",
+            "zkl_tlookup_prove", "zkl_tlookup_prove_fs", "zkl_tlookup_prove_pair_host",
             "zkl_sumcheck_prove"]
 
 
@@ -447,6 +450,32 @@ class Context:
         if self._async:
             return self._defer(err, make)
         return make()
+
+    def prove_pair_host(self, x, y, tx, ty, alpha_f: int, D: int, ch, variant: int = PAPER, want_m: bool = False):
+        """The end-to-end step from HOST int32 buffers (numpy arrays or CPU torch tensors, ideally pinned):
+        zkl_tlookup_prove_pair_host copies them into context-owned device memory, builds the table and proves with a
+        virtual S.  Returns Proof (and m as a numpy array if want_m)."""
+        def hptr(a):
+            if hasattr(a, "data_ptr"):
+                assert not a.is_cuda and a.dtype == self.torch.int32 and a.is_contiguous()
+                return ctypes.c_void_p(a.data_ptr()), a.numel()
+            a = np.ascontiguousarray(a, dtype=np.int32)
+            hptr.keep.append(a)
+            return ctypes.c_void_p(a.ctypes.data), a.size
+        hptr.keep = []
+        (px, nx), (py, _), (ptx, N), (pty, _) = hptr(x), hptr(y), hptr(tx), hptr(ty)
+        d = D.bit_length() - 1
+        evals = (zkl_fr * (4 * max(d, 1)))()
+        fin = zkl_final_evals()
+        err = ctypes.c_int64(-1)
+        af = fr_from_int(alpha_f % R_MODULUS)
+        mh = np.zeros(N, dtype=np.uint32) if want_m else None
+        st = lib().zkl_tlookup_prove_pair_host(self.h, px, py, D, ptx, pty, N, ctypes.byref(af), ctypes.byref(ch),
+                                               variant, evals, ctypes.byref(fin),
+                                               ctypes.c_void_p(mh.ctypes.data) if want_m else None, ctypes.byref(err))
+        self._check(st, err.value)
+        pf = Proof(_evals(evals, d), _finals(fin))
+        return (pf, mh) if want_m else pf
 
     def prove_fs(self, S: Vec, D: int, tab: "Table", m, seed: bytes, variant: int = PAPER, want_A: bool = False,
                  want_B: bool = False):

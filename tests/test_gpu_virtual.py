@@ -172,3 +172,16 @@ def test_bench_step_at_H_matches_golden():
     finally:
         ctx.close()
         torch.cuda.set_stream(torch.cuda.default_stream(dev))
+
+
+@pytest.mark.parametrize("d,n", [(12, 8), (20, 16)])
+def test_prove_pair_host_matches_oracle(ctx, d, n):
+    """The end-to-end entry point from host buffers (zkl_tlookup_prove_pair_host) against the oracle."""
+    x, y, tx, ty, ch = _pair_workload(d, n, 31 + d)
+    D, N = 1 << d, 1 << n
+    chal = C.chal_array(ch.beta, ch.alpha1, ch.alpha2, ch.u, ch.r)
+    ref = C.prove_pair_stream(x, y, tx, ty, ch.alpha_f, chal, TL.PAPER, 2)
+    ctx.reserve(D, N)
+    pf, m = ctx.prove_pair_host(x, y, tx, ty, ch.alpha_f, D, _chal(ch), TL.PAPER, want_m=True)
+    assert np.array_equal(m, ref.m)
+    assert pf.evals == ref.evals and pf.finals == ref.finals
