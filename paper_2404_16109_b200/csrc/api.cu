@@ -1698,11 +1698,9 @@ int zkl_tlookup_prove_pair_host(zkl_ctx* ctx, const int32_t* x_host, const int32
     if ((st = zkl_table_attach_pair(ctx, ctx->hs.table, txd, tyd, alpha_f))) return st;
     zkl_vec Sv{nullptr, Dp};
     if ((st = zkl_tlookup_prepare_pair(ctx, xd, yd, alpha_f, D, ctx->hs.table, Sv, md, err_index))) return st;
-    zkl_vec none{nullptr, 0};
     if ((st = zkl_tlookup_prove(ctx, Sv, D, ctx->hs.table, md, ch, variant, zkl_vec{nullptr, Dp}, zkl_vec{nullptr, N},
                                 round_evals, finals, err_index)))
         return st;
-    (void)none;
     if (m_out) {
         CUDA_TRY(ctx, cudaMemcpyAsync(m_out, md, 4 * N, cudaMemcpyDeviceToHost, ctx->stream));
         return sync_stream(ctx);

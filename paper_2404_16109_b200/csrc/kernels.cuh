@@ -743,7 +743,6 @@ k_round(const uint32_t* __restrict__ Aold, const uint32_t* __restrict__ Sold, ui
     const fr& beta = sh_beta;
     const fr& rk = sh_rk;
 #endif
-    const uint64_t npairs = FOLD ? nold / 4 : nold / 2;   // pairs of the round being evaluated
     const uint64_t nnew = nold / 2;
     const uint32_t G = 1u << gbits;
     // one group of G pairs per CTA (grid = #groups): each thread accumulates its G/256 <= 64 E_lo-weighted terms
