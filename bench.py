@@ -214,6 +214,7 @@ def main():
     ap.add_argument("--impl", default="zkl", choices=["zkl", "reference"])
     ap.add_argument("--log2d", type=int, default=26, help="log2 of the global lookup count (default: H, 2^26)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fs", action="store_true", help="skip the Fiat-Shamir step")
     ap.add_argument("--variant", type=int, default=0)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -253,7 +254,7 @@ def main():
     tmem = ctx.table_mem(N)
     m = torch.empty(N, dtype=torch.int32, device=dev)
 
-    use_async = world == 1   # async mode is single-rank: the histogram overlaps the proof
+    use_async = True   # the histogram overlaps the proof; at P > 1 its all-reduce follows it
 
     def step(xs, ys, txs, tys):
         # a1 (T) + a2, then a1 (S) fused with a3 (zkl_tlookup_prepare_pair), then a4-a9
@@ -311,7 +312,7 @@ def main():
 
     # ---------------- Fiat-Shamir mode (f1, single rank): the same step with challenges derived on the device
     fs_ms = None
-    if world == 1:
+    if not args.no_fs:   # every P: one all-gather of the round sums per local round at P > 1
         seed = bytes(32)
 
         def step_fs():
@@ -323,6 +324,7 @@ def main():
 
         step_fs()
         torch.cuda.synchronize(dev)
+        barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for _ in range(args.steps):
@@ -330,6 +332,10 @@ def main():
         f1.record(stream)
         torch.cuda.synchronize(dev)
         fs_ms = f0.elapsed_time(f1) / args.steps
+        if world > 1:
+            t = torch.tensor([fs_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            fs_ms = float(t.item())
 
     # ---------------- e2e through the library's host-buffer entry point (zkl_tlookup_prove_pair_host): every step
     # copies X, Y, T_X, T_Y from pinned host memory into context-owned device buffers, builds the table, proves and

@@ -708,6 +708,8 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
     }
     const fr* gathered = rank_sums;
     if (ctx->nranks > 1) {
+        // a pending (async) prepare's collectives run on the low stream: order this proof's after them
+        if (ctx->m_pending) CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_m, 0));
         int rc = zkl_dist_exchange(ctx, p.dl, rank_sums, gath, fin, at<fr>(ctx, p.o_gfin));
         if (rc) return rc;
         gathered = gath;
@@ -726,6 +728,10 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
     CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
     LAUNCH(ctx, k_derive, 1, 64, 0, s, gathered, ctx->nranks, p.dl, repl, rounds, tsum, sc, rc, p.d, p.n,
            a.variant, a.prove_mode ? 1 : 0, fin, tfin, out);
+    if (ctx->nranks > 1) {   // every rank sees the smallest error index of any rank (device-side, no host sync)
+        int rc = zkl_dist_min_u64_dev(ctx, err, 3);
+        if (rc) return rc;
+    }
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->host_out, out, sizeof(ProofOut), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(ctx, cudaMemcpyAsync((uint8_t*)ctx->host_out + offsetof(ProofOut, err_index), err,
                                   3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
@@ -749,12 +755,7 @@ int proof_collect(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_ev
     const ProofOut* ho = reinterpret_cast<const ProofOut*>(ctx->host_out);
     const unsigned long long* he = reinterpret_cast<const unsigned long long*>((const uint8_t*)ctx->host_out +
                                                                                offsetof(ProofOut, err_index));
-    unsigned long long eS = he[0], eT = he[1], eMiss = gather ? he[2] : ~0ull;
-    if (ctx->nranks > 1) {
-        int rc = zkl_dist_min_u64(ctx, &eS);
-        if (rc) return rc;
-        if (gather && (rc = zkl_dist_min_u64(ctx, &eMiss))) return rc;
-    }
+    const unsigned long long eS = he[0], eT = he[1], eMiss = gather ? he[2] : ~0ull;   // already min over ranks
     if (eMiss != ~0ull && eT == ~0ull) {
         // an S_i with no table entry (S was not the prepared lookup vector): redo with the inversion path
         // (synchronously, also in async mode: this runs inside zkl_ctx_wait)
@@ -796,13 +797,16 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
     int st;
     const uint64_t N = table->N;
     if ((st = check_shape(ctx, D, N))) return st;
-    if (D < 2) return set_err(ctx, ZKL_E_SHAPE, "Fiat-Shamir mode needs D >= 2");
-    if (ctx->nranks != 1) return set_err(ctx, ZKL_E_ARG, "Fiat-Shamir mode: single rank only (this build)");
+    if (D < 2 || D / ctx->nranks < 2)
+        return set_err(ctx, ZKL_E_SHAPE, "Fiat-Shamir mode needs D >= 2 and D_local >= 2");
     if (!seed || !m_dev || !round_evals || !finals || !derived) return set_err(ctx, ZKL_E_ARG, "null argument");
     std::vector<zkl_fr> u1(kMaxRounds);
     for (auto& x : u1) { memset(&x, 0, sizeof(x)); x.w[0] = 1; }
     Plan p;
-    make_plan(p, D, N, 1, 0, true, u1.data(), true);
+    make_plan(p, D, N, ctx->nranks, ctx->rank, true, u1.data(), true);
+    const int P = ctx->nranks;
+    fr* rank_sums = at<fr>(ctx, p.o_rank);   // P > 1: this rank's sums of the current round (5 fr)
+    fr* gath = at<fr>(ctx, p.o_gath);        // P > 1: the ranks' sums of the current round, rank-major (P x 5 fr)
     if ((st = need_ws(ctx, p))) return st;
     const bool virt = S.limbs == nullptr;
     const bool keys_ok = ctx->prep_valid && ctx->prep_S == S.limbs && ctx->prep_n == p.Dp && ctx->prep_table == table;
@@ -840,7 +844,7 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
                         {sizeof(hs->seed), sizeof(hs->rounds), sizeof(hs->jobs)})))
         return st;
     CUDA_TRY(ctx, cudaMemsetAsync(err, 0xff, 4 * sizeof(unsigned long long), s));
-    LAUNCH(ctx, k_fs_init, 1, 1, 0, s, dseed, D, N, variant, p.d, sc, fst, dder);
+    LAUNCH(ctx, k_fs_init, 1, 1, 0, s, dseed, D, N, variant, p.d, sc, fst, dder, p.pbits, p.rank);
     LAUNCH(ctx, k_eq_fill, grid_for(p.arena, 256), 256, 0, s, jobs, p.njobs, p.arena, sc, arena);
     // ---- B = 1/(beta + T) and the table working vectors
     uint32_t* tB = at<uint32_t>(ctx, p.o_tB);
@@ -934,14 +938,22 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
         // single-CTA derivation below (on the critical path of every round) does not sum 16K rows
         const fr* r1 = partials + p.rd[0].part_base;
         uint32_t r1rows = p.rd[0].nblocks;
-        if (r1rows > 256) {
-            fr* folded = at<fr>(ctx, p.o_rank);   // kMaxRounds x kSlots fr >= 5 x 32
-            LAUNCH(ctx, k_rows_fold, 32, 256, 0, s, r1, r1rows, folded, 32u);
-            r1 = folded;
-            r1rows = 32;
+        if (P > 1) {
+            // the rank's round-1 sums, all-gathered: every rank derives g_1 and r_1 from the same global sums
+            LAUNCH(ctx, k_rows_fold, 1, 256, 0, s, r1, r1rows, rank_sums, 1u);
+            if ((st = zkl_dist_allgather(ctx, rank_sums, gath, kSlots * sizeof(fr)))) return st;
+            LAUNCH(ctx, k_fs_round, 1, 256, 0, s, 1, p.d, p.n, variant, gath, (uint32_t)P, h01, tpart,
+                   p.n >= 1 ? p.tnb[0] : 0u, tfin, sc, fst, out, dder, 0, err + 2, 1u, (uint32_t)kSlots);
+        } else {
+            if (r1rows > 256) {
+                fr* folded = at<fr>(ctx, p.o_rank);   // kMaxRounds x kSlots fr >= 5 x 32
+                LAUNCH(ctx, k_rows_fold, 32, 256, 0, s, r1, r1rows, folded, 32u);
+                r1 = folded;
+                r1rows = 32;
+            }
+            LAUNCH(ctx, k_fs_round, 1, 256, 0, s, 1, p.d, p.n, variant, r1, r1rows, h01, tpart,
+                   p.n >= 1 ? p.tnb[0] : 0u, tfin, sc, fst, out, dder, 0, err + 2, r1rows, 1u);
         }
-        LAUNCH(ctx, k_fs_round, 1, 256, 0, s, 1, p.d, p.n, variant, r1, r1rows, h01, tpart,
-               p.n >= 1 ? p.tnb[0] : 0u, tfin, sc, fst, out, dder, 0, err + 2);
     }
     // ---- rounds 2..d
     const uint32_t *cA = Abuf, *cS = Sin;
@@ -986,7 +998,20 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
             if (k <= p.n) LAUNCH(ctx, k_tab_eval, p.tnb[k - 1], 256, 0, ctx->side, tcur, tlen, sc, variant, tpart);
             CUDA_TRY(ctx, cudaEventRecord(ctx->ev_join, ctx->side));
         }
-        if (k == 2 && r2_gather) {
+        if (k == p.dl + 1) {
+            // the local rounds are done: fold the rank's last pair with r_dl, all-gather the P folded (A, S), and run
+            // the last log2 P rounds identically on every rank on the gathered vectors (replicated, no exchange)
+            LAUNCH(ctx, k_fold_final, 1, 32, 0, s, cA, cS, len, sc, p.dl, fin);
+            fr* g2 = gath + (size_t)P * kSlots;
+            if ((st = zkl_dist_allgather(ctx, fin, g2, 2 * sizeof(fr)))) return st;
+            uint32_t* gfin = reinterpret_cast<uint32_t*>(at<fr>(ctx, p.o_gfin));
+            LAUNCH(ctx, k_pairs_to_soa, 1, 32, 0, s, g2, P, gfin);
+            cA = gfin;
+            cS = gfin + 8 * (size_t)P;
+            len = (uint64_t)P;
+            LAUNCH(ctx, (k_round<false, true>), r.nblocks, kRoundThreads, 0, s, cA, cS, len, nullptr, nullptr, sc, k,
+                   arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, partials + r.part_base);
+        } else if (k == 2 && r2_gather) {
             const uint32_t* keys = at<uint32_t>(ctx, p.o_keys);
             const uint4* TB = at<uint4>(ctx, p.o_tBaos);
             if (derive)
@@ -1001,17 +1026,28 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
         else
             LAUNCH(ctx, (k_round<true, true>), r.nblocks, kRoundThreads, 0, s, cA, cS, len, nA, nS, sc, k,
                    arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, partials + r.part_base);
-        cA = nA; cS = nS;
-        len /= 2;
+        if (k != p.dl + 1) {
+            cA = nA; cS = nS;
+            len /= 2;
+        }
         if (side) CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
-        LAUNCH(ctx, k_fs_round, 1, 256, 0, s, k, p.d, p.n, variant, partials + r.part_base, r.nblocks, 0, tpart,
-               k <= p.n ? p.tnb[k - 1] : 0u, tfin, sc, fst, out, dder, derive ? 1 : 0, err + 2);
+        if (P > 1 && k <= p.dl) {   // a local round: its sums become global with one small all-gather
+            LAUNCH(ctx, k_rows_fold, 1, 256, 0, s, partials + r.part_base, r.nblocks, rank_sums, 1u);
+            if ((st = zkl_dist_allgather(ctx, rank_sums, gath, kSlots * sizeof(fr)))) return st;
+            LAUNCH(ctx, k_fs_round, 1, 256, 0, s, k, p.d, p.n, variant, gath, (uint32_t)P, 0, tpart,
+                   k <= p.n ? p.tnb[k - 1] : 0u, tfin, sc, fst, out, dder, derive ? 1 : 0, err + 2, 1u,
+                   (uint32_t)kSlots);
+        } else {
+            LAUNCH(ctx, k_fs_round, 1, 256, 0, s, k, p.d, p.n, variant, partials + r.part_base, r.nblocks, 0, tpart,
+                   k <= p.n ? p.tnb[k - 1] : 0u, tfin, sc, fst, out, dder, derive ? 1 : 0, err + 2, r.nblocks, 1u);
+        }
     }
     if (!coop_done) {
         LAUNCH(ctx, k_fold_final, 1, 32, 0, s, cA, cS, len, sc, p.d, fin);
         if (p.n == p.d) LAUNCH(ctx, k_tab_fold, 1, 32, 0, s, tcur, tlen, tnxt, sc, p.d, tfin);
     }
     LAUNCH(ctx, k_fs_finish, 1, 32, 0, s, fin, tfin, out);
+    if (P > 1 && (st = zkl_dist_min_u64_dev(ctx, err, 3))) return st;
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->host_out, out, sizeof(ProofOut), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(ctx, cudaMemcpyAsync((uint8_t*)ctx->host_out + offsetof(ProofOut, err_index), err,
                                   3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
@@ -1194,7 +1230,8 @@ int zkl_ctx_create_loopback(int device, void* cuda_stream, zkl_group* group, int
 
 int zkl_ctx_set_async(zkl_ctx* ctx, int on) {
     if (!ctx) return ZKL_E_ARG;
-    if (on && ctx->nranks > 1) return set_err(ctx, ZKL_E_ARG, "async mode: single-rank contexts only");
+    // P > 1: allowed with NCCL (the prepare's histogram and its all-reduce go to the low-priority stream); the
+    // loopback communicator synchronises the host inside every collective, so its prepare stays synchronous
     if (!on && (ctx->pend_prepare || ctx->pend_prove)) return set_err(ctx, ZKL_E_STATE, "pending work: zkl_ctx_wait first");
     ctx->async_mode = on ? 1 : 0;
     return ZKL_OK;
@@ -1548,7 +1585,7 @@ static int prepare_impl(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T,
     const int key_bits = std::max(1, p.n + (p.Dp < (uint64_t)kHistTile ? 1 : 0));
     // async mode (single rank): the histogram runs on the low-priority stream, overlapping the proof that follows
     // (which needs m only for the table side: it waits for ev_m there; zkl_ctx_wait orders the ctx stream after it)
-    const bool hist_low = ctx->async_mode && ctx->nranks == 1;
+    const bool hist_low = ctx->async_mode && !ctx->group;
     cudaStream_t hs = ctx->stream;
     if (hist_low) {
         CUDA_TRY(ctx, cudaEventRecord(ctx->ev_keys, ctx->stream));
@@ -1559,16 +1596,23 @@ static int prepare_impl(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T,
     const int hrows = hist_low ? std::min(p.hist_rows, kHistAsyncRows) : p.hist_rows;
     LAUNCH(ctx, k_hist_count, hrows, kHistThreads, 0, hs, keys, p.Dp, (uint32_t)T->N, rows, key_bits);
     LAUNCH(ctx, k_hist_colsum, grid_for(T->N, 256), 256, 0, hs, rows, hrows, T->N, m_dev);
+    unsigned long long* herr = reinterpret_cast<unsigned long long*>((uint8_t*)ctx->host_out + 60000);
+    {
+        // the collectives follow the histogram on its stream (NCCL calls of one communicator stay in one order)
+        cudaStream_t cs = hist_low ? ctx->low : ctx->stream;
+        cudaStream_t main_s = ctx->stream;
+        ctx->stream = cs;   // the dist helpers enqueue on ctx->stream
+        int rc = ZKL_OK;
+        if (ctx->nranks > 1) rc = zkl_dist_allreduce_u32(ctx, m_dev, T->N);
+        if (!rc && ctx->nranks > 1) rc = zkl_dist_min_u64_dev(ctx, err, 2);   // NOT_IN_TABLE index, range miss
+        ctx->stream = main_s;
+        if (rc) return rc;
+        CUDA_TRY(ctx, cudaMemcpyAsync(herr, err, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, cs));
+    }
     if (hist_low) {
         CUDA_TRY(ctx, cudaEventRecord(ctx->ev_m, ctx->low));
         ctx->m_pending = 1;
     }
-    if (ctx->nranks > 1) {
-        int rc = zkl_dist_allreduce_u32(ctx, m_dev, T->N);
-        if (rc) return rc;
-    }
-    unsigned long long* herr = reinterpret_cast<unsigned long long*>((uint8_t*)ctx->host_out + 60000);
-    CUDA_TRY(ctx, cudaMemcpyAsync(herr, err, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
     PrepArgs pa;
     memset(&pa, 0, sizeof(pa));
     pa.S = S; pa.D = D; pa.T = T; pa.m_dev = m_dev; pa.err_index = err_index;
@@ -1598,12 +1642,7 @@ static int prepare_impl(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T,
 
 static int prepare_collect(zkl_ctx* ctx, const PrepArgs& a, uint64_t Dp, bool range_path) {
     const unsigned long long* he = reinterpret_cast<const unsigned long long*>((const uint8_t*)ctx->host_out + 60000);
-    unsigned long long e = he[0], miss = he[1];
-    if (ctx->nranks > 1) {
-        int rc = zkl_dist_min_u64(ctx, &e);
-        if (rc) return rc;
-        if (range_path && (rc = zkl_dist_min_u64(ctx, &miss))) return rc;
-    }
+    const unsigned long long e = he[0], miss = he[1];   // already min over ranks (device-side all-reduce)
     if (range_path && miss != ~0ull) {
         // some (x, y) is not (x0 + j, ty_j): redo with the exact hash index (NOT_IN_TABLE, or an entry that a
         // special alpha made equal), synchronously

@@ -67,7 +67,7 @@ __device__ inline zkl_fr fs_canon_out(const fr& c) {
 
 // derive beta, alpha1, alpha2, u into sc (Montgomery) and `derived` (canonical: beta, alpha1, alpha2, u[d], r[d])
 __global__ void k_fs_init(const uint8_t* __restrict__ seed, uint64_t D, uint64_t N, int variant, int d,
-                          ProofScalars* sc, FsState* st, zkl_fr* derived) {
+                          ProofScalars* sc, FsState* st, zkl_fr* derived, int pbits, int rank) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     uint8_t msg[9 + 32 + 8 + 8 + 4];
     const char* tag = "zkl-fs-v1";
@@ -93,7 +93,13 @@ __global__ void k_fs_init(const uint8_t* __restrict__ seed, uint64_t D, uint64_t
         sc->u[c] = fr_to_mont(u);
         derived[3 + c] = fs_canon_out(u);
     }
-    sc->rank_eq = fr_one();
+    // this rank's factor of e~(u, .): eq(u[0:log2 P], bits(rank)) (the top coordinates are the rank)
+    fr re = fr_one();
+    for (int b = 0; b < pbits; ++b) {
+        const bool bit = (rank >> (pbits - 1 - b)) & 1;
+        re = fr_mul(re, bit ? sc->u[b] : fr_sub(fr_one(), sc->u[b]));
+    }
+    sc->rank_eq = re;
     st->C = fr_one();
     st->tscale = fr_one();
 }
@@ -172,15 +178,18 @@ __global__ void k_rows_fold(const fr* __restrict__ part, uint32_t nrows, fr* out
 // derive_h1: the round's k_round did not sum H(1) (k_round<true, false>); it follows from the running claim,
 // H(1) = (g_{k-1}(r_{k-1}) - cl0 H(0) - a0 - a1 - tab(0) - tab(1)) / cl1.  cl1 = 0 with alpha1 C_k != 0 (u_{d-k} = 0,
 // probability ~2^-255) cannot be derived: the proof is flagged through `miss` and redone with H(1) summed.
+// part: the round's D-side rows; element (slot q, row b) at part[q * slot_stride + b * row_stride] (partial rows:
+// slot-major, slot_stride = nrows, row_stride = 1; P > 1: the all-gathered rank sums, rank-major, 1 and kSlots).
 __global__ void k_fs_round(int k, int d, int n, int variant, const fr* __restrict__ part, uint32_t nrows,
                            int h01_one, const fr* __restrict__ tpart, uint32_t tnb, const fr* __restrict__ tfin,
                            ProofScalars* sc, FsState* st, ProofOut* out, zkl_fr* derived, int derive_h1,
-                           unsigned long long* miss) {
+                           unsigned long long* miss, uint32_t slot_stride, uint32_t row_stride) {
     __shared__ fr scratch[5 * 8];
     fr s[5];
     for (int q = 0; q < 5; ++q) {
         s[q] = fr_zero();
-        for (uint32_t b = threadIdx.x; b < nrows; b += blockDim.x) s[q] = fr_add(s[q], part[(uint64_t)q * nrows + b]);
+        for (uint32_t b = threadIdx.x; b < nrows; b += blockDim.x)
+            s[q] = fr_add(s[q], part[(uint64_t)q * slot_stride + (uint64_t)b * row_stride]);
     }
     block_sum_fr<5>(s, scratch);
     fr tab[4] = {fr_zero(), fr_zero(), fr_zero(), fr_zero()};

@@ -3,11 +3,14 @@
 // one already mapped in the process and dlopen returns it.
 //
 // Collectives of one proof:
-//   prepare: ncclAllReduce(u32, sum) of m (N entries) + ncclAllReduce(u64, min) of the error index;
+//   prepare: ncclAllReduce(u32, sum) of m (N entries) + ncclAllReduce(u64, min) of the error words, both on
+//            the device (no host round trip);
 //   prove:   ONE ncclAllGather of this rank's per-round sums {H0, H1, Hinf, a0, a1} for all local
 //            rounds (Fr cannot be added by NCCL; the device sums the gathered rows mod r in k_derive),
 //            ONE ncclAllGather of the rank's fully folded (A, S) for the last log2 P rounds, which every
-//            rank then runs identically (replicated tail), + an error-index min.
+//            rank then runs identically (replicated tail), + a device-side min of the error words.
+//   Fiat-Shamir prove: one small ncclAllGather per local round (r_k depends on g_k, so each round's sums must be
+//            global before r_k is derived), identically on every rank.
 // The per-round sums are exchanged after the local rounds rather than between them: with the challenges
 // passed in explicitly (north star) no local round depends on an earlier round's sums, so the P-way
 // exchange of all rounds costs one collective.
@@ -119,6 +122,12 @@ int nccl_allreduce_u32(zkl_ctx* ctx, uint32_t* buf, uint64_t n) {
     return ZKL_OK;
 }
 
+// element-wise min over ranks of n device u64 words, in place on the ctx stream (error indices: no host round trip)
+int nccl_allreduce_min_u64_dev(zkl_ctx* ctx, unsigned long long* d, int n) {
+    NCCL_TRY(ctx, nccl().AllReduce(d, d, (size_t)n, ncclUint64, ncclMin, (ncclComm_t)ctx->nccl_comm, ctx->stream));
+    return ZKL_OK;
+}
+
 // min over ranks of a host u64 (uses the pinned host page + a device word)
 int nccl_min_u64(zkl_ctx* ctx, unsigned long long* v) {
     unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->dscratch + 16);
@@ -192,6 +201,30 @@ int lb_allreduce_u32(zkl_ctx* ctx, uint32_t* buf, uint64_t n) {
     return ZKL_OK;
 }
 
+__global__ void k_min_rows_u64(const unsigned long long* __restrict__ rows, int nrows, int n, unsigned long long* out) {
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        unsigned long long v = ~0ull;
+        for (int r = 0; r < nrows; ++r) v = rows[(size_t)r * n + j] < v ? rows[(size_t)r * n + j] : v;
+        out[j] = v;
+    }
+}
+
+int lb_allreduce_min_u64_dev(zkl_ctx* ctx, unsigned long long* d, int n) {
+    zkl_group* g = ctx->group;
+    const size_t bytes = (size_t)n * sizeof(unsigned long long);
+    if ((size_t)g->nranks * bytes > g->staging_bytes) return ZKL_E_OOM;
+    if (cudaMemcpyAsync(g->staging + (size_t)ctx->rank * bytes, d, bytes, cudaMemcpyDeviceToDevice, ctx->stream) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+        return ZKL_E_CUDA;
+    lb_barrier(g);
+    k_min_rows_u64<<<1, 32, 0, ctx->stream>>>(reinterpret_cast<const unsigned long long*>(g->staging), g->nranks, n, d);
+    ctx->launches++;
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return ZKL_E_CUDA;
+    lb_barrier(g);
+    return ZKL_OK;
+}
+
 int lb_min_u64(zkl_ctx* ctx, unsigned long long* v) {
     zkl_group* g = ctx->group;
     {
@@ -228,6 +261,15 @@ int zkl_dist_exchange(zkl_ctx* ctx, int dl, const zkl::fr* rank_sums, zkl::fr* g
 }
 int zkl_dist_allreduce_u32(zkl_ctx* ctx, uint32_t* buf, uint64_t n) {
     return ctx->group ? lb_allreduce_u32(ctx, buf, n) : nccl_allreduce_u32(ctx, buf, n);
+}
+// every rank's `bytes` (a multiple of 4) at src -> dst, rank-major, on the ctx stream
+int zkl_dist_allgather(zkl_ctx* ctx, const void* src, void* dst, size_t bytes) {
+    if (ctx->group) return lb_allgather(ctx, src, dst, bytes);
+    NCCL_TRY(ctx, nccl().AllGather(src, dst, bytes / 4, ncclUint32, (ncclComm_t)ctx->nccl_comm, ctx->stream));
+    return ZKL_OK;
+}
+int zkl_dist_min_u64_dev(zkl_ctx* ctx, unsigned long long* d, int n) {
+    return ctx->group ? lb_allreduce_min_u64_dev(ctx, d, n) : nccl_allreduce_min_u64_dev(ctx, d, n);
 }
 int zkl_dist_min_u64(zkl_ctx* ctx, unsigned long long* v) {
     return ctx->group ? lb_min_u64(ctx, v) : nccl_min_u64(ctx, v);

@@ -149,3 +149,130 @@ def test_loopback_pair_range_prepare(bad):
         ref = np.bincount(x.astype(np.int64) + 128, minlength=N)
         for r in res:
             assert np.array_equal(r, ref)
+
+
+def _run_ranks_pair(P, D, x, y, tx, ty, ch, variant):
+    """P loopback ranks, each proving its slice of a function lookup through prepare_pair with a virtual S."""
+    import torch
+    from paper_2404_16109_b200 import zkl
+    N = len(tx)
+    Dp = D // P
+    group = zkl.LoopbackGroup(P, max_D_local=Dp, max_N=N)
+    out, errs = [None] * P, []
+
+    def rank_main(p):
+        try:
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                ctx = zkl.Context(0, stream=stream, rank=p, group=group)
+                ctx.reserve(Dp, N)
+                tab = ctx.table(ctx.import_pair(tx, ty, ch.alpha_f))
+                assert ctx.table_attach_pair(tab, tx, ty, ch.alpha_f)
+                _, m = ctx.prepare_pair(x[p * Dp:(p + 1) * Dp], y[p * Dp:(p + 1) * Dp], ch.alpha_f, D, tab,
+                                        virtual_s=True)
+                chg = zkl.Context.challenges(ch.beta, ch.alpha1, ch.alpha2, ch.u, ch.r)
+                pf = ctx.prove(None, D, tab, m, chg, variant)
+                out[p] = (m.cpu().numpy().astype(np.uint32), pf)
+                ctx.close()
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    th = [threading.Thread(target=rank_main, args=(p,)) for p in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=900)
+    group.close()
+    if errs:
+        raise errs[0]
+    return out
+
+
+@pytest.mark.parametrize("P,dl", [(2, 19), (8, 20)])
+@pytest.mark.parametrize("variant", [TL.PAPER, TL.LOGUP])
+def test_loopback_big_local_rounds(P, dl, variant):
+    """D_local >= 2^19: the multi-block k_round rounds (with the round-2 gather of the virtual S) and the causal
+    chunked rounds run under P > 1; bit-identical to the single-rank oracle."""
+    import workloads as W
+    D = P << dl
+    d, n = D.bit_length() - 1, 16
+    N = 1 << n
+    rng = np.random.default_rng(P * 1000 + dl + variant)
+    tx = (np.arange(N) - N // 2).astype(np.int32)
+    ty = rng.integers(-2 ** 31, 2 ** 31, N, dtype=np.int64).astype(np.int32)
+    pick = np.clip(np.rint(N / 2 + rng.normal(0, N / 8, D)), 0, N - 1).astype(np.int64)
+    x, y = tx[pick], ty[pick]
+    ch = W.challenges(f"loop{P}.{dl}", d)
+    chal = C.chal_array(ch.beta, ch.alpha1, ch.alpha2, ch.u, ch.r)
+    ref = C.prove_pair_stream(x, y, tx, ty, ch.alpha_f, chal, variant, 2)
+    out = _run_ranks_pair(P, D, x, y, tx, ty, ch, variant)
+    for m, pf in out:
+        assert np.array_equal(m, ref.m)
+        assert pf.evals == ref.evals and pf.finals == ref.finals
+
+
+def _run_ranks_pair_fs(P, D, x, y, tx, ty, alpha_f, seed, variant):
+    import torch
+    from paper_2404_16109_b200 import zkl
+    N = len(tx)
+    Dp = D // P
+    group = zkl.LoopbackGroup(P, max_D_local=Dp, max_N=N)
+    out, errs = [None] * P, []
+
+    def rank_main(p):
+        try:
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                ctx = zkl.Context(0, stream=stream, rank=p, group=group)
+                ctx.reserve(Dp, N)
+                tab = ctx.table(ctx.import_pair(tx, ty, alpha_f))
+                assert ctx.table_attach_pair(tab, tx, ty, alpha_f)
+                _, m = ctx.prepare_pair(x[p * Dp:(p + 1) * Dp], y[p * Dp:(p + 1) * Dp], alpha_f, D, tab,
+                                        virtual_s=True)
+                out[p] = ctx.prove_fs(None, D, tab, m, seed, variant)
+                ctx.close()
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    th = [threading.Thread(target=rank_main, args=(p,)) for p in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=900)
+    group.close()
+    if errs:
+        raise errs[0]
+    return out
+
+
+@pytest.mark.parametrize("P,dl,n", [(2, 15, 16), (4, 18, 16), (8, 20, 16), (8, 3, 4)])
+@pytest.mark.parametrize("variant", [TL.PAPER, TL.LOGUP])
+def test_loopback_fiat_shamir(P, dl, n, variant):
+    """Fiat-Shamir at P > 1 (one all-gather of the round sums per local round, then the replicated last log2 P
+    rounds): every rank derives the same challenges, and the transcript equals the single-rank one and the oracle's
+    on those challenges."""
+    import hashlib
+    import workloads as W
+    from paper_2404_16109_b200 import zkl
+    D = P << dl
+    N = 1 << n
+    rng = np.random.default_rng(P * 77 + dl + variant)
+    tx = (np.arange(N) - N // 2).astype(np.int32)
+    ty = rng.integers(-2 ** 31, 2 ** 31, N, dtype=np.int64).astype(np.int32)
+    pick = np.clip(np.rint(N / 2 + rng.normal(0, N / 8, D)), 0, N - 1).astype(np.int64)
+    x, y = tx[pick], ty[pick]
+    alpha_f = W.chal(f"fsloop{P}", "alpha_f", 0)
+    seed = hashlib.sha256(f"fs-loopback-{P}-{dl}".encode()).digest()
+    out = _run_ranks_pair_fs(P, D, x, y, tx, ty, alpha_f, seed, variant)
+    ctx = zkl.Context(0)
+    ctx.reserve(D, N)
+    tab = ctx.table(ctx.import_pair(tx, ty, alpha_f))
+    _, m = ctx.prepare_pair(x, y, alpha_f, D, tab, virtual_s=True)
+    ref, dref = ctx.prove_fs(None, D, tab, m, seed, variant)
+    ctx.close()
+    chal = C.chal_array(dref["beta"], dref["alpha1"], dref["alpha2"], dref["u"], dref["r"])
+    o = C.prove_pair_stream(x, y, tx, ty, alpha_f, chal, variant, 2)
+    assert ref.evals == o.evals and ref.finals == o.finals
+    for pf, der in out:
+        assert der == dref
+        assert pf.evals == ref.evals and pf.finals == ref.finals

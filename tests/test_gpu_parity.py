@@ -353,7 +353,7 @@ def test_c2_activation_full(ctx, variant):
 
 @pytest.mark.parametrize("variant", [TL.PAPER, TL.LOGUP])
 def test_big_table_rounds(ctx, variant):
-    """N = 2^14 (> 2 x 4096 pairs): the multi-block table rounds on the main stream + the one-block tail."""
+    """N = 2^14: the chunked table rounds (k_tab_chunk, 2^14 <= 2^17 entries) + the one-block tail."""
     rng = random.Random(4242 + variant)
     d, n = 15, 14
     D, N = 1 << d, 1 << n
@@ -365,5 +365,35 @@ def test_big_table_rounds(ctx, variant):
     m, pf = _gpu_prove(ctx, S, T, ch, variant, D, N)
     ref = C.prove(C.ints_to_limbs(S), C.ints_to_limbs(T), C.chal_array(ch.beta, ch.alpha1, ch.alpha2, ch.u, ch.r),
                   variant)
+    assert ctx.export_ints(pf.B) == C.limbs_to_ints(ref.B)
+    assert pf.evals == ref.evals and pf.finals == ref.finals
+
+
+@pytest.mark.parametrize("variant", [TL.PAPER, TL.LOGUP])
+def test_table_rounds_above_2p17(ctx, variant):
+    """N = 2^18 > 2^17 entries: the multi-block table round k_tab_round runs (round 1) before the chunked table
+    rounds; D = 2^19 function lookups through the virtual-S path, against the streaming C oracle."""
+    d, n = 19, 18
+    D, N = 1 << d, 1 << n
+    rng = np.random.default_rng(1818 + variant)
+    tx = (np.arange(N) - N // 2).astype(np.int32)
+    ty = rng.integers(-2 ** 31, 2 ** 31, N, dtype=np.int64).astype(np.int32)
+    pick = rng.integers(0, N, D)
+    x, y = tx[pick], ty[pick]
+    ch = W.challenges(f"bigtab{variant}", d)
+    chal = C.chal_array(ch.beta, ch.alpha1, ch.alpha2, ch.u, ch.r)
+    ref = C.prove_pair_stream(x, y, tx, ty, ch.alpha_f, chal, variant, 2)
+    ctx.reserve(D, N)
+    tab = ctx.table(ctx.import_pair(tx, ty, ch.alpha_f))
+    assert ctx.table_attach_pair(tab, tx, ty, ch.alpha_f)
+    ctx.set_profiling(True)
+    try:
+        _, m = ctx.prepare_pair(x, y, ch.alpha_f, D, tab, virtual_s=True)
+        pf = ctx.prove(None, D, tab, m, _chal_gpu(ch), variant, want_B=True)
+        names = [rec[0] for rec in ctx.profile_read()]
+    finally:
+        ctx.set_profiling(False)
+    assert "k_tab_round" in names, names
+    assert np.array_equal(m.cpu().numpy().astype(np.uint32), ref.m)
     assert ctx.export_ints(pf.B) == C.limbs_to_ints(ref.B)
     assert pf.evals == ref.evals and pf.finals == ref.finals
