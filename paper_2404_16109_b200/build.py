@@ -90,5 +90,24 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_check() -> str:
+    """Debug variant libzkl_check.so: the tlookup translation unit compiled with -DZKL_CHECK (device asserts on every
+    SoA access and table gather; tools/sanitize_cases.py --check).  Not used by the product path."""
+    build()
+    objdir = os.path.join(HERE, "build")
+    out = os.path.join(HERE, "libzkl_check.so")
+    obj = os.path.join(objdir, "api_check.o")
+    cflags = [f for f in FLAGS if f != "-shared"]
+    subprocess.run([NVCC, *cflags, "-I", _nccl_include(), "-DZKL_CHECK", "-c", "-o", obj, os.path.join(CSRC, "api.cu")],
+                   check=True, capture_output=True)
+    subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, obj,
+                    os.path.join(objdir, "mm_api.o"), os.path.join(objdir, "hx_api.o"), "-ldl"], check=True,
+                   capture_output=True)
+    return out
+
+
 if __name__ == "__main__":
+    if "--check" in sys.argv:
+        print(build_check())
+        sys.exit(0)
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -16,8 +16,18 @@ enum { SLOT_H0 = 0, SLOT_H1 = 1, SLOT_HINF = 2, SLOT_A0 = 3, SLOT_A1 = 4 };
 constexpr int kMaxBlocks = 1184;        // partial-sum rows per round (148 SMs x 8)
 constexpr int kTailMax = 2048;          // the single-CTA tail holds <= 2048 elements of A and S
 
+// Debug builds (-DZKL_CHECK; tools/sanitize_cases.py --check): every SoA access and table gather is bounds-checked
+// with a device assert (compute-sanitizer is not available on this GPU pool).
+#ifdef ZKL_CHECK
+#include <assert.h>
+#define ZKL_ASSERT(c) assert(c)
+#else
+#define ZKL_ASSERT(c) ((void)0)
+#endif
+
 // ------------------------------------------------------------------ SoA access
 __device__ __forceinline__ fr ld_fr(const uint32_t* __restrict__ base, uint64_t n, uint64_t i) {
+    ZKL_ASSERT(i < n);
     fr x;
 #pragma unroll
     for (int l = 0; l < 8; ++l) x.v[l] = base[(uint64_t)l * n + i];
@@ -25,12 +35,14 @@ __device__ __forceinline__ fr ld_fr(const uint32_t* __restrict__ base, uint64_t 
 }
 
 __device__ __forceinline__ void st_fr(uint32_t* __restrict__ base, uint64_t n, uint64_t i, const fr& x) {
+    ZKL_ASSERT(i < n);
 #pragma unroll
     for (int l = 0; l < 8; ++l) base[(uint64_t)l * n + i] = x.v[l];
 }
 
 // 4 consecutive elements i..i+3 (i % 4 == 0, n % 4 == 0): one 128-bit load per limb plane
 __device__ __forceinline__ void ld_fr4(const uint32_t* __restrict__ base, uint64_t n, uint64_t i, fr (&x)[4]) {
+    ZKL_ASSERT(i + 4 <= n && (i & 3) == 0);
 #pragma unroll
     for (int l = 0; l < 8; ++l) {
         uint4 q = __ldg(reinterpret_cast<const uint4*>(base + (uint64_t)l * n + i));
@@ -39,6 +51,7 @@ __device__ __forceinline__ void ld_fr4(const uint32_t* __restrict__ base, uint64
 }
 
 __device__ __forceinline__ void st_fr4(uint32_t* __restrict__ base, uint64_t n, uint64_t i, const fr (&x)[4]) {
+    ZKL_ASSERT(i + 4 <= n && (i & 3) == 0);
 #pragma unroll
     for (int l = 0; l < 8; ++l) {
         uint4 q = make_uint4(x[0].v[l], x[1].v[l], x[2].v[l], x[3].v[l]);
@@ -48,6 +61,7 @@ __device__ __forceinline__ void st_fr4(uint32_t* __restrict__ base, uint64_t n, 
 
 // 2 consecutive elements (i even, n even): one 64-bit access per plane
 __device__ __forceinline__ void ld_fr2(const uint32_t* __restrict__ base, uint64_t n, uint64_t i, fr (&x)[2]) {
+    ZKL_ASSERT(i + 2 <= n && (i & 1) == 0);
 #pragma unroll
     for (int l = 0; l < 8; ++l) {
         uint2 q = __ldg(reinterpret_cast<const uint2*>(base + (uint64_t)l * n + i));
@@ -57,6 +71,7 @@ __device__ __forceinline__ void ld_fr2(const uint32_t* __restrict__ base, uint64
 
 __device__ __forceinline__ void st_fr2(uint32_t* __restrict__ base, uint64_t n, uint64_t i, const fr& a,
                                        const fr& b) {
+    ZKL_ASSERT(i + 2 <= n && (i & 1) == 0);
 #pragma unroll
     for (int l = 0; l < 8; ++l)
         *reinterpret_cast<uint2*>(base + (uint64_t)l * n + i) = make_uint2(a.v[l], b.v[l]);

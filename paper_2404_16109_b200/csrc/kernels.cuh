@@ -667,6 +667,7 @@ k_round1_keys(const uint32_t* __restrict__ S, uint64_t n, const uint32_t* __rest
             k.x = k.x >= N ? 0 : k.x;
             k.y = k.y >= N ? 0 : k.y;
         }
+        ZKL_ASSERT(k.x < N && k.y < N);
         const uint4* r0 = TB + 4 * (uint64_t)k.x;
         const uint4* r1 = TB + 4 * (uint64_t)k.y;
         const fr A0 = ld_fr_256(r0), A1 = ld_fr_256(r1);

@@ -3,6 +3,7 @@ item 9): every kernel family of the tlookup path at sizes the tools finish in mi
 against the CPU oracle so a run that exits 0 also computed the right thing.
 
     compute-sanitizer --tool memcheck --error-exitcode 9 python tools/sanitize_cases.py
+    python tools/sanitize_cases.py --check      # the same cases on libzkl_check.so (device bounds asserts)
 
 Cases: C1 (D = 2^10 range check, one-CTA prove, both variants), a 2^14 random-table proof (inversion hierarchy,
 hash index), a 2^19 function lookup with a virtual S (pair-range prepare, histogram, round-1 gather, round-2
@@ -16,6 +17,8 @@ import threading
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+if "--check" in sys.argv:   # compute-sanitizer is closed on this pool: device asserts on every access instead
+    os.environ["ZKL_LIB"] = os.path.join(ROOT, "paper_2404_16109_b200", "libzkl_check.so")
 
 import numpy as np  # noqa: E402
 
