@@ -645,7 +645,7 @@ k_gather_keys_round1(const uint32_t* __restrict__ S, uint64_t n, const uint32_t*
 // never materialised: round 2 gathers it again (k_round<..., GATHER>).  Same tile / pair layout and partial rows as
 // k_inv_bwd<true>: tile = 2048 pairs, thread t owns pairs 256 g + t (g = 0..7), W = E_hi[tile] E_lo[256 g + t].
 #ifndef ZKL_R1_CTAS
-#define ZKL_R1_CTAS 2
+#define ZKL_R1_CTAS 3   // 24 warps per SM hide the gathers' latency better than 16 without spills (measured -7%)
 #endif
 template <bool VERIFY, bool WRITE_A>
 __global__ void __launch_bounds__(kInvThreads, ZKL_R1_CTAS)
@@ -723,8 +723,11 @@ constexpr int kRoundThreads = 256;
 
 // GATHER (round 2 after k_round1_keys): the four old elements of A and S are the (B, T) records of keys[4y..4y+3]
 // (A_i = B_key, S_i = T_key): 16 B of keys from HBM and four 64-byte records from L2 replace 256 B of A and S.
+#ifndef ZKL_ROUND_CTAS
+#define ZKL_ROUND_CTAS 2
+#endif
 template <bool FOLD, bool DIRECT, bool GATHER = false>
-__global__ void __launch_bounds__(kRoundThreads, 2)
+__global__ void __launch_bounds__(kRoundThreads, ZKL_ROUND_CTAS)
 k_round(const uint32_t* __restrict__ Aold, const uint32_t* __restrict__ Sold, uint64_t nold,
         uint32_t* __restrict__ Anew, uint32_t* __restrict__ Snew, const ProofScalars* __restrict__ sc, int k,
         const fr* __restrict__ elo, const fr* __restrict__ ehi, int gbits, fr* partials,
