@@ -80,7 +80,7 @@ struct Plan {
     int inv_blocks;
     int hist_rows;
     // workspace offsets
-    size_t o_out, o_sc, o_err, o_rounds, o_jobs, o_chal, o_part, o_tpart, o_tnb, o_rank, o_gath, o_repl, o_tsum,
+    size_t o_out, o_sc, o_err, o_perr, o_rounds, o_jobs, o_chal, o_part, o_tpart, o_tnb, o_rank, o_gath, o_repl, o_tsum,
         o_fin, o_tfin, o_gfin, o_rc, o_fs, o_small, o_Sv, o_derived, o_arena, o_hist, o_keys, o_tot, o_totinv, o_A, o_A1, o_S1, o_A2, o_S2, o_tB, o_tX, o_tM,
         o_tE, o_twk, o_tBaos, o_chA, o_chS, o_coop, total;
 };
@@ -247,6 +247,7 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
     p.o_out = take(sizeof(ProofOut));
     p.o_sc = take(sizeof(ProofScalars));
     p.o_err = take(4 * sizeof(unsigned long long));
+    p.o_perr = take(4 * sizeof(unsigned long long));
     p.o_rounds = take(sizeof(RoundDesc) * kMaxRounds);
     p.o_jobs = take(sizeof(EqJob) * 2 * kMaxRounds);
     p.o_chal = take(sizeof(zkl_fr) * (3 + 2 * kMaxRounds));
@@ -485,7 +486,9 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
     }
     cudaStream_t s = ctx->stream, s2 = ctx->side;
     ProofScalars* sc = at<ProofScalars>(ctx, p.o_sc);
-    unsigned long long* err = at<unsigned long long>(ctx, p.o_err);   // [0] S, [1] T
+    // the proof's own error words ([0] DIV_ZERO_S, [1] DIV_ZERO_T, [2] gather miss): a pending async prepare may still
+    // be copying its error words (o_err) when this proof's setup starts on the aux stream
+    unsigned long long* err = at<unsigned long long>(ctx, p.o_perr);
     RoundDesc* rounds = at<RoundDesc>(ctx, p.o_rounds);
     EqJob* jobs = at<EqJob>(ctx, p.o_jobs);
     zkl_fr* chal = at<zkl_fr>(ctx, p.o_chal);
@@ -515,13 +518,17 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
     memcpy(hs->rounds, p.rd, sizeof(p.rd));
     memcpy(hs->jobs, p.jobs, sizeof(p.jobs));
     memcpy(hs->tnb, p.tnb, sizeof(p.tnb));
-    if ((st = h2d_small(ctx, s, {{chal, hs->chal}, {rounds, hs->rounds}, {jobs, hs->jobs}, {at<uint32_t>(ctx, p.o_tnb), hs->tnb}},
+    // The setup (challenges, eq tables) and B = 1/(beta + T) depend on neither the keys nor m: in prove mode they run
+    // on the aux stream from the moment of the call, overlapping the prepare still in flight on the ctx stream (async
+    // mode); the D side waits for them (ev_b) just before round 1.
+    cudaStream_t sp = a.prove_mode ? ctx->aux : s;
+    if ((st = h2d_small(ctx, sp, {{chal, hs->chal}, {rounds, hs->rounds}, {jobs, hs->jobs}, {at<uint32_t>(ctx, p.o_tnb), hs->tnb}},
                         {sizeof(hs->chal), sizeof(hs->rounds), sizeof(hs->jobs), sizeof(hs->tnb)})))
         return st;
-    CUDA_TRY(ctx, cudaMemsetAsync(err, 0xff, 4 * sizeof(unsigned long long), s));
-    LAUNCH(ctx, k_setup, 1, 1, 0, s, chal, p.d, p.pbits, p.rank, N, D, sc);
-    LAUNCH(ctx, k_eq_fill, grid_for(p.arena, 256), 256, 0, s, jobs, p.njobs, p.arena, sc, arena);
-    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, s));
+    CUDA_TRY(ctx, cudaMemsetAsync(err, 0xff, 4 * sizeof(unsigned long long), sp));
+    LAUNCH(ctx, k_setup, 1, 1, 0, sp, chal, p.d, p.pbits, p.rank, N, D, sc);
+    LAUNCH(ctx, k_eq_fill, grid_for(p.arena, 256), 256, 0, sp, jobs, p.njobs, p.arena, sc, arena);
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, sp));
     CUDA_TRY(ctx, cudaStreamWaitEvent(s2, ctx->ev_fork, 0));
     RoundConst* rc = at<RoundConst>(ctx, p.o_rc);
     LAUNCH(ctx, k_round_consts, 1, 64, 0, s2, sc, p.d, p.n, rc);
@@ -535,7 +542,7 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
     // the gather path (A_i = B_j(i)) needs B on the critical path: compute it on the main stream first
     const bool gather = a.prove_mode && !p.small && !a.force_inversion;
     if (a.prove_mode) {
-        cudaStream_t sb = s;   // B feeds both the table side and (gather path) the D side
+        cudaStream_t sb = sp;   // B feeds both the table side and (gather path) the D side
         if (N >= (uint64_t)kInvTile) {
             if ((st = inv_forward(ctx, p.tinv, Tsrc, N, tB, sc, 0, err + 1, sb, sb, nullptr))) return st;
             if ((st = inv_backward0(ctx, p.tinv, Tsrc, N, tB, sc, nullptr, nullptr, nullptr, 0, sb))) return st;
@@ -544,13 +551,14 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
             const unsigned bt = (unsigned)std::min<uint64_t>(1024, std::max<uint64_t>(32, N));
             LAUNCH(ctx, k_batch_invert, 1, bt, 4 * bt * sizeof(fr), sb, tX, N, (uint64_t)0, N, tB);
         }
-        if (gather) LAUNCH(ctx, k_pack_tb, grid_for(N, 256), 256, 0, s, Tsrc, tB, N, at<uint4>(ctx, p.o_tBaos));
+        if (gather) LAUNCH(ctx, k_pack_tb, grid_for(N, 256), 256, 0, sb, Tsrc, tB, N, at<uint4>(ctx, p.o_tBaos));
+        CUDA_TRY(ctx, cudaEventRecord(ctx->ev_b, sb));
+        CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_b, 0));   // the D side (and a table side on s) needs B
         // B_out (if requested) is the variant's B, written by k_tab_init.  With the histogram still running on the
         // low stream (async mode), the whole table side moves to the side stream, so that the D side does not wait
         // for m
         cudaStream_t ts = s;
         if (ctx->m_pending) {
-            CUDA_TRY(ctx, cudaEventRecord(ctx->ev_b, s));
             CUDA_TRY(ctx, cudaStreamWaitEvent(s2, ctx->ev_b, 0));
             ts = s2;
         }
