@@ -1,7 +1,7 @@
 """Time the tlookup step on every BASELINE.json configuration on one GPU (for BASELINE.md §5).
 
 A step = a1 (import) + a2 (table) + a3 (prepare) + a4-a9 (prove), inputs resident in HBM, CUDA events, warm-up 2.
-C4 runs its K = 5 digit instances back to back as one step (value = 5 * 2^27 / time).
+C4 runs its K = 5 digit instances (32 heads each) in flight together as one step (value = 5 * 2^27 / time).
     python tools/bench_configs.py [C1 C2 C3 H C4 C5]
 """
 import json
@@ -19,52 +19,66 @@ import workloads as W  # noqa: E402
 from paper_2404_16109_b200 import zkl  # noqa: E402
 
 
-def run_instances(ctx, wls, steps=5, warmup=2):
+def run_instances(wls, steps=5, warmup=2):
+    """The bench step on every instance: import T, table (+ pair-range attachment), prepare_pair with a virtual S
+    (range lookups as pairs with y = 0: T = [0, 2^16) + alpha * 0), prove.  Several instances are kept in flight on
+    their own contexts and streams (async mode): instance i+1's setup overlaps instance i's proof."""
     dev = torch.device("cuda", 0)
-    Dmax = max(w.D for w in wls)
-    Nmax = max(w.N for w in wls)
-    ctx.reserve(Dmax, Nmax)
     prepared = []
     for wl in wls:
+        st = torch.cuda.Stream(device=dev)
+        ctx = zkl.Context(0, stream=st)
+        ctx.reserve(wl.D, wl.N)
         if wl.kind == "pair":
-            ins = (torch.from_numpy(np.ascontiguousarray(wl.x)).to(dev), torch.from_numpy(np.ascontiguousarray(wl.y)).to(dev),
-                   torch.from_numpy(np.ascontiguousarray(wl.tx)).to(dev), torch.from_numpy(np.ascontiguousarray(wl.ty)).to(dev))
-        else:
-            ins = (torch.from_numpy(np.asarray(wl.s, np.int64)).to(dev), torch.from_numpy(np.asarray(wl.t, np.int64)).to(dev))
+            x, y, tx, ty = wl.x, wl.y, wl.tx, wl.ty
+        else:   # a range lookup: S = x + alpha * 0 over T = t + alpha * 0
+            x = np.asarray(wl.s, np.int32)
+            y = np.zeros_like(x)
+            tx = np.asarray(wl.t, np.int32)
+            ty = np.zeros_like(tx)
+        ins = tuple(torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (x, y, tx, ty))
         ch = wl.chal
-        prepared.append((wl, ins, zkl.Context.challenges(ch.beta, ch.alpha1, ch.alpha2, ch.u, ch.r), ctx.vec(wl.D),
+        prepared.append((ctx, st, wl, ins, zkl.Context.challenges(ch.beta, ch.alpha1, ch.alpha2, ch.u, ch.r),
                          ctx.vec(wl.N), ctx.table_mem(wl.N), torch.empty(wl.N, dtype=torch.int32, device=dev)))
 
     def step():
-        for wl, ins, chal, S, T, tmem, m in prepared:
-            if wl.kind == "pair":
-                ctx.import_pair(ins[2], ins[3], wl.chal.alpha_f, T)
-                tab = ctx.table(T, tmem)
-                ctx.table_attach_pair(tab, ins[2], ins[3], wl.chal.alpha_f)   # pair-range fast path of prepare_pair
-                ctx.prepare_pair(ins[0], ins[1], wl.chal.alpha_f, wl.D, tab, S, m)
-            else:
-                ctx.import_ints(ins[1], T)
-                tab = ctx.table(T, tmem)
-                ctx.import_ints(ins[0], S)
-                ctx.prepare(S, wl.D, tab, m)
-            ctx.prove(S, wl.D, tab, m, chal)
+        pend = []
+        for ctx, st, wl, ins, chal, T, tmem, m in prepared:
+            ctx.import_pair(ins[2], ins[3], wl.chal.alpha_f, T)
+            tab = ctx.table(T, tmem)
+            ctx.table_attach_pair(tab, ins[2], ins[3], wl.chal.alpha_f)
+            ctx.set_async(True)
+            ctx.prepare_pair(ins[0], ins[1], wl.chal.alpha_f, wl.D, tab, m=m, virtual_s=True)
+            pend.append((ctx, ctx.prove(None, wl.D, tab, m, chal), tab))
+        for ctx, p, _ in pend:
+            ctx.wait()
+            ctx.set_async(False)
+        return [p.result() for _, p, _ in pend]
 
     for _ in range(warmup):
         step()
     torch.cuda.synchronize()
+    streams = [p[1] for p in prepared]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
+    e0.record(streams[0])
+    for s_ in streams[1:]:
+        s_.wait_event(e0)
     for _ in range(steps):
         step()
-    e1.record()
+    for s_ in streams[1:]:
+        ev = torch.cuda.Event()
+        ev.record(s_)
+        streams[0].wait_event(ev)
+    e1.record(streams[0])
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
+    for p in prepared:
+        p[0].close()
     total = sum(w.D for w in wls)
     return ms, total / (ms / 1e3)
 
 
 def main(names):
-    ctx = zkl.Context(0)
     out = []
     for name in names:
         t0 = time.time()
@@ -75,7 +89,7 @@ def main(names):
         else:
             wls = [W.activation({"C2": "2", "C3": "3", "H": "H", "C5": "5"}[name])]
         gen = time.time() - t0
-        ms, lps = run_instances(ctx, wls, steps=3 if name in ("C4", "C5") else 5)
+        ms, lps = run_instances(wls, steps=3 if name in ("C4", "C5") else 5)
         rec = {"config": name, "lookups": sum(w.D for w in wls), "ms_per_step": ms, "lookups_per_s": lps,
                "instances": len(wls), "gen_s": gen}
         print(json.dumps(rec), flush=True)
