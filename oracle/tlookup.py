@@ -177,7 +177,7 @@ def lagrange_0123(g: Sequence[int], x: int) -> int:
     return acc
 
 
-def sumcheck_prove(A, S, B, T, m, ch: Challenges, variant: int = PAPER) -> Transcript:
+def sumcheck_prove(A, S, B, T, m, ch: Challenges, variant: int = PAPER, next_r=None) -> Transcript:
     """Sumcheck on Eq. tlookup-sumcheck, linear time.
 
     All seven multilinear vectors are laid out on the D-point hypercube (the table
@@ -186,12 +186,15 @@ def sumcheck_prove(A, S, B, T, m, ch: Challenges, variant: int = PAPER) -> Trans
     t in {0,1,2,3} as V_t = V_0 + t (V_1 - V_0) (multilinearity), the summand is
     evaluated there and summed over y; then every vector is folded with r_k as
     V' = V_0 + r_k (V_1 - V_0).
+
+    next_r(k, g_k) -> r_k (optional): a Fiat-Shamir transcript supplies r_k once g_k is known (it is appended to
+    ch.r); by default r_k = ch.r[k-1].
     """
     D, N = len(A), len(B)
     check_shapes(D, N)
     d, n = log2_exact(D), log2_exact(N)
     assert len(S) == D and len(T) == N and len(m) == N
-    assert len(ch.u) == d and len(ch.r) == d
+    assert len(ch.u) == d and (len(ch.r) == d or next_r is not None)
     w = N * F.inv(D) % R
     E = eq_table(ch.u)
     E2 = eq_table(ch.u[d - n:])
@@ -207,6 +210,8 @@ def sumcheck_prove(A, S, B, T, m, ch: Challenges, variant: int = PAPER) -> Trans
                 vals = [(v[2 * y] + tt * (v[2 * y + 1] - v[2 * y])) % R for v in vecs]
                 g[tt] = (g[tt] + tlookup_poly(*vals, ch.beta, ch.alpha1, ch.alpha2, w, variant)) % R
         evals.append(g)
+        if next_r is not None:
+            ch.r.append(next_r(k, g) % R)
         rk = ch.r[k - 1]
         vecs = [[(v[2 * y] + rk * (v[2 * y + 1] - v[2 * y])) % R for y in range(half)] for v in vecs]
     finals = {"A": vecs[0][0], "S": vecs[1][0], "B": vecs[3][0], "T": vecs[4][0], "m": vecs[5][0]}
