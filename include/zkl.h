@@ -169,6 +169,35 @@ int zkl_hyrax_commit(zkl_ctx* ctx, const void* pp_dev, uint64_t cols, zkl_vec S,
 int zkl_hyrax_prove_eval(zkl_ctx* ctx, zkl_vec S, uint64_t D, uint64_t cols, const zkl_fr* v, zkl_vec w_out,
                          zkl_fr* y_host);
 
+/* ---------------------------------------------------------------- Protocol 1 with its commitments (§8(f1) + (f3))
+ * PAPER.md:252-278 (Protocol 1, tlookup) in the function-lookup form of PAPER.md:287 (X + alpha_f Y in
+ * T_X + alpha_f T_Y), non-interactive: every message is absorbed into a SHA-256 transcript before the challenge
+ * that follows it:
+ *   h = SHA256("zkl-p1-v1" || seed || le64(D) || le64(N) || le32(variant) || le64(cols));
+ *   absorb [T_X], [T_Y] (tlookup-Setup, Commit(T; 0)), [X], [Y]  -> alpha_f;  S = X + alpha_f Y, [S] = [X] + alpha_f [Y];
+ *   m (tlookup-Prep), absorb [m]  -> beta;  A, B, absorb [A], [B]  -> alpha1 (alpha2 = alpha1^2), u;
+ *   the sumcheck with r_k from the transcript (as zkl_tlookup_prove_fs);
+ *   row-restriction proofs of evaluation (zkl_hyrax_prove_eval) of A, X, Y at v and of T_X, T_Y, m, B at v'.
+ * Commitments are Hyrax rows of `cols` entries (cols | N | D), with no hiding (blinds 0) in this build.
+ * x, y (D int32) and tx, ty (N int32, tx a contiguous range) are device arrays; pp from zkl_hyrax_setup(cols).
+ * Every output pointer is HOST memory the caller provides: C_X, C_Y, C_A (D / cols points), C_TX, C_TY, C_m, C_B
+ * (N / cols points), round_evals (log2 D x 4), derived (3 + 2 log2 D: beta, alpha1, alpha2, u, r), the w vectors
+ * (cols canonical values each) and the y values.  Single rank, synchronous.  The context's workspace must hold
+ * zkl_workspace_bytes(D, N, 1); the Hyrax steps use a buffer the context owns. */
+typedef struct {
+    zkl_g1 *C_X, *C_Y, *C_TX, *C_TY, *C_m, *C_A, *C_B;
+    zkl_fr* round_evals;
+    zkl_final_evals finals;
+    zkl_fr alpha_f;
+    zkl_fr* derived;
+    zkl_fr *w_A, *w_X, *w_Y, *w_TX, *w_TY, *w_m, *w_B;
+    zkl_fr y_A, y_X, y_Y, y_TX, y_TY, y_m, y_B;
+} zkl_p1_proof;
+
+int zkl_tlookup_prove_p1(zkl_ctx* ctx, const void* pp_dev, uint64_t cols, const int32_t* x_dev, const int32_t* y_dev,
+                         uint64_t D, const int32_t* tx_dev, const int32_t* ty_dev, uint64_t N, const uint8_t seed[32],
+                         zkl_variant variant, zkl_p1_proof* out);
+
 /* ---------------------------------------------------------------- async mode (many instances)
  * With async on, zkl_tlookup_prepare(_pair), zkl_tlookup_prove(_fs) and zkl_sumcheck_prove validate their
  * arguments, enqueue their kernels on the ctx stream and return ZKL_OK at once; their outputs (m is on the device

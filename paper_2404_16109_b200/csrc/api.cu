@@ -26,6 +26,7 @@
 #include "kernels.cuh"
 #include "host_common.h"
 #include "nccl_loader.h"
+#include "sha256_host.h"
 
 using namespace zkl;
 
@@ -797,9 +798,12 @@ int proof_fs_collect(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table
                      const uint8_t* seed, int variant, zkl_vec A_out, zkl_vec B_out, zkl_fr* round_evals,
                      zkl_final_evals* finals, zkl_fr* derived, int64_t* err_index, bool gather, int d);
 
+// preset (host, 3 + log2 D canonical values: the transcript state h as 32 bytes, beta, alpha1, u): the transcript was
+// started by the caller (Protocol 1, zkl_tlookup_prove_p1), so `seed` is unused
 int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, const uint32_t* m_dev,
                  const uint8_t* seed, int variant, zkl_vec A_out, zkl_vec B_out, zkl_fr* round_evals,
-                 zkl_final_evals* finals, zkl_fr* derived, int64_t* err_index, bool force_inversion) {
+                 zkl_final_evals* finals, zkl_fr* derived, int64_t* err_index, bool force_inversion,
+                 const zkl_fr* preset = nullptr) {
     if (err_index) *err_index = -1;
     if (ctx->async_mode && ctx->pend_prove) return set_err(ctx, ZKL_E_STATE, "a proof is already pending (zkl_ctx_wait)");
     int st;
@@ -807,7 +811,8 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
     if ((st = check_shape(ctx, D, N))) return st;
     if (D < 2 || D / ctx->nranks < 2)
         return set_err(ctx, ZKL_E_SHAPE, "Fiat-Shamir mode needs D >= 2 and D_local >= 2");
-    if (!seed || !m_dev || !round_evals || !finals || !derived) return set_err(ctx, ZKL_E_ARG, "null argument");
+    if ((!seed && !preset) || !m_dev || !round_evals || !finals || !derived)
+        return set_err(ctx, ZKL_E_ARG, "null argument");
     std::vector<zkl_fr> u1(kMaxRounds);
     for (auto& x : u1) { memset(&x, 0, sizeof(x)); x.w[0] = 1; }
     Plan p;
@@ -843,16 +848,23 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
         uint8_t seed[32];
         RoundDesc rounds[kMaxRounds];
         EqJob jobs[2 * kMaxRounds];
+        zkl_fr pre[3 + kMaxRounds];
     };
     Staging* hs = reinterpret_cast<Staging*>((uint8_t*)ctx->host_out + sizeof(ProofOut));
-    memcpy(hs->seed, seed, 32);
+    if (seed) memcpy(hs->seed, seed, 32);
     memcpy(hs->rounds, p.rd, sizeof(p.rd));
     memcpy(hs->jobs, p.jobs, sizeof(p.jobs));
-    if ((st = h2d_small(ctx, s, {{dseed, hs->seed}, {rounds, hs->rounds}, {jobs, hs->jobs}},
-                        {sizeof(hs->seed), sizeof(hs->rounds), sizeof(hs->jobs)})))
+    zkl_fr* dpre = at<zkl_fr>(ctx, p.o_chal) + 2;   // after the 32-byte seed slot
+    if (preset) memcpy(hs->pre, preset, sizeof(zkl_fr) * (3 + p.d));
+    if ((st = h2d_small(ctx, s, {{dseed, hs->seed}, {rounds, hs->rounds}, {jobs, hs->jobs}, {dpre, hs->pre}},
+                        {sizeof(hs->seed), sizeof(hs->rounds), sizeof(hs->jobs),
+                         preset ? sizeof(zkl_fr) * (3 + p.d) : (size_t)0})))
         return st;
     CUDA_TRY(ctx, cudaMemsetAsync(err, 0xff, 4 * sizeof(unsigned long long), s));
-    LAUNCH(ctx, k_fs_init, 1, 1, 0, s, dseed, D, N, variant, p.d, sc, fst, dder, p.pbits, p.rank);
+    if (preset)
+        LAUNCH(ctx, k_fs_init_preset, 1, 1, 0, s, dpre, p.d, sc, fst, dder, p.pbits, p.rank);
+    else
+        LAUNCH(ctx, k_fs_init, 1, 1, 0, s, dseed, D, N, variant, p.d, sc, fst, dder, p.pbits, p.rank);
     LAUNCH(ctx, k_eq_fill, grid_for(p.arena, 256), 256, 0, s, jobs, p.njobs, p.arena, sc, arena);
     // ---- B = 1/(beta + T) and the table working vectors
     uint32_t* tB = at<uint32_t>(ctx, p.o_tB);
@@ -1270,6 +1282,9 @@ void zkl_ctx_destroy(zkl_ctx* c) {
     cudaSetDevice(c->device);
     if (c->hs.table) zkl_table_destroy(c->hs.table);
     if (c->hs.buf) cudaFree(c->hs.buf);
+    if (c->p1.table) zkl_table_destroy(c->p1.table);
+    if (c->p1.buf) cudaFree(c->p1.buf);
+    if (c->p1.hxws) cudaFree(c->p1.hxws);
     if (c->prof[0].a)
         for (int i = 0; i < 256; ++i) { cudaEventDestroy(c->prof[i].a); cudaEventDestroy(c->prof[i].b); }
     if (c->nccl_comm) zkl_nccl_destroy(c);
@@ -1751,6 +1766,220 @@ int zkl_tlookup_prove_pair_host(zkl_ctx* ctx, const int32_t* x_host, const int32
     if (m_out) {
         CUDA_TRY(ctx, cudaMemcpyAsync(m_out, md, 4 * N, cudaMemcpyDeviceToHost, ctx->stream));
         return sync_stream(ctx);
+    }
+    return ZKL_OK;
+}
+
+// ---------------------------------------------------------------- Protocol 1 with its commitments
+namespace {
+
+// the Protocol-1 transcript on the host (oracle/protocol1.py is the verifier's side)
+struct P1Transcript {
+    uint8_t h[32];
+    void absorb_points(const char* label, const zkl_g1* C, uint64_t n) {
+        Sha256 sh;
+        sh.update(h, 32);
+        sh.update(label, strlen(label));
+        const uint32_t cnt = (uint32_t)n;
+        uint8_t le[4] = {(uint8_t)cnt, (uint8_t)(cnt >> 8), (uint8_t)(cnt >> 16), (uint8_t)(cnt >> 24)};
+        sh.update(le, 4);
+        for (uint64_t i = 0; i < n; ++i) {
+            uint8_t b[97];
+            for (int w = 0; w < 12; ++w)
+                for (int k = 0; k < 4; ++k) {
+                    b[4 * w + k] = C[i].infinity ? 0 : (uint8_t)(C[i].x[w] >> (8 * k));
+                    b[48 + 4 * w + k] = C[i].infinity ? 0 : (uint8_t)(C[i].y[w] >> (8 * k));
+                }
+            b[96] = C[i].infinity ? 1 : 0;
+            sh.update(b, 97);
+        }
+        sh.final(h);
+    }
+    zkl_fr chal(const char* label, uint32_t i) const {
+        Sha256 sh;
+        sh.update(h, 32);
+        sh.update(label, strlen(label));
+        uint8_t le[4] = {(uint8_t)i, (uint8_t)(i >> 8), (uint8_t)(i >> 16), (uint8_t)(i >> 24)};
+        sh.update(le, 4);
+        uint8_t dg[32];
+        sh.final(dg);
+        zkl_fr z;
+        for (int w = 0; w < 8; ++w)
+            z.w[w] = (uint32_t)dg[4 * w] | ((uint32_t)dg[4 * w + 1] << 8) | ((uint32_t)dg[4 * w + 2] << 16) |
+                     ((uint32_t)dg[4 * w + 3] << 24);
+        static const uint32_t rl[8] = {0x00000001u, 0xffffffffu, 0xfffe5bfeu, 0x53bda402u,
+                                       0x09a1d805u, 0x3339d808u, 0x299d7d48u, 0x73eda753u};
+        while (fr_ge_r_host(z)) {   // a digest < 2^256 < 3r: at most two subtractions of r
+            uint64_t bw = 0;
+            for (int w = 0; w < 8; ++w) {
+                const uint64_t d = (uint64_t)z.w[w] - rl[w] - bw;
+                z.w[w] = (uint32_t)d;
+                bw = (d >> 63) & 1;
+            }
+        }
+        return z;
+    }
+};
+
+// the Hyrax steps run in the context's own Hyrax workspace (they clear the prepared-keys flag: restored after)
+struct HxScope {
+    zkl_ctx* c;
+    uint8_t* ws;
+    size_t bytes;
+    int prep;
+    HxScope(zkl_ctx* ctx) : c(ctx), ws(ctx->ws), bytes(ctx->ws_bytes), prep(ctx->prep_valid) {
+        c->ws = (uint8_t*)c->p1.hxws;
+        c->ws_bytes = c->p1.hxbytes;
+    }
+    ~HxScope() {
+        c->ws = ws;
+        c->ws_bytes = bytes;
+        c->prep_valid = prep;
+    }
+};
+
+}  // namespace
+
+int zkl_tlookup_prove_p1(zkl_ctx* ctx, const void* pp, uint64_t cols, const int32_t* x, const int32_t* y, uint64_t D,
+                         const int32_t* tx, const int32_t* ty, uint64_t N, const uint8_t seed[32], zkl_variant variant,
+                         zkl_p1_proof* out) {
+    int st;
+    if ((st = check_ctx(ctx))) return st;
+    if ((st = check_idle(ctx))) return st;
+    if (ctx->async_mode || ctx->nranks != 1)
+        return set_err(ctx, ZKL_E_STATE, "zkl_tlookup_prove_p1: synchronous, single-rank calls only");
+    if (!pp || !x || !y || !tx || !ty || !seed || !out || !out->C_X || !out->C_Y || !out->C_TX || !out->C_TY ||
+        !out->C_m || !out->C_A || !out->C_B || !out->round_evals || !out->derived || !out->w_A || !out->w_X ||
+        !out->w_Y || !out->w_TX || !out->w_TY || !out->w_m || !out->w_B)
+        return set_err(ctx, ZKL_E_ARG, "null argument");
+    if ((st = check_shape(ctx, D, N))) return st;
+    if (!is_pow2(cols) || cols > N) return set_err(ctx, ZKL_E_SHAPE, "cols must be a power of two dividing N");
+    const int d = ilog2(D), n = ilog2(N);
+    // owned device memory: X, Y, A (D), TX, TY, T, m_fr, B (N) as SoA vectors, w (cols), the table, m (u32)
+    const size_t o_X = 0, o_Y = o_X + soa_bytes(D), o_A = o_Y + soa_bytes(D), o_TX = o_A + soa_bytes(D),
+                 o_TY = o_TX + soa_bytes(N), o_T = o_TY + soa_bytes(N), o_mf = o_T + soa_bytes(N),
+                 o_B = o_mf + soa_bytes(N), o_w = o_B + soa_bytes(N), o_tab = o_w + soa_bytes(cols),
+                 o_m = o_tab + align_up(zkl_table_bytes(N)), total = o_m + align_up(4 * N);
+    const size_t hxb = zkl_hyrax_workspace_bytes(D, cols);
+    if (ctx->p1.bytes < total || ctx->p1.hxbytes < hxb) {
+        CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        if (ctx->p1.table) { zkl_table_destroy(ctx->p1.table); ctx->p1.table = nullptr; }
+        if (ctx->p1.buf) cudaFree(ctx->p1.buf);
+        if (ctx->p1.hxws) cudaFree(ctx->p1.hxws);
+        ctx->p1.buf = ctx->p1.hxws = nullptr;
+        ctx->p1.bytes = ctx->p1.hxbytes = 0;
+        CUDA_TRY(ctx, cudaMalloc(&ctx->p1.buf, total));
+        CUDA_TRY(ctx, cudaMalloc(&ctx->p1.hxws, hxb));
+        ctx->p1.bytes = total;
+        ctx->p1.hxbytes = hxb;
+    }
+    uint8_t* b = reinterpret_cast<uint8_t*>(ctx->p1.buf);
+    auto vec = [&](size_t o, uint64_t len) { return zkl_vec{reinterpret_cast<uint32_t*>(b + o), len}; };
+    const zkl_vec X = vec(o_X, D), Y = vec(o_Y, D), A = vec(o_A, D), TX = vec(o_TX, N), TY = vec(o_TY, N),
+                  T = vec(o_T, N), Mf = vec(o_mf, N), B = vec(o_B, N), Wv = vec(o_w, cols);
+    uint32_t* md = reinterpret_cast<uint32_t*>(b + o_m);
+    cudaStream_t s = ctx->stream;
+    LAUNCH(ctx, k_import_i32, grid_for(D, 256), 256, 0, s, x, D, 0, X.limbs);
+    LAUNCH(ctx, k_import_i32, grid_for(D, 256), 256, 0, s, y, D, 0, Y.limbs);
+    LAUNCH(ctx, k_import_i32, grid_for(N, 256), 256, 0, s, tx, N, 0, TX.limbs);
+    LAUNCH(ctx, k_import_i32, grid_for(N, 256), 256, 0, s, ty, N, 0, TY.limbs);
+    // tlookup-Setup and the lookups' commitments, then alpha_f
+    P1Transcript tr;
+    {
+        Sha256 sh;
+        sh.update("zkl-p1-v1", 9);
+        sh.update(seed, 32);
+        uint8_t le[8];
+        for (int i = 0; i < 8; ++i) le[i] = (uint8_t)(D >> (8 * i));
+        sh.update(le, 8);
+        for (int i = 0; i < 8; ++i) le[i] = (uint8_t)(N >> (8 * i));
+        sh.update(le, 8);
+        const uint32_t vv = (uint32_t)variant;
+        uint8_t l4[4] = {(uint8_t)vv, (uint8_t)(vv >> 8), (uint8_t)(vv >> 16), (uint8_t)(vv >> 24)};
+        sh.update(l4, 4);
+        for (int i = 0; i < 8; ++i) le[i] = (uint8_t)(cols >> (8 * i));
+        sh.update(le, 8);
+        sh.final(tr.h);
+    }
+    const uint64_t rD = D / cols, rN = N / cols;
+    {
+        HxScope hx(ctx);
+        if ((st = zkl_hyrax_commit(ctx, pp, cols, TX, N, nullptr, out->C_TX))) return st;
+        if ((st = zkl_hyrax_commit(ctx, pp, cols, TY, N, nullptr, out->C_TY))) return st;
+        if ((st = zkl_hyrax_commit(ctx, pp, cols, X, D, nullptr, out->C_X))) return st;
+        if ((st = zkl_hyrax_commit(ctx, pp, cols, Y, D, nullptr, out->C_Y))) return st;
+    }
+    tr.absorb_points("TX", out->C_TX, rN);
+    tr.absorb_points("TY", out->C_TY, rN);
+    tr.absorb_points("X", out->C_X, rD);
+    tr.absorb_points("Y", out->C_Y, rD);
+    const zkl_fr af = tr.chal("alpha_f", 0);
+    out->alpha_f = af;
+    // T = T_X + alpha_f T_Y, its index, and tlookup-Prep with a virtual S = X + alpha_f Y; then [m] and beta
+    if ((st = zkl_vec_import_pair(ctx, tx, ty, &af, T))) return st;
+    if (ctx->p1.table) { zkl_table_destroy(ctx->p1.table); ctx->p1.table = nullptr; }
+    int64_t ei = -1;
+    if ((st = zkl_table_create(ctx, T, b + o_tab, zkl_table_bytes(N), &ctx->p1.table, &ei))) return st;
+    if ((st = zkl_table_attach_pair(ctx, ctx->p1.table, tx, ty, &af))) return st;
+    const zkl_vec Sv{nullptr, D};
+    if ((st = zkl_tlookup_prepare_pair(ctx, x, y, &af, D, ctx->p1.table, Sv, md, &ei))) return st;
+    LAUNCH(ctx, k_import_i32, grid_for(N, 256), 256, 0, s, reinterpret_cast<const int32_t*>(md), N, 1, Mf.limbs);
+    {
+        HxScope hx(ctx);
+        if ((st = zkl_hyrax_commit(ctx, pp, cols, Mf, N, nullptr, out->C_m))) return st;
+    }
+    tr.absorb_points("m", out->C_m, rN);
+    const zkl_fr beta = tr.chal("beta", 0);
+    // A = 1/(beta + S), B (the variant's): the explicit-challenge prove with this beta writes both
+    {
+        std::vector<zkl_fr> zeros((size_t)d), ev((size_t)4 * d);
+        for (auto& z : zeros) memset(&z, 0, sizeof(z));
+        zkl_fr one;
+        memset(&one, 0, sizeof(one));
+        one.w[0] = 1;
+        zkl_challenges ch0{beta, one, one, zeros.data(), zeros.data()};
+        zkl_final_evals f0;
+        if ((st = zkl_tlookup_prove(ctx, Sv, D, ctx->p1.table, md, &ch0, variant, A, B, ev.data(), &f0, &ei)))
+            return st;
+    }
+    {
+        HxScope hx(ctx);
+        if ((st = zkl_hyrax_commit(ctx, pp, cols, A, D, nullptr, out->C_A))) return st;
+        if ((st = zkl_hyrax_commit(ctx, pp, cols, B, N, nullptr, out->C_B))) return st;
+    }
+    tr.absorb_points("A", out->C_A, rD);
+    tr.absorb_points("B", out->C_B, rN);
+    std::vector<zkl_fr> pre(3 + (size_t)d);
+    for (int w = 0; w < 8; ++w)
+        pre[0].w[w] = (uint32_t)tr.h[4 * w] | ((uint32_t)tr.h[4 * w + 1] << 8) | ((uint32_t)tr.h[4 * w + 2] << 16) |
+                      ((uint32_t)tr.h[4 * w + 3] << 24);
+    pre[1] = beta;
+    pre[2] = tr.chal("alpha", 0);
+    for (int c = 0; c < d; ++c) pre[3 + c] = tr.chal("u", (uint32_t)c);
+    // the sumcheck, continuing the transcript on the device
+    if ((st = run_proof_fs(ctx, Sv, D, ctx->p1.table, md, nullptr, variant, zkl_vec{nullptr, D}, zkl_vec{nullptr, N},
+                           out->round_evals, &out->finals, out->derived, &ei, false, pre.data())))
+        return st;
+    // proofs of evaluation at v = (r_d, ..., r_1) and v' = v[d-n:]
+    std::vector<zkl_fr> v((size_t)d);
+    for (int c = 0; c < d; ++c) v[c] = out->derived[3 + d + (d - c - 1)];
+    const zkl_fr* vt = v.data() + (d - n);
+    struct EvalJob {
+        zkl_vec src;
+        uint64_t len;
+        const zkl_fr* pt;
+        zkl_fr* w;
+        zkl_fr* y;
+    } jobs[7] = {{A, D, v.data(), out->w_A, &out->y_A},   {X, D, v.data(), out->w_X, &out->y_X},
+                 {Y, D, v.data(), out->w_Y, &out->y_Y},   {TX, N, vt, out->w_TX, &out->y_TX},
+                 {TY, N, vt, out->w_TY, &out->y_TY},      {Mf, N, vt, out->w_m, &out->y_m},
+                 {B, N, vt, out->w_B, &out->y_B}};
+    for (const auto& j : jobs) {
+        {
+            HxScope hx(ctx);
+            if ((st = zkl_hyrax_prove_eval(ctx, j.src, j.len, cols, j.pt, Wv, j.y))) return st;
+        }
+        if ((st = zkl_vec_export(ctx, Wv, j.w, 0))) return st;
     }
     return ZKL_OK;
 }

@@ -254,6 +254,14 @@ struct zkl_ctx {
         size_t bytes;
         zkl_table* table;
     } hs;
+    // zkl_tlookup_prove_p1: the field vectors, table and m it owns, and a separate workspace for the Hyrax steps
+    struct P1Buf {
+        void* buf;
+        size_t bytes;
+        void* hxws;
+        size_t hxbytes;
+        zkl_table* table;
+    } p1;
     // optional per-kernel timing (zkl_ctx_set_profiling): events around every launch
     int profiling;
     int nprof;

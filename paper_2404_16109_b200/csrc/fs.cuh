@@ -104,6 +104,41 @@ __global__ void k_fs_init(const uint8_t* __restrict__ seed, uint64_t D, uint64_t
     st->tscale = fr_one();
 }
 
+// Protocol-1 transcript: the host absorbed the commitments and derived beta, alpha1 and u; the device
+// continues the same transcript for the rounds.  pre (canonical zkl_fr): [0] h as 32 bytes, [1] beta, [2] alpha1,
+// [3 ..] u[0 .. d-1].
+__global__ void k_fs_init_preset(const zkl_fr* __restrict__ pre, int d, ProofScalars* sc, FsState* st,
+                                 zkl_fr* derived, int pbits, int rank) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    for (int i = 0; i < 8; ++i)
+        for (int b = 0; b < 4; ++b) st->h[4 * i + b] = (uint8_t)(pre[0].w[i] >> (8 * b));
+    auto canon = [](const zkl_fr& z) {
+        fr x;
+        for (int l = 0; l < 8; ++l) x.v[l] = z.w[l];
+        return x;
+    };
+    const fr beta = canon(pre[1]), a1 = canon(pre[2]);
+    const fr a1m = fr_to_mont(a1);
+    sc->beta = fr_to_mont(beta);
+    sc->alpha1 = a1m;
+    sc->alpha2 = fr_mul(a1m, a1m);
+    derived[0] = pre[1];
+    derived[1] = pre[2];
+    derived[2] = to_canon(sc->alpha2);
+    for (int c = 0; c < d; ++c) {
+        sc->u[c] = fr_to_mont(canon(pre[3 + c]));
+        derived[3 + c] = pre[3 + c];
+    }
+    fr re = fr_one();
+    for (int b = 0; b < pbits; ++b) {
+        const bool bit = (rank >> (pbits - 1 - b)) & 1;
+        re = fr_mul(re, bit ? sc->u[b] : fr_sub(fr_one(), sc->u[b]));
+    }
+    sc->rank_eq = re;
+    st->C = fr_one();
+    st->tscale = fr_one();
+}
+
 // table side, split for the causal order: fold with r_{k-1} (after it is derived), then evaluate round k
 __global__ void __launch_bounds__(256)
 k_tab_eval(const fr* __restrict__ cur, uint64_t len, const ProofScalars* __restrict__ sc, int variant, fr* tpart) {

@@ -38,6 +38,14 @@ __global__ void k_import_i64(const int64_t* __restrict__ src, uint64_t n, uint32
         st_fr(dst, n, i, fr_to_mont(fr_from_i64(src[i])));
 }
 
+// 32-bit integers -> Montgomery SoA (is_unsigned: u32 counts such as m; else int32 with x < 0 -> r - |x|)
+__global__ void k_import_i32(const int32_t* __restrict__ src, uint64_t n, int is_unsigned, uint32_t* __restrict__ dst) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const int64_t v = is_unsigned ? (int64_t)(uint32_t)src[i] : (int64_t)src[i];
+        st_fr(dst, n, i, fr_to_mont(fr_from_i64(v)));
+    }
+}
+
 // S_i = x_i + alpha_f y_i for 32-bit x, y, straight into Montgomery form without a full
 // field multiplication: with Cx = +-2^32 R, Cy = +-alpha_f 2^32 R (mod r, sign of x / y),
 //   U = |x| Cx + |y| Cy  (< 2^32 r, 9 words),  V = (U + q r) / 2^32 with q = -U mod 2^32 (r' = -1)

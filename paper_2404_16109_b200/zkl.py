@@ -52,6 +52,17 @@ class zkl_final_evals(ctypes.Structure):
     _fields_ = [("A", zkl_fr), ("S", zkl_fr), ("B", zkl_fr), ("T", zkl_fr), ("m", zkl_fr)]
 
 
+_G1P, _FRP = ctypes.POINTER(zkl_g1), ctypes.POINTER(zkl_fr)
+
+
+class zkl_p1_proof(ctypes.Structure):
+    _fields_ = [("C_X", _G1P), ("C_Y", _G1P), ("C_TX", _G1P), ("C_TY", _G1P), ("C_m", _G1P), ("C_A", _G1P),
+                ("C_B", _G1P), ("round_evals", _FRP), ("finals", zkl_final_evals), ("alpha_f", zkl_fr),
+                ("derived", _FRP), ("w_A", _FRP), ("w_X", _FRP), ("w_Y", _FRP), ("w_TX", _FRP), ("w_TY", _FRP),
+                ("w_m", _FRP), ("w_B", _FRP), ("y_A", zkl_fr), ("y_X", zkl_fr), ("y_Y", zkl_fr), ("y_TX", zkl_fr),
+                ("y_TY", zkl_fr), ("y_m", zkl_fr), ("y_B", zkl_fr)]
+
+
 class ZklError(RuntimeError):
     def __init__(self, status: int, index: int = -1, msg: str = ""):
         name = STATUS[status] if 0 <= status < len(STATUS) else str(status)
@@ -112,6 +123,8 @@ def lib() -> ctypes.CDLL:
             "zkl_tlookup_prove_fs": ([P, zkl_vec, U64, P, P, ctypes.c_char_p, I32, zkl_vec, zkl_vec,
                                       ctypes.POINTER(zkl_fr), ctypes.POINTER(zkl_final_evals), ctypes.POINTER(zkl_fr),
                                       I64P], I32),
+            "zkl_tlookup_prove_p1": ([P, P, U64, P, P, U64, P, P, U64, ctypes.c_char_p, I32,
+                                      ctypes.POINTER(zkl_p1_proof)], I32),
             "zkl_tlookup_prove_pair_host": ([P, P, P, U64, P, P, U64, ctypes.POINTER(zkl_fr),
                                              ctypes.POINTER(zkl_challenges), I32, ctypes.POINTER(zkl_fr),
                                              ctypes.POINTER(zkl_final_evals), P, I64P], I32),
@@ -137,7 +150,7 @@ EXPORTED = ["zkl_strerror", "zkl_ctx_create", "zkl_nccl_unique_id", "zkl_ctx_cre
             "zkl_vec_import", "zkl_vec_import_i64", "zkl_vec_import_pair", "zkl_vec_export", "zkl_table_bytes",
             "zkl_table_create", "zkl_table_destroy", "zkl_tlookup_prepare", "zkl_tlookup_prepare_pair",
             "zkl_tlookup_prove", "zkl_tlookup_prove_fs", "zkl_tlookup_prove_pair_host",
-            "zkl_sumcheck_prove"]
+            "zkl_tlookup_prove_p1", "zkl_sumcheck_prove"]
 
 
 def __getattr__(name):   # C names exposed unchanged: zkl.zkl_tlookup_prove(...)
@@ -476,6 +489,41 @@ class Context:
         self._check(st, err.value)
         pf = Proof(_evals(evals, d), _finals(fin))
         return (pf, mh) if want_m else pf
+
+    def prove_p1(self, pp, x, y, tx, ty, seed: bytes, variant: int = PAPER):
+        """Protocol 1 with its commitments (zkl_tlookup_prove_p1): x, y, tx, ty int32 (device tensors or arrays).
+        Returns the proof in the form oracle/protocol1.py verifies (points as (x, y) or None, field elements as
+        ints)."""
+        dev = lambda a: a if hasattr(a, "data_ptr") else self.torch.as_tensor(np.asarray(a, np.int32)).to(self.device)  # noqa: E731
+        xd, yd, txd, tyd = dev(x), dev(y), dev(tx), dev(ty)
+        D, N, cols = xd.numel(), txd.numel(), pp["cols"]
+        d = D.bit_length() - 1
+        rD, rN = D // cols, N // cols
+        arr = {k: (zkl_g1 * (rD if k in ("C_X", "C_Y", "C_A") else rN))() for k in
+               ("C_X", "C_Y", "C_TX", "C_TY", "C_m", "C_A", "C_B")}
+        wv = {k: (zkl_fr * cols)() for k in ("w_A", "w_X", "w_Y", "w_TX", "w_TY", "w_m", "w_B")}
+        ev = (zkl_fr * (4 * d))()
+        der = (zkl_fr * (3 + 2 * d))()
+        pf = zkl_p1_proof()
+        for k, a in arr.items():
+            setattr(pf, k, ctypes.cast(a, _G1P))
+        for k, a in wv.items():
+            setattr(pf, k, ctypes.cast(a, _FRP))
+        pf.round_evals = ctypes.cast(ev, _FRP)
+        pf.derived = ctypes.cast(der, _FRP)
+        if len(seed) != 32:
+            raise ValueError("seed must be 32 bytes")
+        self._check(lib().zkl_tlookup_prove_p1(self.h, ctypes.c_void_p(pp["ptr"]), cols, ctypes.c_void_p(xd.data_ptr()),
+                                               ctypes.c_void_p(yd.data_ptr()), D, ctypes.c_void_p(txd.data_ptr()),
+                                               ctypes.c_void_p(tyd.data_ptr()), N, seed, variant, ctypes.byref(pf)))
+        dv = [fr_to_int(der[i]) for i in range(3 + 2 * d)]
+        C = {k[2:]: [g1_to_py(a[i]) for i in range(len(a))] for k, a in arr.items()}
+        proofs = {k[2:]: ([fr_to_int(wv[k][i]) for i in range(cols)], fr_to_int(getattr(pf, "y_" + k[2:])))
+                  for k in wv}
+        return {"D": D, "N": N, "cols": cols, "variant": variant, "seed": seed, "C": C,
+                "alpha_f": fr_to_int(pf.alpha_f), "evals": _evals(ev, d), "finals": _finals(pf.finals),
+                "derived": {"beta": dv[0], "alpha1": dv[1], "alpha2": dv[2], "u": dv[3:3 + d], "r": dv[3 + d:]},
+                "eval_proofs": proofs}
 
     def prove_fs(self, S: Vec, D: int, tab: "Table", m, seed: bytes, variant: int = PAPER, want_A: bool = False,
                  want_B: bool = False):
