@@ -133,6 +133,7 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
             }
             const int gbits = round_gbits(np);
             choose_round(p, k, np, gbits, (int)std::max<uint64_t>(1, np >> gbits));
+            if (k >= 2) p.rd[k - 1].a1_derived = 1;   // k_round<true, ...>
         }
         // H(1) summed directly, except in the big rounds (>= 2^20 elements), whose k_round hides the one inversion
         // per round that deriving H(1) from the running claim needs (k_fs_inv on the side stream)
@@ -155,6 +156,7 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
                     RoundDesc& r = p.rd[kk - 1];
                     r.gbits = kk < k + kChunkBits ? std::min(10, p.dl - kk) : p.dl - kk;
                     r.direct_h1 = 1;
+                    r.a1_derived = 0;
                 }
             }
         }
@@ -175,6 +177,7 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
             const uint64_t np = nk / 2;
             const int gbits = round_gbits(np);
             choose_round(p, k, np, gbits, (int)std::max<uint64_t>(1, np >> gbits));
+            if (k >= 2) p.rd[k - 1].a1_derived = 1;   // k_round<true, ...>
         }
         p.k0 = k;
         p.fold_in = 1;
@@ -199,6 +202,7 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
         p.rd[k - 1].gbits = p.dl - k;
         p.rd[k - 1].nblocks = tail_rows;
         p.rd[k - 1].direct_h1 = 1;
+        p.rd[k - 1].a1_derived = 0;
     }
     for (int k = 1; k <= p.dl; ++k) {
         if (k == 1 && !prove_mode) p.rd[0].direct_h1 = 1;
@@ -212,6 +216,7 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
         p.rd[k - 1].gbits = p.d - k;
         p.rd[k - 1].nblocks = P <= kTailWarpMax ? 1u : (uint32_t)(kTailThreads / 32);
         p.rd[k - 1].direct_h1 = 1;
+        p.rd[k - 1].a1_derived = (fs && k >= p.dl + 2) ? 1 : 0;   // Fiat-Shamir: k_round<true, true> on the P values
     }
     // ---- eq arena jobs: per round E_lo then E_hi
     uint64_t off = 0;
@@ -963,7 +968,7 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
             LAUNCH(ctx, k_rows_fold, 1, 256, 0, s, r1, r1rows, rank_sums, 1u);
             if ((st = zkl_dist_allgather(ctx, rank_sums, gath, kSlots * sizeof(fr)))) return st;
             LAUNCH(ctx, k_fs_round, 1, 256, 0, s, 1, p.d, p.n, variant, gath, (uint32_t)P, h01, tpart,
-                   p.n >= 1 ? p.tnb[0] : 0u, tfin, sc, fst, out, dder, 0, err + 2, 1u, (uint32_t)kSlots);
+                   p.n >= 1 ? p.tnb[0] : 0u, tfin, sc, fst, out, dder, 0, err + 2, 1u, (uint32_t)kSlots, 0);
         } else {
             if (r1rows > 256) {
                 fr* folded = at<fr>(ctx, p.o_rank);   // kMaxRounds x kSlots fr >= 5 x 32
@@ -972,7 +977,7 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
                 r1rows = 32;
             }
             LAUNCH(ctx, k_fs_round, 1, 256, 0, s, 1, p.d, p.n, variant, r1, r1rows, h01, tpart,
-                   p.n >= 1 ? p.tnb[0] : 0u, tfin, sc, fst, out, dder, 0, err + 2, r1rows, 1u);
+                   p.n >= 1 ? p.tnb[0] : 0u, tfin, sc, fst, out, dder, 0, err + 2, r1rows, 1u, 0);
         }
     }
     // ---- rounds 2..d
@@ -1056,10 +1061,11 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
             if ((st = zkl_dist_allgather(ctx, rank_sums, gath, kSlots * sizeof(fr)))) return st;
             LAUNCH(ctx, k_fs_round, 1, 256, 0, s, k, p.d, p.n, variant, gath, (uint32_t)P, 0, tpart,
                    k <= p.n ? p.tnb[k - 1] : 0u, tfin, sc, fst, out, dder, derive ? 1 : 0, err + 2, 1u,
-                   (uint32_t)kSlots);
+                   (uint32_t)kSlots, (int)r.a1_derived);
         } else {
             LAUNCH(ctx, k_fs_round, 1, 256, 0, s, k, p.d, p.n, variant, partials + r.part_base, r.nblocks, 0, tpart,
-                   k <= p.n ? p.tnb[k - 1] : 0u, tfin, sc, fst, out, dder, derive ? 1 : 0, err + 2, r.nblocks, 1u);
+                   k <= p.n ? p.tnb[k - 1] : 0u, tfin, sc, fst, out, dder, derive ? 1 : 0, err + 2, r.nblocks, 1u,
+                   (int)r.a1_derived);
         }
     }
     if (!coop_done) {

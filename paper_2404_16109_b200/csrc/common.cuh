@@ -177,7 +177,8 @@ struct RoundDesc {
     uint32_t gbits;              // log2 of the group size G (pairs sharing one E_hi entry)
     uint32_t nblocks;            // partial rows (blocks / tiles) written for this round
     uint32_t direct_h1;          // 1: H(1) summed directly (round 1 of sumcheck_prove, u_c = 0)
-    uint32_t pad;
+    uint32_t a1_derived;         // 1: the round's kernel (k_round<FOLD>) does not sum a(1) = sum_y A(y,1); folding
+                                 // is linear, so a0_k + a1_k = a0_{k-1} + r_{k-1} (a1_{k-1} - a0_{k-1}) gives it
 };
 
 struct ProofScalars {

@@ -22,45 +22,82 @@ struct FsLocal {
 };
 
 // Round k of the Fiat-Shamir transcript from the round's sums (H(1) summed directly): g_k(0..3), absorb, r_k.
-// Single thread.  write: this thread also records the transcript (evals, derived r_k, sc->r).
-__device__ __noinline__ fr fs_round_core(int k, int d, const fr* s, const fr* tab, const ProofScalars* sc,
-                                         FsLocal& st, bool write, ProofOut* out, zkl_fr* derived,
-                                         ProofScalars* scw) {
-    const fr one = fr_one(), two = fr_two_m(), three = fr_three_m(), six = fr_six_m();
+// Warp-cooperative (all 32 lanes of one warp call): lanes 0..3 form g_k(t) for their t in parallel (the small
+// constant multiples by additions), lane 0 hashes; the sequential chain is 7 Montgomery products plus two SHA-256
+// calls, against ~20 products single-threaded.  s, tab: the round's sums (shared memory).  write: this warp also
+// records the transcript (evals, derived r_k, sc->r).  Returns r_k (Montgomery) in every lane.
+__device__ __noinline__ fr fs_round_warp(int k, int d, const fr* s, const fr* tab, const ProofScalars* sc,
+                                         FsLocal& st, bool write, ProofOut* out, zkl_fr* derived, ProofScalars* scw) {
+    const int lane = threadIdx.x & 31;
+    const fr one = fr_one();
     const fr u = sc->u[d - k];
     const fr coef = fs_mul(sc->alpha1, st.C);
-    const fr cl0 = fs_mul(coef, fr_sub(one, u)), cl1 = fs_mul(coef, u);
-    const fr cl2 = fs_mul(coef, fr_sub(fs_mul(three, u), one)), cl3 = fs_mul(coef, fr_sub(fs_mul(fr_five_m(), u), two));
-    const fr H0 = s[SLOT_H0], H1 = s[SLOT_H1], Hinf = s[SLOT_HINF], a0 = s[SLOT_A0], a1 = s[SLOT_A1];
-    const fr da = fr_sub(a1, a0);
-    const fr H2 = fr_add(fr_sub(fr_add(H1, H1), H0), fr_add(Hinf, Hinf));
-    const fr H3 = fr_add(fr_sub(fs_mul(three, H1), fr_add(H0, H0)), fs_mul(six, Hinf));
-    fr g[4];
-    g[0] = fr_add(fr_add(fs_mul(cl0, H0), a0), tab[0]);
-    g[1] = fr_add(fr_add(fs_mul(cl1, H1), a1), tab[1]);
-    g[2] = fr_add(fr_add(fs_mul(cl2, H2), fr_add(a0, fr_add(da, da))), tab[2]);
-    g[3] = fr_add(fr_add(fs_mul(cl3, H3), fr_add(a0, fs_mul(three, da))), tab[3]);
-    uint8_t msg[32 + 1 + 4 + 128];
-    int p = 0;
-    for (int i = 0; i < 32; ++i) msg[p++] = st.h[i];
-    msg[p++] = 'g';
-    for (int i = 0; i < 4; ++i) msg[p++] = (uint8_t)((uint32_t)k >> (8 * i));
-    for (int t = 0; t < 4; ++t) {
-        const zkl_fr c = fs_canon(g[t]);
-        if (write) out->evals[k - 1][t] = c;
-        for (int l = 0; l < 8; ++l)
-            for (int b = 0; b < 4; ++b) msg[p++] = (uint8_t)(c.w[l] >> (8 * b));
+    zkl_fr c;
+    for (int l = 0; l < 8; ++l) c.w[l] = 0;
+    if (lane < 4) {
+        const fr H0 = s[SLOT_H0], H1 = s[SLOT_H1], Hinf = s[SLOT_HINF], a0 = s[SLOT_A0], a1 = s[SLOT_A1];
+        const fr da = fr_sub(a1, a0);
+        const fr u2 = fr_add(u, u), H12 = fr_add(H1, H1), Hi2 = fr_add(Hinf, Hinf);
+        fr lt, H, at;
+        if (lane == 0) {            // l_0 = 1 - u
+            lt = fr_sub(one, u); H = H0; at = a0;
+        } else if (lane == 1) {     // l_1 = u
+            lt = u; H = H1; at = a1;
+        } else if (lane == 2) {     // l_2 = 3u - 1, H(2) = 2 H1 - H0 + 2 Hinf
+            lt = fr_sub(fr_add(u2, u), one);
+            H = fr_add(fr_sub(H12, H0), Hi2);
+            at = fr_add(a0, fr_add(da, da));
+        } else {                    // l_3 = 5u - 2, H(3) = 3 H1 - 2 H0 + 6 Hinf
+            lt = fr_sub(fr_add(fr_add(u2, u2), u), fr_add(one, one));
+            H = fr_add(fr_sub(fr_add(H12, H1), fr_add(H0, H0)), fr_add(fr_add(Hi2, Hi2), Hi2));
+            at = fr_add(a0, fr_add(fr_add(da, da), da));
+        }
+        const fr g = fr_add(fr_add(fs_mul(fs_mul(coef, lt), H), at), tab[lane]);
+        c = fs_canon(g);
+        if (write) out->evals[k - 1][lane] = c;
     }
-    sha256(msg, p, st.h);
-    const fr r = fs_challenge(st.h, "r", 1, (uint32_t)k);
-    const fr rm = fs_mul(r, fr_r2());
-    if (write) {
-        derived[3 + d + (k - 1)] = fs_canon_out(r);
-        scw->r[k - 1] = rm;
+    uint32_t cw[4][8];
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int l = 0; l < 8; ++l) cw[t][l] = __shfl_sync(0xffffffffu, c.w[l], t);
+    fr rm = fr_zero();
+    if (lane == 0) {
+        uint8_t msg[32 + 1 + 4 + 128];
+        int p = 0;
+        for (int i = 0; i < 32; ++i) msg[p++] = st.h[i];
+        msg[p++] = 'g';
+        for (int i = 0; i < 4; ++i) msg[p++] = (uint8_t)((uint32_t)k >> (8 * i));
+        for (int t = 0; t < 4; ++t)
+            for (int l = 0; l < 8; ++l)
+                for (int b = 0; b < 4; ++b) msg[p++] = (uint8_t)(cw[t][l] >> (8 * b));
+        sha256(msg, p, st.h);
+        const fr r = fs_challenge(st.h, "r", 1, (uint32_t)k);
+        rm = fs_mul(r, fr_r2());
+        if (write) {
+            derived[3 + d + (k - 1)] = fs_canon_out(r);
+            scw->r[k - 1] = rm;
+        }
+        const fr l0 = fr_sub(one, u);
+        st.C = fs_mul(st.C, fr_add(l0, fs_mul(rm, fr_sub(u, l0))));
     }
-    const fr l0 = fr_sub(one, u);
-    st.C = fs_mul(st.C, fr_add(l0, fs_mul(rm, fr_sub(u, l0))));
+#pragma unroll
+    for (int l = 0; l < 8; ++l) rm.v[l] = __shfl_sync(0xffffffffu, rm.v[l], 0);
     return rm;
+}
+
+// the constant table term tau 2^{-(k-n)} of a round k > n (lane 0; tau computed once, cached in *tau_cache)
+__device__ __forceinline__ fr fs_table_const(const fr* tfin, const ProofScalars* sc, int variant, FsLocal& st,
+                                             fr* tau_cache, bool& have_tau) {
+    if (!have_tau) {
+        const fr tb = tfin[0], tt = tfin[1], tm = tfin[2], te = tfin[3], beta = sc->beta;
+        *tau_cache = (variant == ZKL_VARIANT_PAPER)
+            ? fs_mul(tb, fr_sub(fs_mul(fs_mul(sc->alpha2, te), fr_add(tt, beta)), tm))
+            : fr_sub(fs_mul(fs_mul(sc->alpha2, te), fr_sub(fs_mul(tb, fr_add(tt, beta)), tm)), tb);
+        have_tau = true;
+    }
+    st.tscale = fs_mul(st.tscale, fr_inv2_m());
+    return fs_mul(*tau_cache, st.tscale);
 }
 
 constexpr int kCoopTabMax = 512;   // table entries (per vector) CTA 0 keeps in shared memory
@@ -135,8 +172,9 @@ __global__ void __launch_bounds__(kChunkThreads, 1) k_fs_rounds_coop(CoopFsArgs 
     fr* Ss = smem_fr + kChunk;
     fr* V = smem_fr + 2 * kChunk;
     __shared__ fr scratch[5 * (kChunkThreads / 32)];
-    __shared__ fr sh_r, sh_tab[4];
+    __shared__ fr sh_r, sh_tab[4], sh_s[5], sh_tau;
     __shared__ FsLocal st;
+    bool have_tau = false;   // (thread 0's) tau of the fully bound table
     const int t = threadIdx.x, nt = blockDim.x;
     const bool cta0 = blockIdx.x == 0;
     const uint32_t nchunks = gridDim.x;
@@ -202,19 +240,18 @@ __global__ void __launch_bounds__(kChunkThreads, 1) k_fs_rounds_coop(CoopFsArgs 
         }
         block_sum_fr<5>(s, scratch);
         if (t == 0) {
-            fr tab[4];
+            for (int q = 0; q < 5; ++q) sh_s[q] = s[q];
             if (k <= a.n) {
-                for (int q = 0; q < 4; ++q) tab[q] = a.tabbuf[(k - a.kc) * 4 + q];
+                for (int q = 0; q < 4; ++q) sh_tab[q] = a.tabbuf[(k - a.kc) * 4 + q];
             } else {
-                const fr tb = a.tfin[0], tt = a.tfin[1], tm = a.tfin[2], te = a.tfin[3];
-                const fr tau = (a.variant == ZKL_VARIANT_PAPER)
-                    ? fs_mul(tb, fr_sub(fs_mul(fs_mul(sc->alpha2, te), fr_add(tt, beta)), tm))
-                    : fr_sub(fs_mul(fs_mul(sc->alpha2, te), fr_sub(fs_mul(tb, fr_add(tt, beta)), tm)), tb);
-                st.tscale = fs_mul(st.tscale, fr_inv2_m());
-                const fr c = fs_mul(tau, st.tscale);
-                for (int q = 0; q < 4; ++q) tab[q] = c;
+                const fr c = fs_table_const(a.tfin, sc, a.variant, st, &sh_tau, have_tau);
+                for (int q = 0; q < 4; ++q) sh_tab[q] = c;
             }
-            sh_r = fs_round_core(k, a.d, s, tab, sc, st, cta0, a.out, a.derived, a.sc);
+        }
+        __syncthreads();
+        if (t < 32) {
+            const fr rk = fs_round_warp(k, a.d, sh_s, sh_tab, sc, st, cta0, a.out, a.derived, a.sc);
+            if (t == 0) sh_r = rk;
         }
         __syncthreads();
         const fr rk = sh_r;
@@ -273,20 +310,15 @@ __global__ void __launch_bounds__(kChunkThreads, 1) k_fs_rounds_coop(CoopFsArgs 
 #pragma unroll
                 for (int q = 0; q < 5; ++q) v[q] = fr_add(v[q], shfl_down_fr(v[q], off));
             if (t == 0) {
-                fr tab[4];
-                if (k <= a.n) {
-                    for (int q = 0; q < 4; ++q) tab[q] = sh_tab[q];
-                } else {
-                    const fr tb = a.tfin[0], tt = a.tfin[1], tm = a.tfin[2], te = a.tfin[3];
-                    const fr tau = (a.variant == ZKL_VARIANT_PAPER)
-                        ? fs_mul(tb, fr_sub(fs_mul(fs_mul(sc->alpha2, te), fr_add(tt, beta)), tm))
-                        : fr_sub(fs_mul(fs_mul(sc->alpha2, te), fr_sub(fs_mul(tb, fr_add(tt, beta)), tm)), tb);
-                    st.tscale = fs_mul(st.tscale, fr_inv2_m());
-                    const fr c = fs_mul(tau, st.tscale);
-                    for (int q = 0; q < 4; ++q) tab[q] = c;
+                for (int q = 0; q < 5; ++q) sh_s[q] = v[q];
+                if (k > a.n) {
+                    const fr c = fs_table_const(a.tfin, sc, a.variant, st, &sh_tau, have_tau);
+                    for (int q = 0; q < 4; ++q) sh_tab[q] = c;
                 }
-                sh_r = fs_round_core(k, a.d, v, tab, sc, st, true, a.out, a.derived, a.sc);
             }
+            __syncwarp();
+            const fr rk = fs_round_warp(k, a.d, sh_s, sh_tab, sc, st, true, a.out, a.derived, a.sc);
+            if (t == 0) sh_r = rk;
         }
         __syncthreads();
         const fr rk = sh_r;

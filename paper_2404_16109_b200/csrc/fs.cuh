@@ -30,6 +30,7 @@ struct FsState {
     fr tscale;   // 2^{-(k-n)} once the table coordinates are bound
     fr gprev[4]; // g_{k-1}(0..3), Montgomery: the running claim g_{k-1}(r_{k-1}) of a derived-H(1) round
     fr inv_cl1;  // 1 / (alpha1 C_k u_{d-k}) for round k (k_fs_inv, side stream, during round k's fold + eval)
+    fr aprev[2]; // a0_{k-1}, a1_{k-1}: a(1) of a round whose kernel did not sum it (RoundDesc::a1_derived)
 };
 
 // 1 / (alpha1 C_k u_{d-k}) for round k: launched once r_{k-1} (hence C_k) is known, overlapping k_round(k)
@@ -218,7 +219,7 @@ __global__ void k_rows_fold(const fr* __restrict__ part, uint32_t nrows, fr* out
 __global__ void k_fs_round(int k, int d, int n, int variant, const fr* __restrict__ part, uint32_t nrows,
                            int h01_one, const fr* __restrict__ tpart, uint32_t tnb, const fr* __restrict__ tfin,
                            ProofScalars* sc, FsState* st, ProofOut* out, zkl_fr* derived, int derive_h1,
-                           unsigned long long* miss, uint32_t slot_stride, uint32_t row_stride) {
+                           unsigned long long* miss, uint32_t slot_stride, uint32_t row_stride, int a1_derived) {
     __shared__ fr scratch[5 * 8];
     fr s[5];
     for (int q = 0; q < 5; ++q) {
@@ -234,6 +235,12 @@ __global__ void k_fs_round(int k, int d, int n, int variant, const fr* __restric
         block_sum_fr<4>(tab, scratch);
     }
     if (threadIdx.x != 0) return;
+    if (a1_derived) {   // a0_k + a1_k = a0_{k-1} + r_{k-1} (a1_{k-1} - a0_{k-1})
+        const fr p0 = st->aprev[0], p1 = st->aprev[1];
+        s[SLOT_A1] = fr_sub(fr_add(p0, fs_mul(sc->r[k - 2], fr_sub(p1, p0))), s[SLOT_A0]);
+    }
+    st->aprev[0] = s[SLOT_A0];
+    st->aprev[1] = s[SLOT_A1];
     const fr one = fr_one(), two = fr_two_m(), three = fr_three_m(), six = fr_six_m();
     if (k > n) {
         const fr tb = tfin[0], tt = tfin[1], tm = tfin[2], te = tfin[3];

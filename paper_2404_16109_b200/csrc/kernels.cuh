@@ -809,14 +809,14 @@ k_round(const uint32_t* __restrict__ Aold, const uint32_t* __restrict__ Sold, ui
         fr_wide_mac(cinf, e, fr_mul(fr_sub(A1, A0), fr_sub_lazy(S1, S0)));
         if (direct_h1) c1 = fr_add(c1, fr_mul(e, fr_mul(A1, fr_add_lazy(S1, beta))));
         fr_acc_add(a0, A0);
-        fr_acc_add(a1, A1);
+        if (!FOLD) fr_acc_add(a1, A1);   // FOLD rounds: a(1) follows from round k-1 (RoundDesc::a1_derived)
     }
     const fr eh = ehi[grp];
     fr H0 = fr_mul(eh, fr_wide_redc(c0));
     fr Hinf = fr_mul(eh, fr_wide_redc(cinf));
     fr H1 = direct_h1 ? fr_mul(eh, c1) : fr_zero();
     __shared__ fr scratch[5 * (kRoundThreads / 32)];
-    fr v[5] = {H0, H1, Hinf, fr_acc_final(a0), fr_acc_final(a1)};
+    fr v[5] = {H0, H1, Hinf, fr_acc_final(a0), FOLD ? fr_zero() : fr_acc_final(a1)};
     block_sum_fr<5>(v, scratch);
     if (threadIdx.x == 0) {
 #pragma unroll
@@ -1463,19 +1463,32 @@ __global__ void k_derive(const fr* __restrict__ gathered, int nranks, int dl, co
     __shared__ Affine form[kMaxRounds][4];    // g_k(t) as affine functions of c_{k-1}
     __shared__ Affine step[kMaxRounds];
     __shared__ fr claim[kMaxRounds + 1];
+    __shared__ fr sums[kMaxRounds][kSlots];
     const int k = threadIdx.x + 1;
     const fr one = fr_one(), zero = fr_zero();
     if (k <= d) {
-        fr s[5];
         for (int q = 0; q < 5; ++q) {
-            s[q] = zero;
+            fr v = zero;
             if (k <= dl) {
                 for (int p = 0; p < nranks; ++p)
-                    s[q] = fr_add(s[q], gathered[((uint64_t)p * dl + (k - 1)) * kSlots + q]);
+                    v = fr_add(v, gathered[((uint64_t)p * dl + (k - 1)) * kSlots + q]);
             } else {
-                s[q] = repl_sums[(k - dl - 1) * kSlots + q];
+                v = repl_sums[(k - dl - 1) * kSlots + q];
             }
+            sums[k - 1][q] = v;
         }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)   // a(1) of the FOLD rounds from the previous round (one product per such round)
+        for (int j = 2; j <= d; ++j)
+            if (rounds[j - 1].a1_derived) {
+                const fr p0 = sums[j - 2][SLOT_A0], p1 = sums[j - 2][SLOT_A1];
+                sums[j - 1][SLOT_A1] = fr_sub(fr_add(p0, fr_mul(sc->r[j - 2], fr_sub(p1, p0))), sums[j - 1][SLOT_A0]);
+            }
+    __syncthreads();
+    if (k <= d) {
+        fr s[5];
+        for (int q = 0; q < 5; ++q) s[q] = sums[k - 1][q];
         const RoundConst q = rc[k - 1];
         fr tab[4];
         if (k <= n) {
