@@ -106,7 +106,27 @@ def build_check() -> str:
     return out
 
 
+def build_variant(name: str, defines) -> str:
+    """Experiment variant build/exp_<name>.so: the tlookup translation unit compiled with extra -D flags (timing
+    experiments through ZKL_LIB, tools only; never the product path)."""
+    build()
+    objdir = os.path.join(HERE, "build")
+    out = os.path.join(objdir, f"exp_{name}.so")
+    obj = os.path.join(objdir, f"api_{name}.o")
+    cflags = [f for f in FLAGS if f != "-shared"]
+    subprocess.run([NVCC, *cflags, "-I", _nccl_include(), *defines, "-c", "-o", obj, os.path.join(CSRC, "api.cu")],
+                   check=True, capture_output=True)
+    subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, obj,
+                    os.path.join(objdir, "mm_api.o"), os.path.join(objdir, "hx_api.o"), "-ldl"], check=True,
+                   capture_output=True)
+    return out
+
+
 if __name__ == "__main__":
+    if "--variant" in sys.argv:   # python -m paper_2404_16109_b200.build --variant NAME -DFOO -DBAR=2
+        i = sys.argv.index("--variant")
+        print(build_variant(sys.argv[i + 1], sys.argv[i + 2:]))
+        sys.exit(0)
     if "--check" in sys.argv:
         print(build_check())
         sys.exit(0)

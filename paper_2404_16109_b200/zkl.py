@@ -16,7 +16,7 @@ from typing import Dict, List, Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("ZKL_LIB", os.path.join(HERE, "libzkl.so"))   # ZKL_LIB: experiment builds (tools only)
+LIB_PATH = os.environ.get("ZKL_LIB") or os.path.join(HERE, "libzkl.so")   # ZKL_LIB: experiment builds (tools only)
 R_MODULUS = 0x73EDA753299D7D483339D80809A1D80553BDA402FFFE5BFEFFFFFFFF00000001
 
 STATUS = ["ZKL_OK", "ZKL_E_ARG", "ZKL_E_SHAPE", "ZKL_E_NONCANONICAL", "ZKL_E_DUP_TABLE", "ZKL_E_NOT_IN_TABLE",
