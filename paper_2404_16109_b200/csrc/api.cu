@@ -24,6 +24,7 @@
 #include "coop.cuh"
 #include "fs.cuh"
 #include "kernels.cuh"
+#include "mhist.cuh"
 #include "host_common.h"
 #include "nccl_loader.h"
 #include "sha256_host.h"
@@ -33,6 +34,26 @@ using namespace zkl;
 namespace {
 
 using namespace zkl_host;
+
+// workspace of the N <= 2^16 histogram (csrc/mhist.cuh): digit-major low bytes, tot and rel [chunk][256], the 256
+// digit totals, partial rows [piece][256] (pieces <= chunks + 256)
+struct MhLayout {
+    size_t out, tot, rel, total, partial, bytes;
+};
+MhLayout mh_layout(uint64_t Dp) {
+    const uint64_t C = mh_chunks(Dp);
+    MhLayout l;
+    size_t o = 0;
+    auto take = [&](size_t b) { size_t r = o; o += (b + 255) & ~(size_t)255; return r; };
+    l.out = take(Dp + 16);
+    l.tot = take(sizeof(uint32_t) * C * kMhBins);
+    l.rel = take(sizeof(uint32_t) * C * kMhBins);
+    l.total = take(sizeof(uint32_t) * kMhBins);
+    l.partial = take(sizeof(uint32_t) * (C + kMhBins) * kMhBins);
+    l.bytes = o;
+    return l;
+}
+size_t mh_bytes(uint64_t Dp) { return mh_layout(Dp).bytes; }
 
 int hist_rows_for(uint64_t Dp, uint64_t N) {
     uint64_t ntiles = (Dp + kHistTile - 1) / kHistTile;
@@ -249,7 +270,7 @@ void make_plan(Plan& p, uint64_t D, uint64_t N, int P, int rank, bool prove_mode
     p.o_keys = take(sizeof(uint32_t) * std::max<uint64_t>(p.Dp, 4));
     // the histogram rows of an async-mode prepare are written on the low stream while the following proof runs, so
     // they too sit at an offset that depends only on (D_local, N): never inside any plan's proof buffers
-    p.o_hist = take(sizeof(uint32_t) * (size_t)p.hist_rows * N);
+    p.o_hist = take(std::max(sizeof(uint32_t) * (size_t)p.hist_rows * N, mh_bytes(p.Dp)));
     p.o_out = take(sizeof(ProofOut));
     p.o_sc = take(sizeof(ProofScalars));
     p.o_err = take(4 * sizeof(unsigned long long));
@@ -1190,6 +1211,9 @@ static int ctx_create_common(int device, void* stream, zkl_ctx** out) {
     cudaFuncSetAttribute(k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tail_smem);
     cudaFuncSetAttribute(k_batch_invert, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 1024 * (int)sizeof(fr));
     cudaFuncSetAttribute(k_tab_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kTabChunk * (int)sizeof(fr));
+    cudaFuncSetAttribute(k_mh_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMhSmem);
+    cudaFuncSetAttribute(k_mh_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMhScatterSmem);
+    cudaFuncSetAttribute(k_mh_lo, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMhSmem);
     cudaFuncSetAttribute(k_fs_rounds_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)((2 * kChunk + 4 * kCoopTabMax) * sizeof(fr)));
     cudaFuncSetAttribute(k_chunk_rounds_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1621,10 +1645,30 @@ static int prepare_impl(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* T,
         CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->low, ctx->ev_keys, 0));
         hs = ctx->low;
     }
-    // in the background a few CTAs suffice (the proof's kernels keep the rest of the GPU)
-    const int hrows = hist_low ? std::min(p.hist_rows, kHistAsyncRows) : p.hist_rows;
-    LAUNCH(ctx, k_hist_count, hrows, kHistThreads, 0, hs, keys, p.Dp, (uint32_t)T->N, rows, key_bits);
-    LAUNCH(ctx, k_hist_colsum, grid_for(T->N, 256), 256, 0, hs, rows, hrows, T->N, m_dev);
+    if (p.n <= 16) {
+        // N <= 2^16: the atomic-free two-digit counting passes (csrc/mhist.cuh)
+        const MhLayout l = mh_layout(p.Dp);
+        uint8_t* wsh = reinterpret_cast<uint8_t*>(rows);
+        uint32_t* tot = reinterpret_cast<uint32_t*>(wsh + l.tot);
+        uint32_t* rel = reinterpret_cast<uint32_t*>(wsh + l.rel);
+        uint32_t* total = reinterpret_cast<uint32_t*>(wsh + l.total);
+        uint32_t* partial = reinterpret_cast<uint32_t*>(wsh + l.partial);
+        const unsigned C = (unsigned)mh_chunks(p.Dp);
+        const bool two = p.n > 8;
+        LAUNCH(ctx, k_mh_count, C, kMhThreads, kMhSmem, hs, keys, p.Dp, two ? 8 : 0, tot);
+        LAUNCH(ctx, k_mh_scan, kMhBins, 256, 0, hs, tot, C, two ? rel : nullptr, total, two ? nullptr : m_dev,
+               (uint32_t)T->N);
+        if (two) {
+            LAUNCH(ctx, k_mh_scatter, C, kMhThreads, kMhScatterSmem, hs, keys, p.Dp, tot, rel, total, wsh + l.out);
+            LAUNCH(ctx, k_mh_lo, C + kMhBins, kMhThreads, kMhSmem, hs, wsh + l.out, total, m_dev, partial);
+            LAUNCH(ctx, k_mh_fix, (unsigned)(T->N >> 8), kMhThreads, 0, hs, total, partial, m_dev);
+        }
+    } else {
+        // in the background a few CTAs suffice (the proof's kernels keep the rest of the GPU)
+        const int hrows = hist_low ? std::min(p.hist_rows, kHistAsyncRows) : p.hist_rows;
+        LAUNCH(ctx, k_hist_count, hrows, kHistThreads, 0, hs, keys, p.Dp, (uint32_t)T->N, rows, key_bits);
+        LAUNCH(ctx, k_hist_colsum, grid_for(T->N, 256), 256, 0, hs, rows, hrows, T->N, m_dev);
+    }
     unsigned long long* herr = reinterpret_cast<unsigned long long*>((uint8_t*)ctx->host_out + 60000);
     {
         // the collectives follow the histogram on its stream (NCCL calls of one communicator stay in one order)

@@ -18,7 +18,7 @@ ch = wl.chal
 chal = zkl.Context.challenges(ch.beta, ch.alpha1, ch.alpha2, ch.u, ch.r)
 xd, yd = torch.from_numpy(wl.x).to(dev), torch.from_numpy(wl.y).to(dev)
 txd, tyd = torch.from_numpy(wl.tx).to(dev), torch.from_numpy(wl.ty).to(dev)
-S, T, tmem = ctx.vec(D), ctx.vec(wl.N), ctx.table_mem(wl.N)
+T, tmem = ctx.vec(wl.N), ctx.table_mem(wl.N)
 m = torch.empty(wl.N, dtype=torch.int32, device=dev)
 
 
@@ -27,8 +27,8 @@ def step():
     tab = ctx.table(T, tmem)
     ctx.table_attach_pair(tab, txd, tyd, ch.alpha_f)
     ctx.set_async(True)
-    ctx.prepare_pair(xd, yd, ch.alpha_f, D, tab, S, m)
-    pf = ctx.prove(S, D, tab, m, chal)
+    ctx.prepare_pair(xd, yd, ch.alpha_f, D, tab, m=m, virtual_s=True)   # the bench step: S virtual
+    pf = ctx.prove(None, D, tab, m, chal)
     ctx.wait()
     ctx.set_async(False)
     return pf.result()
