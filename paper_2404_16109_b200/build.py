@@ -112,13 +112,15 @@ def build_variant(name: str, defines) -> str:
     build()
     objdir = os.path.join(HERE, "build")
     out = os.path.join(objdir, f"exp_{name}.so")
-    obj = os.path.join(objdir, f"api_{name}.o")
     cflags = [f for f in FLAGS if f != "-shared"]
-    subprocess.run([NVCC, *cflags, "-I", _nccl_include(), *defines, "-c", "-o", obj, os.path.join(CSRC, "api.cu")],
+    objs = []
+    for src in SOURCES:   # every translation unit with the extra flags
+        obj = os.path.join(objdir, f"{src[:-3]}_{name}.o")
+        subprocess.run([NVCC, *cflags, "-I", _nccl_include(), *defines, "-c", "-o", obj, os.path.join(CSRC, src)],
+                       check=True, capture_output=True)
+        objs.append(obj)
+    subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, *objs, "-ldl"],
                    check=True, capture_output=True)
-    subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, obj,
-                    os.path.join(objdir, "mm_api.o"), os.path.join(objdir, "hx_api.o"), "-ldl"], check=True,
-                   capture_output=True)
     return out
 
 

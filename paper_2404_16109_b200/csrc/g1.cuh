@@ -114,8 +114,110 @@ __device__ __forceinline__ fq fq_sub(const fq& a, const fq& b) {
 __device__ __forceinline__ fq fq_neg(const fq& a) { return fq_is_zero(a) ? a : fq_sub(fq_zero(), a); }
 __device__ __forceinline__ fq fq_dbl(const fq& a) { return fq_add(a, a); }
 
-// CIOS Montgomery multiplication a b / 2^384 mod q (a, b < q; also valid for a < 2^384 when b < q: a b < R q)
-__device__ __forceinline__ fq fq_mul(const fq& a, const fq& b) {
+// Montgomery multiplication a b / 2^384 mod q (a, b < q), CIOS with aligned register pairs: the F_q analogue of
+// fr_mul (csrc/fr.cuh).  The running value is X + Y 2^32, X = x0..x12 aligned at word 0 and Y = y0..y11 aligned at
+// word 1; even products a_j b_i and m q_j go to X, odd ones to Y, so each lo/hi pair is one IMAD.WIDE.U32: 288
+// of them plus 12 IMAD for m = x0 q' (q' = -q^{-1} mod 2^32).  The dropped carries are zero (checked word by word
+// for random and extreme operands by tools/sim_fq_mul.py).
+#define ZKQ_MP(dl, dh, a, b, al, ah) \
+    "madc.lo.cc.u32 " dl ", " a ", " b ", " al ";\n\t" "madc.hi.cc.u32 " dh ", " a ", " b ", " ah ";\n\t"
+#define ZKQ_REDUCE()                                                                                     \
+    asm("{\n\t.reg .u32 m;\n\t" \
+        "mul.lo.u32 m, %0, 0xfffcfffd;\n\t" \
+        "mad.lo.cc.u32 %0, m, %25, %0;\n\t" \
+        "madc.hi.cc.u32 %1, m, %25, %1;\n\t" \
+        ZKQ_MP("%2", "%3", "m", "%27", "%2", "%3") \
+        ZKQ_MP("%4", "%5", "m", "%29", "%4", "%5") \
+        ZKQ_MP("%6", "%7", "m", "%31", "%6", "%7") \
+        ZKQ_MP("%8", "%9", "m", "%33", "%8", "%9") \
+        ZKQ_MP("%10", "%11", "m", "%35", "%10", "%11") \
+        "addc.u32 %12, %12, 0;\n\t" \
+        "mad.lo.cc.u32 %13, m, %26, %13;\n\t" \
+        "madc.hi.cc.u32 %14, m, %26, %14;\n\t" \
+        ZKQ_MP("%15", "%16", "m", "%28", "%15", "%16") \
+        ZKQ_MP("%17", "%18", "m", "%30", "%17", "%18") \
+        ZKQ_MP("%19", "%20", "m", "%32", "%19", "%20") \
+        ZKQ_MP("%21", "%22", "m", "%34", "%21", "%22") \
+        "madc.lo.cc.u32 %23, m, %36, %23;\n\t" \
+        "madc.hi.u32 %24, m, %36, %24;\n\t}" \
+        : "+r"(x[0]), "+r"(x[1]), "+r"(x[2]), "+r"(x[3]), "+r"(x[4]), "+r"(x[5]), "+r"(x[6]), "+r"(x[7]), "+r"(x[8]), "+r"(x[9]), "+r"(x[10]), "+r"(x[11]), "+r"(x[12]), "+r"(y[0]), "+r"(y[1]), "+r"(y[2]), "+r"(y[3]), "+r"(y[4]), "+r"(y[5]), "+r"(y[6]), "+r"(y[7]), "+r"(y[8]), "+r"(y[9]), "+r"(y[10]), "+r"(y[11]) \
+        : "n"(0xffffaaab), "n"(0xb9feffff), "n"(0xb153ffff), "n"(0x1eabfffe), "n"(0xf6b0f624), "n"(0x6730d2a0), "n"(0xf38512bf), "n"(0x64774b84), "n"(0x434bacd7), "n"(0x4b1ba7b6), "n"(0x397fe69a), "n"(0x1a0111ea))
+
+// One out-of-line copy by default: the group law inlines ~40 multiplications per kernel, and fully inlined
+// (~33k SASS instructions) the MSM kernel is bound by instruction fetch.  ZKL_FQ_INLINE restores inlining.
+#ifdef ZKL_FQ_INLINE
+#define ZKL_FQ_MUL_ATTR __device__ __forceinline__
+#else
+#define ZKL_FQ_MUL_ATTR static __device__ __noinline__
+#endif
+ZKL_FQ_MUL_ATTR fq fq_mul(const fq a, const fq b) {
+    uint32_t x[13], y[12];
+    {   // iteration 0: plain products
+        const uint32_t bi = b.v[0];
+#pragma unroll
+        for (int j = 0; j < 12; j += 2) {
+            const uint64_t p = (uint64_t)a.v[j] * bi, o = (uint64_t)a.v[j + 1] * bi;
+            x[j] = (uint32_t)p; x[j + 1] = (uint32_t)(p >> 32);
+            y[j] = (uint32_t)o; y[j + 1] = (uint32_t)(o >> 32);
+        }
+        x[12] = 0;
+    }
+    ZKQ_REDUCE();
+#pragma unroll
+    for (int i = 1; i < 12; ++i) {
+        const uint32_t bi = b.v[i];
+        uint32_t X[13], Y[12], M0;
+        asm("add.cc.u32 %0, %13, %14;\n\t"
+            ZKQ_MP("%1", "%2", "%26", "%32", "%15", "%16")
+            ZKQ_MP("%3", "%4", "%27", "%32", "%17", "%18")
+            ZKQ_MP("%5", "%6", "%28", "%32", "%19", "%20")
+            ZKQ_MP("%7", "%8", "%29", "%32", "%21", "%22")
+            ZKQ_MP("%9", "%10", "%30", "%32", "%23", "%24")
+            "madc.lo.cc.u32 %11, %31, %32, %25;\n\t"
+            "madc.hi.u32 %12, %31, %32, 0;"
+            : "=r"(M0), "=r"(Y[0]), "=r"(Y[1]), "=r"(Y[2]), "=r"(Y[3]), "=r"(Y[4]), "=r"(Y[5]), "=r"(Y[6]), "=r"(Y[7]), "=r"(Y[8]), "=r"(Y[9]), "=r"(Y[10]), "=r"(Y[11])
+            : "r"(y[0]), "r"(x[1]), "r"(x[2]), "r"(x[3]), "r"(x[4]), "r"(x[5]), "r"(x[6]), "r"(x[7]), "r"(x[8]), "r"(x[9]), "r"(x[10]), "r"(x[11]), "r"(x[12]), "r"(a.v[1]), "r"(a.v[3]), "r"(a.v[5]), "r"(a.v[7]), "r"(a.v[9]), "r"(a.v[11]), "r"(bi));
+        asm("mad.lo.cc.u32 %0, %25, %31, %13;\n\t"
+            "madc.hi.cc.u32 %1, %25, %31, %14;\n\t"
+            ZKQ_MP("%2", "%3", "%26", "%31", "%15", "%16")
+            ZKQ_MP("%4", "%5", "%27", "%31", "%17", "%18")
+            ZKQ_MP("%6", "%7", "%28", "%31", "%19", "%20")
+            ZKQ_MP("%8", "%9", "%29", "%31", "%21", "%22")
+            ZKQ_MP("%10", "%11", "%30", "%31", "%23", "%24")
+            "addc.u32 %12, 0, 0;"
+            : "=r"(X[0]), "=r"(X[1]), "=r"(X[2]), "=r"(X[3]), "=r"(X[4]), "=r"(X[5]), "=r"(X[6]), "=r"(X[7]), "=r"(X[8]), "=r"(X[9]), "=r"(X[10]), "=r"(X[11]), "=r"(X[12])
+            : "r"(M0), "r"(y[1]), "r"(y[2]), "r"(y[3]), "r"(y[4]), "r"(y[5]), "r"(y[6]), "r"(y[7]), "r"(y[8]), "r"(y[9]), "r"(y[10]), "r"(y[11]), "r"(a.v[0]), "r"(a.v[2]), "r"(a.v[4]), "r"(a.v[6]), "r"(a.v[8]), "r"(a.v[10]), "r"(bi));
+#pragma unroll
+        for (int k = 0; k < 13; ++k) x[k] = X[k];
+#pragma unroll
+        for (int k = 0; k < 12; ++k) y[k] = Y[k];
+        ZKQ_REDUCE();
+    }
+    // T = (x1..x12) + (y0..y11), both aligned at word 0; T < 2q
+    fq r;
+    asm("add.cc.u32 %0, %12, %24;\n\t"
+        "addc.cc.u32 %1, %13, %25;\n\t"
+        "addc.cc.u32 %2, %14, %26;\n\t"
+        "addc.cc.u32 %3, %15, %27;\n\t"
+        "addc.cc.u32 %4, %16, %28;\n\t"
+        "addc.cc.u32 %5, %17, %29;\n\t"
+        "addc.cc.u32 %6, %18, %30;\n\t"
+        "addc.cc.u32 %7, %19, %31;\n\t"
+        "addc.cc.u32 %8, %20, %32;\n\t"
+        "addc.cc.u32 %9, %21, %33;\n\t"
+        "addc.cc.u32 %10, %22, %34;\n\t"
+        "addc.u32 %11, %23, %35;"
+        : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5]), "=r"(r.v[6]), "=r"(r.v[7]), "=r"(r.v[8]), "=r"(r.v[9]), "=r"(r.v[10]), "=r"(r.v[11])
+        : "r"(x[1]), "r"(x[2]), "r"(x[3]), "r"(x[4]), "r"(x[5]), "r"(x[6]), "r"(x[7]), "r"(x[8]), "r"(x[9]), "r"(x[10]), "r"(x[11]), "r"(x[12]), "r"(y[0]), "r"(y[1]), "r"(y[2]), "r"(y[3]), "r"(y[4]), "r"(y[5]), "r"(y[6]), "r"(y[7]), "r"(y[8]), "r"(y[9]), "r"(y[10]), "r"(y[11]));
+    if (fq_geq_q(r)) fq_sub_q(r);
+    return r;
+}
+#undef ZKQ_REDUCE
+#undef ZKQ_MP
+
+// Portable CIOS (64-bit accumulation) for an unreduced left operand: a b / 2^384 mod q for any a < 2^384 and b < q
+// (a b < R q).  Only the hash to the field uses it (a 384-bit digest times R^2); fq_mul needs a, b < q.
+__device__ __forceinline__ fq fq_mul_wide_a(const fq& a, const fq& b) {
     uint32_t t[14];
 #pragma unroll
     for (int i = 0; i < 14; ++i) t[i] = 0;
@@ -149,6 +251,7 @@ __device__ __forceinline__ fq fq_mul(const fq& a, const fq& b) {
     if (t[12] || fq_geq_q(r)) fq_sub_q(r);
     return r;
 }
+
 
 __device__ __forceinline__ fq fq_sqr(const fq& a) { return fq_mul(a, a); }
 __device__ __forceinline__ fq fq_to_mont(const fq& a) { return fq_mul(a, fq_const(kQR2)); }
@@ -204,7 +307,12 @@ __device__ __forceinline__ g1j g1_from_affine(const g1a& a) {
 }
 
 // dbl-2009-l (a = 0): 2M + 5S
-__device__ __forceinline__ g1j g1_dbl(const g1j& p) {
+#ifdef ZKL_G1_NOINLINE
+#define ZKL_G1_ATTR static __device__ __noinline__
+#else
+#define ZKL_G1_ATTR __device__ __forceinline__
+#endif
+ZKL_G1_ATTR g1j g1_dbl(const g1j& p) {
     if (g1_is_inf(p)) return p;
     const fq A = fq_sqr(p.X), B = fq_sqr(p.Y), C = fq_sqr(B);
     fq D = fq_sub(fq_sub(fq_sqr(fq_add(p.X, B)), A), C);
@@ -219,7 +327,7 @@ __device__ __forceinline__ g1j g1_dbl(const g1j& p) {
 }
 
 // madd-2007-bl: Jacobian + affine, 7M + 4S, with the exceptional cases (P = inf, Q = inf, P = Q, P = -Q)
-__device__ __forceinline__ g1j g1_add_affine(const g1j& p, const g1a& q) {
+ZKL_G1_ATTR g1j g1_add_affine(const g1j& p, const g1a& q) {
     if (q.inf) return p;
     if (g1_is_inf(p)) return g1_from_affine(q);
     const fq Z1Z1 = fq_sqr(p.Z);

@@ -52,7 +52,7 @@ __device__ inline g1a hx_hash_to_curve(const uint8_t* tag, int tag_len, uint32_t
         fq A, Bq = fq_zero();
         for (int k = 0; k < 12; ++k) A.v[k] = w[k];
         for (int k = 0; k < 4; ++k) Bq.v[k] = w[12 + k];
-        const fq x = fq_add(fq_mul(A, fq_const(kQR2)), fq_mul(Bq, fq_const(kQR3)));
+        const fq x = fq_add(fq_mul_wide_a(A, fq_const(kQR2)), fq_mul(Bq, fq_const(kQR3)));   // A < 2^384 unreduced
         fq b4 = fq_zero();
         b4.v[0] = 4;
         const fq rhs = fq_add(fq_mul(fq_sqr(x), x), fq_to_mont(b4));
@@ -118,10 +118,29 @@ __global__ void k_hx_htables(const g1a* __restrict__ H, g1a* hw) {
     hw[k] = g1_to_affine(acc);
 }
 
-// canonical scalars (the digits are read from the integer value)
+// signed-magnitude canonical scalars: s in (r/2, r) is written as |s| = r - s with bit 255 set (s G = -(r - s) G),
+// so small signed values (X, Y, the table columns) have zero limbs above the first and cost one 32-bit chunk
 __global__ void k_hx_canon(const uint32_t* __restrict__ S, uint64_t n, uint32_t* out) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        st_fr(out, n, i, fr_from_mont(ld_fr(S, n, i)));
+    const fr half = [] {   // (r - 1) / 2
+        fr h;
+        h.v[0] = 0x80000000u; h.v[1] = 0x7fffffffu; h.v[2] = 0x7fff2dffu; h.v[3] = 0xa9ded201u;
+        h.v[4] = 0x04d0ec02u; h.v[5] = 0x199cec04u; h.v[6] = 0x94cebea4u; h.v[7] = 0x39f6d3a9u;
+        return h;
+    }();
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        fr c = fr_from_mont(ld_fr(S, n, i));
+        bool neg = false;
+        for (int l = 7; l >= 0; --l)
+            if (c.v[l] != half.v[l]) {
+                neg = c.v[l] > half.v[l];
+                break;
+            }
+        if (neg) {
+            c = fr_neg(c);
+            c.v[7] |= 0x80000000u;
+        }
+        st_fr(out, n, i, c);
+    }
 }
 
 // Work split: s = sum_g c_g 2^{32 g} (the 8 limbs of the canonical scalar), so
@@ -140,9 +159,15 @@ k_hx_commit_partial(const uint32_t* __restrict__ Sc, uint64_t D, uint64_t cols, 
     const uint64_t i0 = s * kHxSlice;
     const int len = (int)min((uint64_t)kHxSlice, cols - i0);
     const uint32_t* plane = Sc + (uint64_t)g * D + j * cols + i0;
-    uint32_t c[kHxSlice];
+    const uint32_t* top = Sc + (uint64_t)7 * D + j * cols + i0;   // limb 7: bit 31 is the sign (k_hx_canon)
+    uint32_t c[kHxSlice], neg = 0;
 #pragma unroll
-    for (int k = 0; k < kHxSlice; ++k) c[k] = k < len ? __ldg(plane + k) : 0u;
+    for (int k = 0; k < kHxSlice; ++k) {
+        c[k] = k < len ? __ldg(plane + k) : 0u;
+        const uint32_t t7 = k < len ? __ldg(top + k) : 0u;
+        neg |= (t7 >> 31) << k;
+        if (g == 7) c[k] &= 0x7fffffffu;
+    }
     g1j acc = g1_infinity();
 #pragma unroll 1
     for (int w = 7; w >= 0; --w) {
@@ -155,7 +180,11 @@ k_hx_commit_partial(const uint32_t* __restrict__ Sc, uint64_t D, uint64_t cols, 
 #pragma unroll 1
         for (int k = 0; k < len; ++k) {
             const uint32_t d = (c[k] >> (4 * w)) & 15u;
-            if (d) acc = g1_add_affine(acc, tab[(i0 + k) * kHxTab + d]);
+            if (d) {
+                g1a P = tab[(i0 + k) * kHxTab + d];
+                if ((neg >> k) & 1u) P.y = fq_neg(P.y);
+                acc = g1_add_affine(acc, P);
+            }
         }
     }
     partial[t] = acc;
@@ -188,7 +217,8 @@ __global__ void k_hx_commit_rows(const g1j* __restrict__ Q, uint64_t rows, const
     if (j >= rows) return;
     g1j acc = Q[j * kHxGroups + kHxGroups - 1];
     for (int g = kHxGroups - 2; g >= 0; --g) {
-        for (int k = 0; k < 32; ++k) acc = g1_dbl(acc);
+        if (!g1_is_inf(acc))   // small scalars: the high chunks are empty and cost no doublings
+            for (int k = 0; k < 32; ++k) acc = g1_dbl(acc);
         acc = g1_add(acc, Q[j * kHxGroups + g]);
     }
     if (rho_canon) {   // rho H = sum_w hw[w][digit_w] (htab: the 64 x 16 window table of H)
