@@ -890,7 +890,7 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
     if (preset)
         LAUNCH(ctx, k_fs_init_preset, 1, 1, 0, s, dpre, p.d, sc, fst, dder, p.pbits, p.rank);
     else
-        LAUNCH(ctx, k_fs_init, 1, 1, 0, s, dseed, D, N, variant, p.d, sc, fst, dder, p.pbits, p.rank);
+        LAUNCH(ctx, k_fs_init, 1, 32, 0, s, dseed, D, N, variant, p.d, sc, fst, dder, p.pbits, p.rank);
     LAUNCH(ctx, k_eq_fill, grid_for(p.arena, 256), 256, 0, s, jobs, p.njobs, p.arena, sc, arena);
     // ---- B = 1/(beta + T) and the table working vectors
     uint32_t* tB = at<uint32_t>(ctx, p.o_tB);
@@ -1077,15 +1077,25 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
             len /= 2;
         }
         if (side) CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_join, 0));
+        // the round's partial rows (one per k_round CTA: thousands in the big rounds) are first folded to 32 rows by 32
+        // CTAs, so the single-CTA derivation on the critical path of every round sums only those
+        const fr* rows = partials + r.part_base;
+        uint32_t nrows = r.nblocks;
+        if (nrows > 32) {
+            fr* folded = at<fr>(ctx, p.o_coop);   // scratch: the cooperative rounds use it only after this loop
+            LAUNCH(ctx, k_rows_fold, 32, 256, 0, s, rows, nrows, folded, 32u);
+            rows = folded;
+            nrows = 32;
+        }
         if (P > 1 && k <= p.dl) {   // a local round: its sums become global with one small all-gather
-            LAUNCH(ctx, k_rows_fold, 1, 256, 0, s, partials + r.part_base, r.nblocks, rank_sums, 1u);
+            LAUNCH(ctx, k_rows_fold, 1, 256, 0, s, rows, nrows, rank_sums, 1u);
             if ((st = zkl_dist_allgather(ctx, rank_sums, gath, kSlots * sizeof(fr)))) return st;
             LAUNCH(ctx, k_fs_round, 1, 256, 0, s, k, p.d, p.n, variant, gath, (uint32_t)P, 0, tpart,
                    k <= p.n ? p.tnb[k - 1] : 0u, tfin, sc, fst, out, dder, derive ? 1 : 0, err + 2, 1u,
                    (uint32_t)kSlots, (int)r.a1_derived);
         } else {
-            LAUNCH(ctx, k_fs_round, 1, 256, 0, s, k, p.d, p.n, variant, partials + r.part_base, r.nblocks, 0, tpart,
-                   k <= p.n ? p.tnb[k - 1] : 0u, tfin, sc, fst, out, dder, derive ? 1 : 0, err + 2, r.nblocks, 1u,
+            LAUNCH(ctx, k_fs_round, 1, 256, 0, s, k, p.d, p.n, variant, rows, nrows, 0, tpart,
+                   k <= p.n ? p.tnb[k - 1] : 0u, tfin, sc, fst, out, dder, derive ? 1 : 0, err + 2, nrows, 1u,
                    (int)r.a1_derived);
         }
     }

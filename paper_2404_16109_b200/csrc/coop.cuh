@@ -56,23 +56,18 @@ __device__ __noinline__ fr fs_round_warp(int k, int d, const fr* s, const fr* ta
         c = fs_canon(g);
         if (write) out->evals[k - 1][lane] = c;
     }
-    uint32_t cw[4][8];
+    uint32_t e[32];
 #pragma unroll
     for (int t = 0; t < 4; ++t)
 #pragma unroll
-        for (int l = 0; l < 8; ++l) cw[t][l] = __shfl_sync(0xffffffffu, c.w[l], t);
+        for (int l = 0; l < 8; ++l) e[8 * t + l] = __shfl_sync(0xffffffffu, c.w[l], t);
     fr rm = fr_zero();
     if (lane == 0) {
-        uint8_t msg[32 + 1 + 4 + 128];
-        int p = 0;
-        for (int i = 0; i < 32; ++i) msg[p++] = st.h[i];
-        msg[p++] = 'g';
-        for (int i = 0; i < 4; ++i) msg[p++] = (uint8_t)((uint32_t)k >> (8 * i));
-        for (int t = 0; t < 4; ++t)
-            for (int l = 0; l < 8; ++l)
-                for (int b = 0; b < 4; ++b) msg[p++] = (uint8_t)(cw[t][l] >> (8 * b));
-        sha256(msg, p, st.h);
-        const fr r = fs_challenge(st.h, "r", 1, (uint32_t)k);
+        uint32_t hw[8];
+        fs_h_load(st.h, hw);
+        sha256_round_msg(hw, (uint32_t)k, e);
+        fs_h_store(hw, st.h);
+        const fr r = fs_challenge_w(hw, "r", 1, (uint32_t)k);
         rm = fs_mul(r, fr_r2());
         if (write) {
             derived[3 + d + (k - 1)] = fs_canon_out(r);

@@ -60,6 +60,33 @@ __device__ inline fr fs_challenge(const uint8_t* h, const char* label, int llen,
     return fs_digest_to_fr(dg);
 }
 
+// the transcript digest as its 8 big-endian words and back
+__device__ __forceinline__ void fs_h_load(const uint8_t* h, uint32_t (&hw)[8]) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        hw[i] = ((uint32_t)h[4 * i] << 24) | ((uint32_t)h[4 * i + 1] << 16) | ((uint32_t)h[4 * i + 2] << 8) | h[4 * i + 3];
+}
+__device__ __forceinline__ void fs_h_store(const uint32_t (&hw)[8], uint8_t* h) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        h[4 * i] = (uint8_t)(hw[i] >> 24);
+        h[4 * i + 1] = (uint8_t)(hw[i] >> 16);
+        h[4 * i + 2] = (uint8_t)(hw[i] >> 8);
+        h[4 * i + 3] = (uint8_t)hw[i];
+    }
+}
+// chal(label, idx) from the digest words (= fs_challenge on the digest bytes)
+__device__ inline fr fs_challenge_w(const uint32_t (&hw)[8], const char* label, int llen, uint32_t idx) {
+    uint32_t dg[8];
+    sha256_chal_msg(hw, label, llen, idx, dg);
+    fr x;
+#pragma unroll
+    for (int l = 0; l < 8; ++l) x.v[l] = __byte_perm(dg[l], 0, 0x0123);   // little-endian integer of the digest
+    fr_reduce_once(x);
+    fr_reduce_once(x);
+    return x;
+}
+
 __device__ inline zkl_fr fs_canon_out(const fr& c) {
     zkl_fr z;
     for (int l = 0; l < 8; ++l) z.w[l] = c.v[l];
@@ -69,7 +96,9 @@ __device__ inline zkl_fr fs_canon_out(const fr& c) {
 // derive beta, alpha1, alpha2, u into sc (Montgomery) and `derived` (canonical: beta, alpha1, alpha2, u[d], r[d])
 __global__ void k_fs_init(const uint8_t* __restrict__ seed, uint64_t D, uint64_t N, int variant, int d,
                           ProofScalars* sc, FsState* st, zkl_fr* derived, int pbits, int rank) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    // thread 0: h_0, beta, alpha; then the d independent u_c in parallel (one warp, launched with 32 threads)
+    if (blockIdx.x != 0) return;
+    if (threadIdx.x == 0) {
     uint8_t msg[9 + 32 + 8 + 8 + 4];
     const char* tag = "zkl-fs-v1";
     int p = 0;
@@ -89,11 +118,21 @@ __global__ void k_fs_init(const uint8_t* __restrict__ seed, uint64_t D, uint64_t
     derived[0] = fs_canon_out(beta);
     derived[1] = fs_canon_out(a1);
     derived[2] = to_canon(a2m);
-    for (int c = 0; c < d; ++c) {
-        const fr u = fs_challenge(st->h, "u", 1, (uint32_t)c);
-        sc->u[c] = fr_to_mont(u);
-        derived[3 + c] = fs_canon_out(u);
     }
+    __syncwarp();
+    __threadfence_block();
+    {
+        uint32_t hw[8];
+        fs_h_load(st->h, hw);
+        for (int c = threadIdx.x; c < d; c += blockDim.x) {
+            const fr u = fs_challenge_w(hw, "u", 1, (uint32_t)c);
+            sc->u[c] = fr_to_mont(u);
+            derived[3 + c] = fs_canon_out(u);
+        }
+    }
+    __syncwarp();
+    __threadfence_block();
+    if (threadIdx.x != 0) return;
     // this rank's factor of e~(u, .): eq(u[0:log2 P], bits(rank)) (the top coordinates are the rank)
     fr re = fr_one();
     for (int b = 0; b < pbits; ++b) {
@@ -234,64 +273,97 @@ __global__ void k_fs_round(int k, int d, int n, int variant, const fr* __restric
             for (uint32_t b = threadIdx.x; b < tnb; b += blockDim.x) tab[q] = fr_add(tab[q], tpart[q * kMaxBlocks + b]);
         block_sum_fr<4>(tab, scratch);
     }
-    if (threadIdx.x != 0) return;
-    if (a1_derived) {   // a0_k + a1_k = a0_{k-1} + r_{k-1} (a1_{k-1} - a0_{k-1})
-        const fr p0 = st->aprev[0], p1 = st->aprev[1];
-        s[SLOT_A1] = fr_sub(fr_add(p0, fs_mul(sc->r[k - 2], fr_sub(p1, p0))), s[SLOT_A0]);
+    // the scalar part: warp 0, lanes 0..3 form g_k(t) for their t (the derived H(1) by Lagrange, lane t the
+    // term t), lane 0 hashes (word-level SHA-256): ~12 sequential products instead of ~35 on one thread
+    __shared__ fr sh_s[5], sh_tab[4];
+    if (threadIdx.x == 0) {
+        if (a1_derived) {   // a0_k + a1_k = a0_{k-1} + r_{k-1} (a1_{k-1} - a0_{k-1})
+            const fr p0 = st->aprev[0], p1 = st->aprev[1];
+            s[SLOT_A1] = fr_sub(fr_add(p0, fs_mul(sc->r[k - 2], fr_sub(p1, p0))), s[SLOT_A0]);
+        }
+        st->aprev[0] = s[SLOT_A0];
+        st->aprev[1] = s[SLOT_A1];
+        if (k > n) {
+            const fr tb = tfin[0], tt = tfin[1], tm = tfin[2], te = tfin[3];
+            const fr tau = (variant == ZKL_VARIANT_PAPER)
+                ? fs_mul(tb, fr_sub(fs_mul(fs_mul(sc->alpha2, te), fr_add(tt, sc->beta)), tm))
+                : fr_sub(fs_mul(fs_mul(sc->alpha2, te), fr_sub(fs_mul(tb, fr_add(tt, sc->beta)), tm)), tb);
+            st->tscale = fs_mul(st->tscale, fr_inv2_m());
+            const fr c = fs_mul(tau, st->tscale);
+            for (int q = 0; q < 4; ++q) tab[q] = c;
+        }
+        if (h01_one) { s[SLOT_H0] = fr_one(); s[SLOT_H1] = fr_one(); }
+        for (int q = 0; q < 5; ++q) sh_s[q] = s[q];
+        for (int q = 0; q < 4; ++q) sh_tab[q] = tab[q];
     }
-    st->aprev[0] = s[SLOT_A0];
-    st->aprev[1] = s[SLOT_A1];
-    const fr one = fr_one(), two = fr_two_m(), three = fr_three_m(), six = fr_six_m();
-    if (k > n) {
-        const fr tb = tfin[0], tt = tfin[1], tm = tfin[2], te = tfin[3];
-        const fr tau = (variant == ZKL_VARIANT_PAPER)
-            ? fs_mul(tb, fr_sub(fs_mul(fs_mul(sc->alpha2, te), fr_add(tt, sc->beta)), tm))
-            : fr_sub(fs_mul(fs_mul(sc->alpha2, te), fr_sub(fs_mul(tb, fr_add(tt, sc->beta)), tm)), tb);
-        st->tscale = fs_mul(st->tscale, fr_inv2_m());
-        const fr c = fs_mul(tau, st->tscale);
-        for (int q = 0; q < 4; ++q) tab[q] = c;
-    }
+    __syncthreads();
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    const fr one = fr_one();
     const fr u = sc->u[d - k];
     const fr coef = fs_mul(sc->alpha1, st->C);
-    const fr cl0 = fs_mul(coef, fr_sub(one, u)), cl1 = fs_mul(coef, u);
-    const fr cl2 = fs_mul(coef, fr_sub(fs_mul(three, u), one)), cl3 = fs_mul(coef, fr_sub(fs_mul(fr_five_m(), u), two));
-    fr H0 = s[SLOT_H0], H1 = s[SLOT_H1];
-    if (h01_one) { H0 = one; H1 = one; }
-    const fr Hinf = s[SLOT_HINF], a0 = s[SLOT_A0], a1 = s[SLOT_A1], da = fr_sub(a1, a0);
+    const fr H0 = sh_s[SLOT_H0], Hinf = sh_s[SLOT_HINF], a0 = sh_s[SLOT_A0], a1 = sh_s[SLOT_A1];
+    fr H1 = sh_s[SLOT_H1];
     if (derive_h1) {
-        // claim = g_{k-1}(x), x = r_{k-1}, by Lagrange on the nodes 0..3
-        const fr x = sc->r[k - 2];
-        const fr xm1 = fr_sub(x, one), xm2 = fr_sub(x, two), xm3 = fr_sub(x, three);
-        const fr xa = fs_mul(x, xm1), xb = fs_mul(xm2, xm3);
-        const fr L0 = fr_neg(fs_mul(fs_mul(xm1, xb), fr_inv6_m())), L1 = fs_mul(fs_mul(x, xb), fr_inv2_m());
-        const fr L2 = fr_neg(fs_mul(fs_mul(xa, xm3), fr_inv2_m())), L3 = fs_mul(fs_mul(xa, xm2), fr_inv6_m());
-        const fr claim = fr_add(fr_add(fs_mul(st->gprev[0], L0), fs_mul(st->gprev[1], L1)),
-                                fr_add(fs_mul(st->gprev[2], L2), fs_mul(st->gprev[3], L3)));
-        const fr rest = fr_sub(fr_sub(fr_sub(claim, fs_mul(cl0, H0)), fr_add(a0, a1)), fr_add(tab[0], tab[1]));
-        H1 = fs_mul(rest, st->inv_cl1);
-        if (fr_is_zero(cl1) && !fr_is_zero(coef)) atomicMin(miss, 0ull);
+        // claim = g_{k-1}(x), x = r_{k-1}, by Lagrange on the nodes 0..3: lane t its term g_{k-1}(t) L_t(x)
+        fr term = fr_zero();
+        if (lane < 4) {
+            const fr x = sc->r[k - 2], two = fr_add(one, one), three = fr_add(two, one);
+            const fr xm1 = fr_sub(x, one), xm2 = fr_sub(x, two), xm3 = fr_sub(x, three);
+            fr L;
+            if (lane == 0) L = fr_neg(fs_mul(fs_mul(xm1, fs_mul(xm2, xm3)), fr_inv6_m()));
+            else if (lane == 1) L = fs_mul(fs_mul(x, fs_mul(xm2, xm3)), fr_inv2_m());
+            else if (lane == 2) L = fr_neg(fs_mul(fs_mul(fs_mul(x, xm1), xm3), fr_inv2_m()));
+            else L = fs_mul(fs_mul(fs_mul(x, xm1), xm2), fr_inv6_m());
+            term = fs_mul(st->gprev[lane], L);
+        }
+#pragma unroll
+        for (int off = 2; off > 0; off >>= 1) term = fr_add(term, shfl_down_fr(term, off));
+        fr h1 = fr_zero();
+        if (lane == 0) {
+            const fr cl0 = fs_mul(coef, fr_sub(one, u));
+            const fr rest = fr_sub(fr_sub(fr_sub(term, fs_mul(cl0, H0)), fr_add(a0, a1)), fr_add(sh_tab[0], sh_tab[1]));
+            h1 = fs_mul(rest, st->inv_cl1);
+            if (fr_is_zero(fs_mul(coef, u)) && !fr_is_zero(coef)) atomicMin(miss, 0ull);
+        }
+#pragma unroll
+        for (int l = 0; l < 8; ++l) H1.v[l] = __shfl_sync(0xffffffffu, h1.v[l], 0);
     }
-    const fr H2 = fr_add(fr_sub(fr_add(H1, H1), H0), fr_add(Hinf, Hinf));
-    const fr H3 = fr_add(fr_sub(fs_mul(three, H1), fr_add(H0, H0)), fs_mul(six, Hinf));
-    fr g[4];
-    g[0] = fr_add(fr_add(fs_mul(cl0, H0), a0), tab[0]);
-    g[1] = fr_add(fr_add(fs_mul(cl1, H1), a1), tab[1]);
-    g[2] = fr_add(fr_add(fs_mul(cl2, H2), fr_add(a0, fr_add(da, da))), tab[2]);
-    g[3] = fr_add(fr_add(fs_mul(cl3, H3), fr_add(a0, fs_mul(three, da))), tab[3]);
-    uint8_t msg[32 + 1 + 4 + 128];
-    int p = 0;
-    for (int i = 0; i < 32; ++i) msg[p++] = st->h[i];
-    msg[p++] = 'g';
-    for (int i = 0; i < 4; ++i) msg[p++] = (uint8_t)((uint32_t)k >> (8 * i));
-    for (int t = 0; t < 4; ++t) {
-        st->gprev[t] = g[t];
-        const zkl_fr c = fs_canon(g[t]);
-        out->evals[k - 1][t] = c;
-        for (int l = 0; l < 8; ++l)
-            for (int b = 0; b < 4; ++b) msg[p++] = (uint8_t)(c.w[l] >> (8 * b));
+    zkl_fr c;
+    for (int l = 0; l < 8; ++l) c.w[l] = 0;
+    if (lane < 4) {
+        const fr da = fr_sub(a1, a0);
+        const fr u2 = fr_add(u, u), H12 = fr_add(H1, H1), Hi2 = fr_add(Hinf, Hinf);
+        fr lt, H, at;
+        if (lane == 0) {            // l_0 = 1 - u
+            lt = fr_sub(one, u); H = H0; at = a0;
+        } else if (lane == 1) {     // l_1 = u
+            lt = u; H = H1; at = a1;
+        } else if (lane == 2) {     // l_2 = 3u - 1, H(2) = 2 H1 - H0 + 2 Hinf
+            lt = fr_sub(fr_add(u2, u), one);
+            H = fr_add(fr_sub(H12, H0), Hi2);
+            at = fr_add(a0, fr_add(da, da));
+        } else {                    // l_3 = 5u - 2, H(3) = 3 H1 - 2 H0 + 6 Hinf
+            lt = fr_sub(fr_add(fr_add(u2, u2), u), fr_add(one, one));
+            H = fr_add(fr_sub(fr_add(H12, H1), fr_add(H0, H0)), fr_add(fr_add(Hi2, Hi2), Hi2));
+            at = fr_add(a0, fr_add(fr_add(da, da), da));
+        }
+        const fr g = fr_add(fr_add(fs_mul(fs_mul(coef, lt), H), at), sh_tab[lane]);
+        st->gprev[lane] = g;
+        c = fs_canon(g);
+        out->evals[k - 1][lane] = c;
     }
-    sha256(msg, p, st->h);
-    const fr r = fs_challenge(st->h, "r", 1, (uint32_t)k);
+    uint32_t e[32];
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int l = 0; l < 8; ++l) e[8 * t + l] = __shfl_sync(0xffffffffu, c.w[l], t);
+    if (lane != 0) return;
+    uint32_t hw[8];
+    fs_h_load(st->h, hw);
+    sha256_round_msg(hw, (uint32_t)k, e);
+    fs_h_store(hw, st->h);
+    const fr r = fs_challenge_w(hw, "r", 1, (uint32_t)k);
     derived[3 + d + (k - 1)] = fs_canon_out(r);
     const fr rm = fs_mul(r, fr_r2());
     sc->r[k - 1] = rm;

@@ -45,6 +45,87 @@ __device__ inline void sha256_block(uint32_t (&h)[8], const uint8_t* blk) {
     h[0] += a; h[1] += b; h[2] += c; h[3] += d; h[4] += e; h[5] += f; h[6] += g; h[7] += k;
 }
 
+// one compression from 16 message words (big-endian words of the byte stream).  One out-of-line copy with the 64
+// rounds as 4 passes of 16 unrolled rounds: the 16-word schedule window stays in registers (constant indices) and the
+// code is ~300 instructions instead of ~1,000 per inlined copy -- the transcript runs on one warp between grid
+// barriers, where a long straight-line stream misses the instruction cache on every round.
+static __device__ __noinline__ void sha256_block_w(uint32_t (&h)[8], const uint32_t* m) {
+    uint32_t w[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) w[i] = m[i];
+    uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], k = h[7];
+#pragma unroll 1
+    for (int r = 0; r < 64; r += 16) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            if (r > 0) {
+                const uint32_t w15 = w[(i + 1) & 15], w2 = w[(i + 14) & 15];
+                const uint32_t s0 = sha_rotr(w15, 7) ^ sha_rotr(w15, 18) ^ (w15 >> 3);
+                const uint32_t s1 = sha_rotr(w2, 17) ^ sha_rotr(w2, 19) ^ (w2 >> 10);
+                w[i] = w[i] + s0 + w[(i + 9) & 15] + s1;
+            }
+            const uint32_t S1 = sha_rotr(e, 6) ^ sha_rotr(e, 11) ^ sha_rotr(e, 25);
+            const uint32_t ch = (e & f) ^ (~e & g);
+            const uint32_t t1 = k + S1 + ch + kSha256K[r + i] + w[i];
+            const uint32_t S0 = sha_rotr(a, 2) ^ sha_rotr(a, 13) ^ sha_rotr(a, 22);
+            const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
+            const uint32_t t2 = S0 + mj;
+            k = g; g = f; f = e; e = d + t1; d = c; c = b; b = a; a = t1 + t2;
+        }
+    }
+    h[0] += a; h[1] += b; h[2] += c; h[3] += d; h[4] += e; h[5] += f; h[6] += g; h[7] += k;
+}
+
+__device__ __forceinline__ void sha256_init(uint32_t (&h)[8]) {
+    h[0] = 0x6a09e667u; h[1] = 0xbb67ae85u; h[2] = 0x3c6ef372u; h[3] = 0xa54ff53au;
+    h[4] = 0x510e527fu; h[5] = 0x9b05688cu; h[6] = 0x1f83d9abu; h[7] = 0x5be0cd19u;
+}
+
+// The two per-round transcript hashes on words, no byte buffers (the byte layout is the one
+// sha256() would hash).  hw: the digest as its 8 big-endian words.
+// h_k = SHA256(h_{k-1} || "g" || le32(k) || g_k(0..3) as 4 x 8 LE words): 165 bytes, 3 blocks
+static __device__ __noinline__ void sha256_round_msg(uint32_t (&hw)[8], uint32_t k, const uint32_t (&e)[32]) {
+    uint32_t m[48];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m[i] = hw[i];
+    m[8] = (0x67u << 24) | ((k & 0xffu) << 16) | (((k >> 8) & 0xffu) << 8) | ((k >> 16) & 0xffu);
+    uint32_t prev = k >> 24;   // the byte before the current word's first three
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        m[9 + j] = (prev << 24) | (__byte_perm(e[j], 0, 0x0123) >> 8);
+        prev = e[j] >> 24;
+    }
+    m[41] = (prev << 24) | (0x80u << 16);
+#pragma unroll
+    for (int i = 42; i < 47; ++i) m[i] = 0;
+    m[47] = 165u * 8u;
+    uint32_t h[8];
+    sha256_init(h);
+    sha256_block_w(h, m);
+    sha256_block_w(h, m + 16);
+    sha256_block_w(h, m + 32);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) hw[i] = h[i];
+}
+
+// SHA256(h || label || le32(idx)) for a label of <= 7 bytes (one block); d: the digest's big-endian words
+static __device__ __noinline__ void sha256_chal_msg(const uint32_t (&hw)[8], const char* label, int llen,
+                                                    uint32_t idx, uint32_t (&d)[8]) {
+    uint32_t m[16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m[i] = hw[i];
+#pragma unroll
+    for (int i = 8; i < 16; ++i) m[i] = 0;
+    const int n = 32 + llen + 4;
+    auto put = [&](int pos, uint32_t byte) { m[pos >> 2] |= byte << (24 - 8 * (pos & 3)); };
+    for (int i = 0; i < llen; ++i) put(32 + i, (uint8_t)label[i]);
+    for (int i = 0; i < 4; ++i) put(32 + llen + i, (idx >> (8 * i)) & 0xffu);
+    put(n, 0x80u);
+    m[15] = (uint32_t)n * 8u;
+    sha256_init(d);
+    sha256_block_w(d, m);
+}
+
 // digest (32 bytes, big-endian words as in FIPS 180-4) of msg[0..len); one out-of-line copy per translation unit
 static __device__ __noinline__ void sha256(const uint8_t* msg, uint32_t len, uint8_t* out) {
     uint32_t h[8] = {0x6a09e667u, 0xbb67ae85u, 0x3c6ef372u, 0xa54ff53au,
