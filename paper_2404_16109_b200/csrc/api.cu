@@ -703,10 +703,10 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
                         LAUNCH(ctx, (k_round<true, false, true>), r.nblocks, kRoundThreads, 0, s, nullptr, nullptr,
                                len, nA, nS, sc, k, arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, part, keys, TB);
                 } else if (r.direct_h1)
-                    LAUNCH(ctx, (k_round<true, true>), r.nblocks, kRoundThreads, 0, s, cA, cS, len, nA, nS, sc, k,
+                    LAUNCH(ctx, (k_round<true, true>), r.nblocks, kRoundThreads, kRoundStageSmem, s, cA, cS, len, nA, nS, sc, k,
                            arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, part);
                 else
-                    LAUNCH(ctx, (k_round<true, false>), r.nblocks, kRoundThreads, 0, s, cA, cS, len, nA, nS, sc, k,
+                    LAUNCH(ctx, (k_round<true, false>), r.nblocks, kRoundThreads, kRoundStageSmem, s, cA, cS, len, nA, nS, sc, k,
                            arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, part);
                 cA = nA; cS = nS;
                 len /= 2;
@@ -1067,10 +1067,10 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
                 LAUNCH(ctx, (k_round<true, true, true>), r.nblocks, kRoundThreads, 0, s, nullptr, nullptr, len, nA,
                        nS, sc, k, arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, partials + r.part_base, keys, TB);
         } else if (derive)
-            LAUNCH(ctx, (k_round<true, false>), r.nblocks, kRoundThreads, 0, s, cA, cS, len, nA, nS, sc, k,
+            LAUNCH(ctx, (k_round<true, false>), r.nblocks, kRoundThreads, kRoundStageSmem, s, cA, cS, len, nA, nS, sc, k,
                    arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, partials + r.part_base);
         else
-            LAUNCH(ctx, (k_round<true, true>), r.nblocks, kRoundThreads, 0, s, cA, cS, len, nA, nS, sc, k,
+            LAUNCH(ctx, (k_round<true, true>), r.nblocks, kRoundThreads, kRoundStageSmem, s, cA, cS, len, nA, nS, sc, k,
                    arena + r.elo_off, arena + r.ehi_off, (int)r.gbits, partials + r.part_base);
         if (k != p.dl + 1) {
             cA = nA; cS = nS;
@@ -1221,6 +1221,8 @@ static int ctx_create_common(int device, void* stream, zkl_ctx** out) {
     cudaFuncSetAttribute(k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tail_smem);
     cudaFuncSetAttribute(k_batch_invert, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 1024 * (int)sizeof(fr));
     cudaFuncSetAttribute(k_tab_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kTabChunk * (int)sizeof(fr));
+    cudaFuncSetAttribute(k_round<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRoundStageSmem);
+    cudaFuncSetAttribute(k_round<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRoundStageSmem);
     cudaFuncSetAttribute(k_mh_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMhSmem);
     cudaFuncSetAttribute(k_mh_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMhScatterSmem);
     cudaFuncSetAttribute(k_mh_lo, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMhSmem);

@@ -732,6 +732,21 @@ constexpr int kRoundThreads = 256;
 #define ZKL_ROUND_PREFETCH 1
 #endif
 
+#ifndef ZKL_ROUND_STAGE
+#define ZKL_ROUND_STAGE 1
+#endif
+// plain fold rounds: the next iteration's 4 old A and 4 old S of each thread (16 x 16 B, one per limb plane) are
+// copied to shared memory with cp.async while the current pair is computed, [plane][thread] so the 16-byte reads
+// are bank-conflict free; thread-private slots, so only cp.async.wait_all orders them (no block barrier)
+constexpr size_t kRoundStageSmem = (ZKL_ROUND_STAGE ? 16 * kRoundThreads * 16 : 0);
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // bulk prefetch of [p, p + bytes) into L2 (cp.async.bulk.prefetch; p 16-byte aligned, bytes a multiple of 16)
 __device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
@@ -771,6 +786,17 @@ k_round(const uint32_t* __restrict__ Aold, const uint32_t* __restrict__ Sold, ui
     fr_wide c0 = fr_wide_zero(), cinf = fr_wide_zero();
     fr c1 = fr_zero();
     fr_acc a0 = fr_acc_zero(), a1 = fr_acc_zero();
+    constexpr bool kStage = FOLD && !GATHER && ZKL_ROUND_STAGE;
+    extern __shared__ uint4 rstage[];   // [16 planes][kRoundThreads] (kStage)
+    auto stage_issue = [&](uint64_t yy) {
+#pragma unroll
+        for (int l = 0; l < 8; ++l) {
+            cp_async16(&rstage[l * kRoundThreads + threadIdx.x], Aold + (uint64_t)l * nold + 4 * yy);
+            cp_async16(&rstage[(8 + l) * kRoundThreads + threadIdx.x], Sold + (uint64_t)l * nold + 4 * yy);
+        }
+        cp_async_commit();
+    };
+    if (kStage && threadIdx.x < G) stage_issue((grp << gbits) + threadIdx.x);
     for (uint32_t yl = threadIdx.x; yl < G; yl += blockDim.x) {
         const uint64_t y = (grp << gbits) + yl;
 #if ZKL_ROUND_PREFETCH > 0
@@ -799,6 +825,25 @@ k_round(const uint32_t* __restrict__ Aold, const uint32_t* __restrict__ Sold, ui
                 S0 = fr_add(s0, fr_mul(rk, fr_sub_lazy(s1, s0)));
                 S1 = fr_add(s2, fr_mul(rk, fr_sub_lazy(s3, s2)));
             }
+            st_fr2(Snew, nnew, 2 * y, S0, S1);
+        } else if (kStage) {
+            cp_async_wait_all();
+            fr a[4], sv[4];
+#pragma unroll
+            for (int l = 0; l < 8; ++l) {
+                const uint4 qa = rstage[l * kRoundThreads + threadIdx.x];
+                const uint4 qs = rstage[(8 + l) * kRoundThreads + threadIdx.x];
+                a[0].v[l] = qa.x; a[1].v[l] = qa.y; a[2].v[l] = qa.z; a[3].v[l] = qa.w;
+                sv[0].v[l] = qs.x; sv[1].v[l] = qs.y; sv[2].v[l] = qs.z; sv[3].v[l] = qs.w;
+            }
+            A0 = fr_add(a[0], fr_mul(rk, fr_sub_lazy(a[1], a[0])));
+            A1 = fr_add(a[2], fr_mul(rk, fr_sub_lazy(a[3], a[2])));
+            S0 = fr_add(sv[0], fr_mul(rk, fr_sub_lazy(sv[1], sv[0])));
+            S1 = fr_add(sv[2], fr_mul(rk, fr_sub_lazy(sv[3], sv[2])));
+            // the slot is reused only after the folds consumed every word read from it (in-order issue: the copies
+            // cannot start before those reads returned); the copies then overlap the rest of this pair's work
+            if (yl + blockDim.x < G) stage_issue(y + blockDim.x);
+            st_fr2(Anew, nnew, 2 * y, A0, A1);
             st_fr2(Snew, nnew, 2 * y, S0, S1);
         } else if (FOLD) {
             {
