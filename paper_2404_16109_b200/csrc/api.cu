@@ -112,6 +112,13 @@ struct Plan {
 // groups of 2^gbits pairs (one CTA each, <= 64 pairs per thread): about 1024 CTAs per round from 2^20 pairs up (a
 // thread amortises its per-group reduction over as many pairs as ~3.5 waves allow), 512 below (latency-bound rounds
 // prefer short CTAs); measured against a fixed 2^12 on the B200: -0.09 ms over rounds 2..9 at H
+#ifndef ZKL_R1_TPC
+#define ZKL_R1_TPC 4
+#endif
+int r1_tiles_per_cta(uint64_t ntiles) {
+    return (ntiles % ZKL_R1_TPC == 0 && ntiles >= ZKL_R1_TPC * 3 * (uint64_t)kSMs * 2) ? ZKL_R1_TPC : 1;
+}
+
 int round_gbits(uint64_t np) {
     const int lg = ilog2(np);
     int gbits = std::max(8, std::min(14, lg - (lg >= 20 ? 10 : 9)));
@@ -634,19 +641,20 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
                 const uint4* TB = at<uint4>(ctx, p.o_tBaos);
                 const fr *elo1 = arena + p.rd[0].elo_off, *ehi1 = arena + p.rd[0].ehi_off;
                 fr* part1 = partials + p.rd[0].part_base;
-                const unsigned nb1 = (unsigned)p.ntiles;
+                const int tpc1 = r1_tiles_per_cta(p.ntiles);   // tiles per CTA (the per-CTA reductions amortised)
+            const unsigned nb1 = (unsigned)(p.ntiles / tpc1);
                 if (verify && Aw)
                     LAUNCH(ctx, (k_round1_keys<true, true>), nb1, kInvThreads, 0, s, a.S.limbs, p.Dp, keys, N, TB, Aw,
-                           elo1, ehi1, part1, (int)p.ntiles, err + 2);
+                           elo1, ehi1, part1, (int)p.ntiles, err + 2, tpc1);
                 else if (verify)
                     LAUNCH(ctx, (k_round1_keys<true, false>), nb1, kInvThreads, 0, s, a.S.limbs, p.Dp, keys, N, TB,
-                           Aw, elo1, ehi1, part1, (int)p.ntiles, err + 2);
+                           Aw, elo1, ehi1, part1, (int)p.ntiles, err + 2, tpc1);
                 else if (Aw)
                     LAUNCH(ctx, (k_round1_keys<false, true>), nb1, kInvThreads, 0, s, S1in, p.Dp, keys, N, TB, Aw,
-                           elo1, ehi1, part1, (int)p.ntiles, err + 2);
+                           elo1, ehi1, part1, (int)p.ntiles, err + 2, tpc1);
                 else
                     LAUNCH(ctx, (k_round1_keys<false, false>), nb1, kInvThreads, 0, s, S1in, p.Dp, keys, N, TB, Aw,
-                           elo1, ehi1, part1, (int)p.ntiles, err + 2);
+                           elo1, ehi1, part1, (int)p.ntiles, err + 2, tpc1);
             } else {
                 LAUNCH(ctx, k_gather_round1, (unsigned)p.ntiles, kInvThreads, 0, s, a.S.limbs, p.Dp, tv,
                        at<uint4>(ctx, p.o_tBaos), Abuf, arena + p.rd[0].elo_off, arena + p.rd[0].ehi_off,
@@ -945,19 +953,20 @@ int run_proof_fs(zkl_ctx* ctx, zkl_vec S, uint64_t D, const zkl_table* table, co
             const uint4* TB = at<uint4>(ctx, p.o_tBaos);
             const fr *elo1 = arena + p.rd[0].elo_off, *ehi1 = arena + p.rd[0].ehi_off;
             fr* part1 = partials + p.rd[0].part_base;
-            const unsigned nb1 = (unsigned)p.ntiles;
+            const int tpc1 = r1_tiles_per_cta(p.ntiles);   // tiles per CTA (the per-CTA reductions amortised)
+            const unsigned nb1 = (unsigned)(p.ntiles / tpc1);
             if (!virt && Aw)
                 LAUNCH(ctx, (k_round1_keys<true, true>), nb1, kInvThreads, 0, s, S.limbs, p.Dp, keys, N, TB, Aw, elo1,
-                       ehi1, part1, (int)p.ntiles, err + 2);
+                       ehi1, part1, (int)p.ntiles, err + 2, tpc1);
             else if (!virt)
                 LAUNCH(ctx, (k_round1_keys<true, false>), nb1, kInvThreads, 0, s, S.limbs, p.Dp, keys, N, TB, Aw, elo1,
-                       ehi1, part1, (int)p.ntiles, err + 2);
+                       ehi1, part1, (int)p.ntiles, err + 2, tpc1);
             else if (Aw)
                 LAUNCH(ctx, (k_round1_keys<false, true>), nb1, kInvThreads, 0, s, Sin, p.Dp, keys, N, TB, Aw, elo1,
-                       ehi1, part1, (int)p.ntiles, err + 2);
+                       ehi1, part1, (int)p.ntiles, err + 2, tpc1);
             else
                 LAUNCH(ctx, (k_round1_keys<false, false>), nb1, kInvThreads, 0, s, Sin, p.Dp, keys, N, TB, Aw, elo1,
-                       ehi1, part1, (int)p.ntiles, err + 2);
+                       ehi1, part1, (int)p.ntiles, err + 2, tpc1);
         } else
             LAUNCH(ctx, k_gather_round1, (unsigned)p.ntiles, kInvThreads, 0, s, S.limbs, p.Dp, tv,
                    at<uint4>(ctx, p.o_tBaos), Abuf, arena + p.rd[0].elo_off, arena + p.rd[0].ehi_off,

@@ -659,45 +659,58 @@ template <bool VERIFY, bool WRITE_A>
 __global__ void __launch_bounds__(kInvThreads, ZKL_R1_CTAS)
 k_round1_keys(const uint32_t* __restrict__ S, uint64_t n, const uint32_t* __restrict__ keys, uint64_t N,
               const uint4* __restrict__ TB, uint32_t* __restrict__ Aout, const fr* __restrict__ elo,
-              const fr* __restrict__ ehi, fr* partials, int rows, unsigned long long* miss) {
-    fr_wide acc = fr_wide_zero();   // sum of E_lo dA dS over the thread's 8 pairs, reduced once (fr_wide_*)
+              const fr* __restrict__ ehi, fr* partials, int rows, unsigned long long* miss, int tpc) {
+    // tpc consecutive tiles per CTA (CTA b: tiles b tpc .. b tpc + tpc - 1): per tile the E_lo-weighted sum of dA dS
+    // over the thread's 8 pairs is accumulated wide and scaled by that tile's E_hi; the sums of A and the block
+    // reduction are paid once per CTA.  The CTA's row is row b; rows b + gridDim.x j (j >= 1) are zeroed, so the
+    // round still has one row per tile.
+    fr hinf = fr_zero();
     fr_acc a0 = fr_acc_zero(), a1 = fr_acc_zero();
-    const uint64_t tile = blockIdx.x;
-    const uint64_t base = tile * kInvTile + 2 * threadIdx.x;
-    uint2 kn = __ldg(reinterpret_cast<const uint2*>(keys + base));
 #pragma unroll 1
-    for (int g = 0; g < 8; ++g) {
-        const uint64_t i0 = base + 512 * g;
-        uint2 k = kn;
-        if (g < 7) kn = __ldg(reinterpret_cast<const uint2*>(keys + i0 + 512));   // the next pair's keys
-        if (k.x >= N || k.y >= N) {
-            atomic_min_i64(miss, i0);
-            k.x = k.x >= N ? 0 : k.x;
-            k.y = k.y >= N ? 0 : k.y;
+    for (int q = 0; q < tpc; ++q) {
+        fr_wide acc = fr_wide_zero();
+        const uint64_t tile = (uint64_t)blockIdx.x * tpc + q;
+        const uint64_t base = tile * kInvTile + 2 * threadIdx.x;
+        uint2 kn = __ldg(reinterpret_cast<const uint2*>(keys + base));
+#pragma unroll 1
+        for (int g = 0; g < 8; ++g) {
+            const uint64_t i0 = base + 512 * g;
+            uint2 k = kn;
+            if (g < 7) kn = __ldg(reinterpret_cast<const uint2*>(keys + i0 + 512));   // the next pair's keys
+            if (k.x >= N || k.y >= N) {
+                atomic_min_i64(miss, i0);
+                k.x = k.x >= N ? 0 : k.x;
+                k.y = k.y >= N ? 0 : k.y;
+            }
+            ZKL_ASSERT(k.x < N && k.y < N);
+            const uint4* r0 = TB + 4 * (uint64_t)k.x;
+            const uint4* r1 = TB + 4 * (uint64_t)k.y;
+            const fr A0 = ld_fr_256(r0), A1 = ld_fr_256(r1);
+            const fr S0 = ld_fr_256(r0 + 2), S1 = ld_fr_256(r1 + 2);
+            if (VERIFY) {
+                fr x[2];
+                ld_fr2(S, n, i0, x);
+                if (!fr_eq(x[0], S0) || !fr_eq(x[1], S1)) atomic_min_i64(miss, i0);
+            }
+            if (WRITE_A) st_fr2(Aout, n, i0, A0, A1);
+            const fr dA = fr_sub(A1, A0), dS = fr_sub_lazy(S1, S0);
+            fr_wide_mac(acc, ld_fr_256(elo + 256 * g + threadIdx.x), fr_mul(dA, dS));
+            fr_acc_add(a0, A0);
+            fr_acc_add(a1, A1);
         }
-        ZKL_ASSERT(k.x < N && k.y < N);
-        const uint4* r0 = TB + 4 * (uint64_t)k.x;
-        const uint4* r1 = TB + 4 * (uint64_t)k.y;
-        const fr A0 = ld_fr_256(r0), A1 = ld_fr_256(r1);
-        const fr S0 = ld_fr_256(r0 + 2), S1 = ld_fr_256(r1 + 2);
-        if (VERIFY) {
-            fr x[2];
-            ld_fr2(S, n, i0, x);
-            if (!fr_eq(x[0], S0) || !fr_eq(x[1], S1)) atomic_min_i64(miss, i0);
-        }
-        if (WRITE_A) st_fr2(Aout, n, i0, A0, A1);
-        const fr dA = fr_sub(A1, A0), dS = fr_sub_lazy(S1, S0);
-        fr_wide_mac(acc, ld_fr_256(elo + 256 * g + threadIdx.x), fr_mul(dA, dS));
-        fr_acc_add(a0, A0);
-        fr_acc_add(a1, A1);
+        hinf = fr_add(hinf, fr_mul(ehi[tile], fr_wide_redc(acc)));
     }
-    fr v[3] = {fr_mul(ehi[tile], fr_wide_redc(acc)), fr_acc_final(a0), fr_acc_final(a1)};
+    fr v[3] = {hinf, fr_acc_final(a0), fr_acc_final(a1)};
     __shared__ fr scratch[3 * (kInvThreads / 32)];
     block_sum_fr<3>(v, scratch);
     if (threadIdx.x == 0) {
-        partials[SLOT_HINF * rows + tile] = v[0];
-        partials[SLOT_A0 * rows + tile] = v[1];
-        partials[SLOT_A1 * rows + tile] = v[2];
+        partials[SLOT_HINF * rows + blockIdx.x] = v[0];
+        partials[SLOT_A0 * rows + blockIdx.x] = v[1];
+        partials[SLOT_A1 * rows + blockIdx.x] = v[2];
+    }
+    if (threadIdx.x < 3 * (tpc - 1)) {
+        const int slot = threadIdx.x % 3 == 0 ? SLOT_HINF : (threadIdx.x % 3 == 1 ? SLOT_A0 : SLOT_A1);
+        partials[slot * rows + blockIdx.x + gridDim.x * (1 + threadIdx.x / 3)] = fr_zero();
     }
 }
 
