@@ -841,18 +841,26 @@ k_round(const uint32_t* __restrict__ Aold, const uint32_t* __restrict__ Sold, ui
             st_fr2(Snew, nnew, 2 * y, S0, S1);
         } else if (kStage) {
             cp_async_wait_all();
-            fr a[4], sv[4];
+            {   // A first, then S: half the loaded words live at a time
+                fr a[4];
 #pragma unroll
-            for (int l = 0; l < 8; ++l) {
-                const uint4 qa = rstage[l * kRoundThreads + threadIdx.x];
-                const uint4 qs = rstage[(8 + l) * kRoundThreads + threadIdx.x];
-                a[0].v[l] = qa.x; a[1].v[l] = qa.y; a[2].v[l] = qa.z; a[3].v[l] = qa.w;
-                sv[0].v[l] = qs.x; sv[1].v[l] = qs.y; sv[2].v[l] = qs.z; sv[3].v[l] = qs.w;
+                for (int l = 0; l < 8; ++l) {
+                    const uint4 qa = rstage[l * kRoundThreads + threadIdx.x];
+                    a[0].v[l] = qa.x; a[1].v[l] = qa.y; a[2].v[l] = qa.z; a[3].v[l] = qa.w;
+                }
+                A0 = fr_add(a[0], fr_mul(rk, fr_sub_lazy(a[1], a[0])));
+                A1 = fr_add(a[2], fr_mul(rk, fr_sub_lazy(a[3], a[2])));
             }
-            A0 = fr_add(a[0], fr_mul(rk, fr_sub_lazy(a[1], a[0])));
-            A1 = fr_add(a[2], fr_mul(rk, fr_sub_lazy(a[3], a[2])));
-            S0 = fr_add(sv[0], fr_mul(rk, fr_sub_lazy(sv[1], sv[0])));
-            S1 = fr_add(sv[2], fr_mul(rk, fr_sub_lazy(sv[3], sv[2])));
+            {
+                fr sv[4];
+#pragma unroll
+                for (int l = 0; l < 8; ++l) {
+                    const uint4 qs = rstage[(8 + l) * kRoundThreads + threadIdx.x];
+                    sv[0].v[l] = qs.x; sv[1].v[l] = qs.y; sv[2].v[l] = qs.z; sv[3].v[l] = qs.w;
+                }
+                S0 = fr_add(sv[0], fr_mul(rk, fr_sub_lazy(sv[1], sv[0])));
+                S1 = fr_add(sv[2], fr_mul(rk, fr_sub_lazy(sv[3], sv[2])));
+            }
             // the slot is reused only after the folds consumed every word read from it (in-order issue: the copies
             // cannot start before those reads returned); the copies then overlap the rest of this pair's work
             if (yl + blockDim.x < G) stage_issue(y + blockDim.x);
