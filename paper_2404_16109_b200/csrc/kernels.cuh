@@ -6,6 +6,10 @@
 
 namespace zkl {
 
+// One out-of-line copy of the Montgomery product for single-pass scalar kernels (k_derive, k_round_consts): inlined
+// there dozens of times, their code streams through the instruction cache once per launch.
+static __device__ __noinline__ fr fr_mul_s(const fr a, const fr b) { return fr_mul(a, b); }
+
 // ====================================================================== a1: boundary encode
 // canonical AoS (8 LE words per element) -> SoA Montgomery.  One Fr mul (x * R^2) per element.
 __global__ void k_import_canon(const uint32_t* __restrict__ src, uint64_t n, uint32_t* __restrict__ dst,
@@ -1481,26 +1485,26 @@ __global__ void k_round_consts(const ProofScalars* __restrict__ sc, int d, int n
             C[j] = c;
             const fr u = sc->u[d - j];
             const fr l0 = fr_sub(fr_one(), u);
-            c = fr_mul(c, fr_add(l0, fr_mul(sc->r[j - 1], fr_sub(u, l0))));
+            c = fr_mul_s(c, fr_add(l0, fr_mul_s(sc->r[j - 1], fr_sub(u, l0))));
         }
     }
     __syncthreads();
     if (k <= d) {
         const fr one = fr_one(), two = fr_two_m(), three = fr_three_m();
         const fr u = sc->u[d - k];
-        const fr coef = fr_mul(sc->alpha1, C[k]);
+        const fr coef = fr_mul_s(sc->alpha1, C[k]);
         RoundConst& q = rc[k - 1];
-        q.cl[0] = fr_mul(coef, fr_sub(one, u));
-        q.cl[1] = fr_mul(coef, u);
-        q.cl[2] = fr_mul(coef, fr_sub(fr_mul(three, u), one));
-        q.cl[3] = fr_mul(coef, fr_sub(fr_mul(fr_five_m(), u), two));
+        q.cl[0] = fr_mul_s(coef, fr_sub(one, u));
+        q.cl[1] = fr_mul_s(coef, u);
+        q.cl[2] = fr_mul_s(coef, fr_sub(fr_mul_s(three, u), one));
+        q.cl[3] = fr_mul_s(coef, fr_sub(fr_mul_s(fr_five_m(), u), two));
         const fr x = sc->r[k - 1];
         const fr xm1 = fr_sub(x, one), xm2 = fr_sub(x, two), xm3 = fr_sub(x, three);
         const fr inv2 = fr_inv2_m(), inv6 = fr_inv6_m();
-        q.L[0] = fr_neg(fr_mul(fr_mul(fr_mul(xm1, xm2), xm3), inv6));
-        q.L[1] = fr_mul(fr_mul(fr_mul(x, xm2), xm3), inv2);
-        q.L[2] = fr_neg(fr_mul(fr_mul(fr_mul(x, xm1), xm3), inv2));
-        q.L[3] = fr_mul(fr_mul(fr_mul(x, xm1), xm2), inv6);
+        q.L[0] = fr_neg(fr_mul_s(fr_mul_s(fr_mul_s(xm1, xm2), xm3), inv6));
+        q.L[1] = fr_mul_s(fr_mul_s(fr_mul_s(x, xm2), xm3), inv2);
+        q.L[2] = fr_neg(fr_mul_s(fr_mul_s(fr_mul_s(x, xm1), xm3), inv2));
+        q.L[3] = fr_mul_s(fr_mul_s(fr_mul_s(x, xm1), xm2), inv6);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1508,20 +1512,20 @@ __global__ void k_round_consts(const ProofScalars* __restrict__ sc, int d, int n
         fr pre[kMaxRounds], acc = fr_one();
         for (int j = 0; j < d; ++j) {
             pre[j] = acc;
-            if (!fr_is_zero(rc[j].cl[1])) acc = fr_mul(acc, rc[j].cl[1]);
+            if (!fr_is_zero(rc[j].cl[1])) acc = fr_mul_s(acc, rc[j].cl[1]);
         }
         fr iv = fr_inv(acc);
         for (int j = d - 1; j >= 0; --j) {
             if (fr_is_zero(rc[j].cl[1])) {
                 rc[j].inv_cl1 = fr_zero();
             } else {
-                rc[j].inv_cl1 = fr_mul(iv, pre[j]);
-                iv = fr_mul(iv, rc[j].cl[1]);
+                rc[j].inv_cl1 = fr_mul_s(iv, pre[j]);
+                iv = fr_mul_s(iv, rc[j].cl[1]);
             }
         }
         fr ts = fr_one();
         for (int j = 1; j <= d; ++j) {
-            if (j > n) ts = fr_mul(ts, fr_inv2_m());
+            if (j > n) ts = fr_mul_s(ts, fr_inv2_m());
             rc[j - 1].tscale = ts;
         }
     }
@@ -1566,7 +1570,7 @@ __global__ void k_derive(const fr* __restrict__ gathered, int nranks, int dl, co
         for (int j = 2; j <= d; ++j)
             if (rounds[j - 1].a1_derived) {
                 const fr p0 = sums[j - 2][SLOT_A0], p1 = sums[j - 2][SLOT_A1];
-                sums[j - 1][SLOT_A1] = fr_sub(fr_add(p0, fr_mul(sc->r[j - 2], fr_sub(p1, p0))), sums[j - 1][SLOT_A0]);
+                sums[j - 1][SLOT_A1] = fr_sub(fr_add(p0, fr_mul_s(sc->r[j - 2], fr_sub(p1, p0))), sums[j - 1][SLOT_A0]);
             }
     __syncthreads();
     if (k <= d) {
@@ -1579,56 +1583,56 @@ __global__ void k_derive(const fr* __restrict__ gathered, int nranks, int dl, co
         } else {
             const fr tb = tfin[0], tt = tfin[1], tm = tfin[2], te = tfin[3];
             const fr tau = (variant == ZKL_VARIANT_PAPER)
-                ? fr_mul(tb, fr_sub(fr_mul(fr_mul(sc->alpha2, te), fr_add(tt, sc->beta)), tm))
-                : fr_sub(fr_mul(fr_mul(sc->alpha2, te), fr_sub(fr_mul(tb, fr_add(tt, sc->beta)), tm)), tb);
-            const fr c = fr_mul(tau, q.tscale);
+                ? fr_mul_s(tb, fr_sub(fr_mul_s(fr_mul_s(sc->alpha2, te), fr_add(tt, sc->beta)), tm))
+                : fr_sub(fr_mul_s(fr_mul_s(sc->alpha2, te), fr_sub(fr_mul_s(tb, fr_add(tt, sc->beta)), tm)), tb);
+            const fr c = fr_mul_s(tau, q.tscale);
             for (int t = 0; t < 4; ++t) tab[t] = c;
         }
         fr H0 = s[SLOT_H0];
         const fr H1d = s[SLOT_H1], Hinf = s[SLOT_HINF], a0 = s[SLOT_A0], a1 = s[SLOT_A1];
         fr H1c = H1d;
         if (k == 1 && prove_mode) { H0 = one; H1c = one; }
-        const fr g0 = fr_add(fr_add(fr_mul(q.cl[0], H0), a0), tab[0]);
+        const fr g0 = fr_add(fr_add(fr_mul_s(q.cl[0], H0), a0), tab[0]);
         const bool direct = (k == 1) || rounds[k - 1].direct_h1 || fr_is_zero(q.cl[1]);
         // H1 = p1 c + q1
         fr p1 = zero, q1 = H1c;
         Affine g1;
         if (direct) {
-            g1 = Affine{zero, fr_add(fr_add(fr_mul(q.cl[1], H1c), a1), tab[1])};
+            g1 = Affine{zero, fr_add(fr_add(fr_mul_s(q.cl[1], H1c), a1), tab[1])};
         } else {
             p1 = q.inv_cl1;
-            q1 = fr_neg(fr_mul(fr_add(fr_add(g0, a1), tab[1]), q.inv_cl1));
+            q1 = fr_neg(fr_mul_s(fr_add(fr_add(g0, a1), tab[1]), q.inv_cl1));
             g1 = Affine{one, fr_neg(g0)};
         }
         const fr three = fr_three_m(), six = fr_six_m();
         const fr da = fr_sub(a1, a0);
         // H2 = -H0 + 2 H1 + 2 Hinf ; H3 = -2 H0 + 3 H1 + 6 Hinf
         const Affine H2{fr_add(p1, p1), fr_add(fr_sub(fr_add(q1, q1), H0), fr_add(Hinf, Hinf))};
-        const Affine H3{fr_mul(three, p1), fr_add(fr_sub(fr_mul(three, q1), fr_add(H0, H0)), fr_mul(six, Hinf))};
-        const Affine g2{fr_mul(q.cl[2], H2.a), fr_add(fr_add(fr_mul(q.cl[2], H2.b), fr_add(a0, fr_add(da, da))), tab[2])};
-        const Affine g3{fr_mul(q.cl[3], H3.a), fr_add(fr_add(fr_mul(q.cl[3], H3.b), fr_add(a0, fr_mul(three, da))), tab[3])};
+        const Affine H3{fr_mul_s(three, p1), fr_add(fr_sub(fr_mul_s(three, q1), fr_add(H0, H0)), fr_mul_s(six, Hinf))};
+        const Affine g2{fr_mul_s(q.cl[2], H2.a), fr_add(fr_add(fr_mul_s(q.cl[2], H2.b), fr_add(a0, fr_add(da, da))), tab[2])};
+        const Affine g3{fr_mul_s(q.cl[3], H3.a), fr_add(fr_add(fr_mul_s(q.cl[3], H3.b), fr_add(a0, fr_mul_s(three, da))), tab[3])};
         form[k - 1][0] = Affine{zero, g0};
         form[k - 1][1] = g1;
         form[k - 1][2] = g2;
         form[k - 1][3] = g3;
         // c_k = sum_t g_t L_t
-        step[k - 1] = Affine{fr_add(fr_add(fr_mul(g1.a, q.L[1]), fr_mul(g2.a, q.L[2])), fr_mul(g3.a, q.L[3])),
-                             fr_add(fr_add(fr_mul(g0, q.L[0]), fr_mul(g1.b, q.L[1])),
-                                    fr_add(fr_mul(g2.b, q.L[2]), fr_mul(g3.b, q.L[3])))};
+        step[k - 1] = Affine{fr_add(fr_add(fr_mul_s(g1.a, q.L[1]), fr_mul_s(g2.a, q.L[2])), fr_mul_s(g3.a, q.L[3])),
+                             fr_add(fr_add(fr_mul_s(g0, q.L[0]), fr_mul_s(g1.b, q.L[1])),
+                                    fr_add(fr_mul_s(g2.b, q.L[2]), fr_mul_s(g3.b, q.L[3])))};
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         fr c = (variant == ZKL_VARIANT_PAPER) ? fr_add(sc->alpha1, sc->alpha2) : sc->alpha1;
         for (int j = 0; j < d; ++j) {
             claim[j] = c;
-            c = fr_add(fr_mul(step[j].a, c), step[j].b);
+            c = fr_add(fr_mul_s(step[j].a, c), step[j].b);
         }
         claim[d] = c;
     }
     __syncthreads();
     if (k <= d) {
         const fr c = claim[k - 1];
-        for (int t = 0; t < 4; ++t) out->evals[k - 1][t] = to_canon(fr_add(fr_mul(form[k - 1][t].a, c), form[k - 1][t].b));
+        for (int t = 0; t < 4; ++t) out->evals[k - 1][t] = to_canon(fr_add(fr_mul_s(form[k - 1][t].a, c), form[k - 1][t].b));
     }
     if (threadIdx.x == 0) {
         out->finals[0] = to_canon(fin_loc[0]);
