@@ -562,10 +562,14 @@ int run_proof(zkl_ctx* ctx, uint64_t D, const ProveArgs& a, zkl_fr* round_evals,
                         {sizeof(hs->chal), sizeof(hs->rounds), sizeof(hs->jobs), sizeof(hs->tnb)})))
         return st;
     CUDA_TRY(ctx, cudaMemsetAsync(err, 0xff, 4 * sizeof(unsigned long long), sp));
-    LAUNCH(ctx, k_setup, 1, 1, 0, sp, chal, p.d, p.pbits, p.rank, N, D, sc);
-    LAUNCH(ctx, k_eq_fill, grid_for(p.arena, 256), 256, 0, sp, jobs, p.njobs, p.arena, sc, arena);
+    LAUNCH(ctx, k_setup, 1, 128, 0, sp, chal, p.d, p.pbits, p.rank, N, D, sc);
+    // the eq tables and the round constants on the side stream, beside the B inversion (both need only the
+    // challenges); the D side waits for the tables (ev_eq) with B (ev_b) before round 1
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev_fork, sp));
     CUDA_TRY(ctx, cudaStreamWaitEvent(s2, ctx->ev_fork, 0));
+    LAUNCH(ctx, k_eq_fill, grid_for(p.arena, 256), 256, 0, s2, jobs, p.njobs, p.arena, sc, arena);
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_eq, s2));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_eq, 0));
     RoundConst* rc = at<RoundConst>(ctx, p.o_rc);
     LAUNCH(ctx, k_round_consts, 1, 64, 0, s2, sc, p.d, p.n, rc);
 
@@ -1211,6 +1215,7 @@ static int ctx_create_common(int device, void* stream, zkl_ctx** out) {
         cudaEventCreateWithFlags(&c->ev_keys, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_m, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_eq, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fwd[0], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fwd[1], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_mid[0], cudaEventDisableTiming) != cudaSuccess ||
@@ -1349,6 +1354,7 @@ void zkl_ctx_destroy(zkl_ctx* c) {
     cudaEventDestroy(c->ev_keys);
     cudaEventDestroy(c->ev_m);
     cudaEventDestroy(c->ev_b);
+    cudaEventDestroy(c->ev_eq);
     for (int i = 0; i < 2; ++i) { cudaEventDestroy(c->ev_fwd[i]); cudaEventDestroy(c->ev_mid[i]); }
     cudaEventDestroy(c->ev_fork);
     cudaEventDestroy(c->ev_join);

@@ -225,6 +225,7 @@ struct zkl_ctx {
     cudaStream_t low;              // async-mode histogram (lowest priority: fills the gaps of the proof's critical path)
     cudaEvent_t ev_keys, ev_m;     // index keys written (main) / m written (low)
     cudaEvent_t ev_b;              // B = 1/(beta + T) written (main), for a table side moved to the side stream
+    cudaEvent_t ev_eq;             // the eq tables written (side stream, beside the B inversion)
     int m_pending;                 // ev_m recorded: the next consumer of m on the ctx stream must wait for it
     int prio_lo, prio_hi;
     cudaEvent_t ev_fork, ev_join;

@@ -1424,17 +1424,22 @@ __global__ void k_eq_fill(const EqJob* __restrict__ jobs, int njobs, uint64_t to
 // Canonical challenges -> Montgomery scalars; rank factor eq(u[0:p], rank); w = N / D.
 __global__ void k_setup(const zkl_fr* __restrict__ host_chal, int d, int pbits, int rank, uint64_t N, uint64_t D,
                         ProofScalars* sc) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    auto conv = [](const zkl_fr& z) {
+    // one thread per challenge (3 + 2d <= 83 Montgomery conversions in parallel, launched with 128 threads), then
+    // this rank's eq factor on thread 0
+    const int i = threadIdx.x;
+    if (blockIdx.x != 0) return;
+    if (i < 3 + 2 * d) {
         fr x;
-        for (int l = 0; l < 8; ++l) x.v[l] = z.w[l];
-        return fr_to_mont(x);
-    };
-    sc->beta = conv(host_chal[0]);
-    sc->alpha1 = conv(host_chal[1]);
-    sc->alpha2 = conv(host_chal[2]);
-    for (int c = 0; c < d; ++c) sc->u[c] = conv(host_chal[3 + c]);
-    for (int k = 0; k < d; ++k) sc->r[k] = conv(host_chal[3 + d + k]);
+        for (int l = 0; l < 8; ++l) x.v[l] = host_chal[i].w[l];
+        x = fr_to_mont(x);
+        if (i == 0) sc->beta = x;
+        else if (i == 1) sc->alpha1 = x;
+        else if (i == 2) sc->alpha2 = x;
+        else if (i < 3 + d) sc->u[i - 3] = x;
+        else sc->r[i - 3 - d] = x;
+    }
+    __syncthreads();
+    if (i != 0) return;
     fr re = fr_one();
     for (int b = 0; b < pbits; ++b) {
         const bool bit = (rank >> (pbits - 1 - b)) & 1;
