@@ -315,12 +315,22 @@ def main():
     if not args.no_fs:   # every P: one all-gather of the round sums per local round at P > 1
         seed = bytes(32)
 
+        fs_async = os.environ.get("ZKL_BENCH_FS_ASYNC", "1") == "1"
+
         def step_fs():
             ctx.import_pair(txd, tyd, ch.alpha_f, T)
             tab = ctx.table(T, tmem)
             ctx.table_attach_pair(tab, txd, tyd, ch.alpha_f)   # pair-range fast path of prepare_pair
-            ctx.prepare_pair(xd, yd, ch.alpha_f, D, tab, m=m, virtual_s=True)   # synchronous: a background
-            return ctx.prove_fs(None, D, tab, m, seed, args.variant)   # histogram only slows the FS rounds
+            if not fs_async:
+                ctx.prepare_pair(xd, yd, ch.alpha_f, D, tab, m=m, virtual_s=True)
+                return ctx.prove_fs(None, D, tab, m, seed, args.variant)
+            # as the main step: the histogram on the low-priority stream behind the proof (the table side waits for m)
+            ctx.set_async(True)
+            ctx.prepare_pair(xd, yd, ch.alpha_f, D, tab, m=m, virtual_s=True)
+            pending = ctx.prove_fs(None, D, tab, m, seed, args.variant)
+            ctx.wait()
+            ctx.set_async(False)
+            return pending.result()
 
         step_fs()
         torch.cuda.synchronize(dev)
