@@ -255,10 +255,19 @@ __global__ void k_rows_fold(const fr* __restrict__ part, uint32_t nrows, fr* out
 // probability ~2^-255) cannot be derived: the proof is flagged through `miss` and redone with H(1) summed.
 // part: the round's D-side rows; element (slot q, row b) at part[q * slot_stride + b * row_stride] (partial rows:
 // slot-major, slot_stride = nrows, row_stride = 1; P > 1: the all-gathered rank sums, rank-major, 1 and kSlots).
+#ifdef ZKL_FS_TIMING   // dev instrumentation (build variant only): per-phase clock64 deltas of k_fs_round, printed
+#define FS_T(i) do { if (threadIdx.x == 0) tt[i] = clock64(); } while (0)
+#else
+#define FS_T(i) do { } while (0)
+#endif
 __global__ void k_fs_round(int k, int d, int n, int variant, const fr* __restrict__ part, uint32_t nrows,
                            int h01_one, const fr* __restrict__ tpart, uint32_t tnb, const fr* __restrict__ tfin,
                            ProofScalars* sc, FsState* st, ProofOut* out, zkl_fr* derived, int derive_h1,
                            unsigned long long* miss, uint32_t slot_stride, uint32_t row_stride, int a1_derived) {
+#ifdef ZKL_FS_TIMING
+    long long tt[10];
+#endif
+    FS_T(0);
     __shared__ fr scratch[5 * 8];
     fr s[5];
     for (int q = 0; q < 5; ++q) {
@@ -267,12 +276,14 @@ __global__ void k_fs_round(int k, int d, int n, int variant, const fr* __restric
             s[q] = fr_add(s[q], part[(uint64_t)q * slot_stride + (uint64_t)b * row_stride]);
     }
     block_sum_fr<5>(s, scratch);
+    FS_T(1);
     fr tab[4] = {fr_zero(), fr_zero(), fr_zero(), fr_zero()};
     if (k <= n) {
         for (int q = 0; q < 4; ++q)
             for (uint32_t b = threadIdx.x; b < tnb; b += blockDim.x) tab[q] = fr_add(tab[q], tpart[q * kMaxBlocks + b]);
         block_sum_fr<4>(tab, scratch);
     }
+    FS_T(2);
     // the scalar part: warp 0, lanes 0..3 form g_k(t) for their t (the derived H(1) by Lagrange, lane t the
     // term t), lane 0 hashes (word-level SHA-256): ~12 sequential products instead of ~35 on one thread
     __shared__ fr sh_s[5], sh_tab[4];
@@ -297,6 +308,7 @@ __global__ void k_fs_round(int k, int d, int n, int variant, const fr* __restric
         for (int q = 0; q < 4; ++q) sh_tab[q] = tab[q];
     }
     __syncthreads();
+    FS_T(3);
     if (threadIdx.x >= 32) return;
     const int lane = threadIdx.x;
     const fr one = fr_one();
@@ -329,6 +341,7 @@ __global__ void k_fs_round(int k, int d, int n, int variant, const fr* __restric
 #pragma unroll
         for (int l = 0; l < 8; ++l) H1.v[l] = __shfl_sync(0xffffffffu, h1.v[l], 0);
     }
+    FS_T(4);
     zkl_fr c;
     for (int l = 0; l < 8; ++l) c.w[l] = 0;
     if (lane < 4) {
@@ -359,16 +372,25 @@ __global__ void k_fs_round(int k, int d, int n, int variant, const fr* __restric
 #pragma unroll
         for (int l = 0; l < 8; ++l) e[8 * t + l] = __shfl_sync(0xffffffffu, c.w[l], t);
     if (lane != 0) return;
+    FS_T(5);
     uint32_t hw[8];
     fs_h_load(st->h, hw);
     sha256_round_msg(hw, (uint32_t)k, e);
     fs_h_store(hw, st->h);
+    FS_T(6);
     const fr r = fs_challenge_w(hw, "r", 1, (uint32_t)k);
+    FS_T(7);
     derived[3 + d + (k - 1)] = fs_canon_out(r);
     const fr rm = fs_mul(r, fr_r2());
     sc->r[k - 1] = rm;
     const fr l0 = fr_sub(one, u);
     st->C = fs_mul(st->C, fr_add(l0, fs_mul(rm, fr_sub(u, l0))));
+    FS_T(8);
+#ifdef ZKL_FS_TIMING
+    printf("fs_round k=%d rows=%lld tab=%lld t0sec=%lld coef+h1=%lld g=%lld sha=%lld chal=%lld tail=%lld total=%lld\n",
+           k, tt[1] - tt[0], tt[2] - tt[1], tt[3] - tt[2], tt[4] - tt[3], tt[5] - tt[4], tt[6] - tt[5], tt[7] - tt[6],
+           tt[8] - tt[7], tt[8] - tt[0]);
+#endif
 }
 
 __global__ void k_fs_finish(const fr* __restrict__ fin, const fr* __restrict__ tfin, ProofOut* out) {
