@@ -90,3 +90,20 @@ def test_prove_eval(ctx):
     assert ctx.export_ints(w) == ow and y == oy == mle.mle_eval(S, v)
     G, Hb = ctx.hyrax_generators(pp)
     assert HX.verify_eval(C, cols, G, Hb, v[:4], v[4:], ow, oy, rho)
+
+
+def test_commit_signed_magnitude_boundaries(ctx, pp8):
+    """k_hx_canon commits s > (r-1)/2 as -(r - s) (the table point negated): scalars on both sides of the split,
+    small negatives (one 32-bit chunk), and rows that are all small (no Horner doublings) equal the oracle's."""
+    from paper_2404_16109_b200 import zkl
+    h = (R - 1) // 2
+    cols, rows = 8, 4
+    S = [h, h + 1, h - 1, h + 2, R - 1, R - 2, 1, 0,                          # around the split
+         R - 5, 7, R - (1 << 31), (1 << 31) - 1, R - (1 << 32) + 1, (1 << 32) - 1, R - 255, 3,   # small signed
+         R - 1, R - 1, R - 1, R - 1, R - 1, R - 1, R - 1, R - 1,             # all -1: one negated chunk each
+         (1 << 254), R - (1 << 254), h + (1 << 200), h - (1 << 200), 2, R - 2, 1 << 40, R - (1 << 40)]
+    ctx.reserve(1 << 12, 1 << 4)
+    Sv = ctx.import_canon(zkl.ints_to_canon(S))
+    C = ctx.hyrax_commit(pp8, Sv, rows * cols, None)
+    G, H = HX.generators(cols)
+    assert C == HX.commit(S, cols, G, H)
