@@ -404,7 +404,7 @@ def main():
     # take alternate steps, so one step's PCIe copy overlaps the other's proof -- the way a server keeps two requests
     # in flight.  Timed with CUDA events: the first step's start on its stream to the last step's end on its stream.
     xh, yh, txh, tyh = (t.pin_memory() for t in (x, y, tx, ty))
-    nctx = 2 if world == 1 else 1
+    nctx = int(os.environ.get("ZKL_E2E_INFLIGHT", "0")) or (2 if world == 1 else 1)
     e2e_streams = [torch.cuda.Stream(device=dev) for _ in range(nctx)]
     e2e_ctx = [ctx] if nctx == 1 else []
     for i in range(len(e2e_ctx), nctx):
