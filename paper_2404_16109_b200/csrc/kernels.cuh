@@ -234,23 +234,48 @@ k_import_pair_range(const int32_t* __restrict__ x, const int32_t* __restrict__ y
     __syncthreads();
     bool missed = false;
     if ((n & 3) == 0) {
-        for (uint64_t i = 4 * (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x); i < n;
-             i += 4 * (uint64_t)gridDim.x * blockDim.x) {
+        // two groups of 4 lookups per step: both groups' x, y loads and ty gathers are in flight together
+        const uint64_t stride = 4 * (uint64_t)gridDim.x * blockDim.x;
+        for (uint64_t i = 4 * (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x); i < n; i += 2 * stride) {
+            const uint64_t i2 = i + stride;
+            const bool two = i2 < n;
             const int4 xv = __ldg(reinterpret_cast<const int4*>(x + i));
             const int4 yv = __ldg(reinterpret_cast<const int4*>(y + i));
-            const int xs[4] = {xv.x, xv.y, xv.z, xv.w}, ys[4] = {yv.x, yv.y, yv.z, yv.w};
-            uint32_t kk[4];
-            fr s[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int64_t j = (int64_t)xs[q] - (int64_t)x0;
-                const bool ok = j >= 0 && (uint64_t)j < N && __ldg(ty + j) == ys[q];
-                missed |= !ok;
-                kk[q] = ok ? (uint32_t)j : 0u;
-                if (dst) s[q] = fr_from_small_pair(xs[q], ys[q], c);
+            int4 xv2 = make_int4(0, 0, 0, 0), yv2 = make_int4(0, 0, 0, 0);
+            if (two) {
+                xv2 = __ldg(reinterpret_cast<const int4*>(x + i2));
+                yv2 = __ldg(reinterpret_cast<const int4*>(y + i2));
             }
-            if (dst) st_fr4(dst, n, i, s);
+            const int xs[8] = {xv.x, xv.y, xv.z, xv.w, xv2.x, xv2.y, xv2.z, xv2.w};
+            const int ys[8] = {yv.x, yv.y, yv.z, yv.w, yv2.x, yv2.y, yv2.z, yv2.w};
+            int64_t jj[8];
+            int32_t tyv[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                jj[q] = (int64_t)xs[q] - (int64_t)x0;
+                const bool inr = jj[q] >= 0 && (uint64_t)jj[q] < N && (q < 4 || two);
+                tyv[q] = inr ? __ldg(ty + jj[q]) : ~ys[q];
+            }
+            uint32_t kk[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const bool ok = tyv[q] == ys[q];
+                if (q < 4 || two) missed |= !ok;
+                kk[q] = ok ? (uint32_t)jj[q] : 0u;
+            }
+            if (dst) {
+                fr s4[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) s4[q] = fr_from_small_pair(xs[q], ys[q], c);
+                st_fr4(dst, n, i, s4);
+                if (two) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) s4[q] = fr_from_small_pair(xs[4 + q], ys[4 + q], c);
+                    st_fr4(dst, n, i2, s4);
+                }
+            }
             *reinterpret_cast<uint4*>(keys + i) = make_uint4(kk[0], kk[1], kk[2], kk[3]);
+            if (two) *reinterpret_cast<uint4*>(keys + i2) = make_uint4(kk[4], kk[5], kk[6], kk[7]);
         }
     } else {
         for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
