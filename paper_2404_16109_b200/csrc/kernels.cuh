@@ -774,6 +774,9 @@ constexpr int kRoundThreads = 256;
 #define ZKL_ROUND_PREFETCH 1
 #endif
 
+#ifndef ZKL_ROUND_A0_SMEM
+#define ZKL_ROUND_A0_SMEM 1
+#endif
 #ifndef ZKL_ROUND_STAGE
 #define ZKL_ROUND_STAGE 1
 #endif
@@ -827,7 +830,14 @@ k_round(const uint32_t* __restrict__ Aold, const uint32_t* __restrict__ Sold, ui
     const uint64_t grp = blockIdx.x;
     fr_wide c0 = fr_wide_zero(), cinf = fr_wide_zero();
     fr c1 = fr_zero();
+#if ZKL_ROUND_A0_SMEM
+    // the fold rounds' sum of A(., 0) in shared memory (9 words per thread): 9 fewer live registers in the pair loop
+    __shared__ fr_acc sh_a0[kRoundThreads];
+    sh_a0[threadIdx.x] = fr_acc_zero();
+    fr_acc a1 = fr_acc_zero();
+#else
     fr_acc a0 = fr_acc_zero(), a1 = fr_acc_zero();
+#endif
     constexpr bool kStage = FOLD && !GATHER && ZKL_ROUND_STAGE;
     extern __shared__ uint4 rstage[];   // [16 planes][kRoundThreads] (kStage)
     auto stage_issue = [&](uint64_t yy) {
@@ -920,7 +930,11 @@ k_round(const uint32_t* __restrict__ Aold, const uint32_t* __restrict__ Sold, ui
         fr_wide_mac(c0, e, fr_mul(A0, fr_add_lazy(S0, beta)));
         fr_wide_mac(cinf, e, fr_mul(fr_sub(A1, A0), fr_sub_lazy(S1, S0)));
         if (direct_h1) c1 = fr_add(c1, fr_mul(e, fr_mul(A1, fr_add_lazy(S1, beta))));
+#if ZKL_ROUND_A0_SMEM
+        fr_acc_add(sh_a0[threadIdx.x], A0);
+#else
         fr_acc_add(a0, A0);
+#endif
         if (!FOLD) fr_acc_add(a1, A1);   // FOLD rounds: a(1) follows from round k-1 (RoundDesc::a1_derived)
     }
     const fr eh = ehi[grp];
@@ -928,6 +942,9 @@ k_round(const uint32_t* __restrict__ Aold, const uint32_t* __restrict__ Sold, ui
     fr Hinf = fr_mul(eh, fr_wide_redc(cinf));
     fr H1 = direct_h1 ? fr_mul(eh, c1) : fr_zero();
     __shared__ fr scratch[5 * (kRoundThreads / 32)];
+#if ZKL_ROUND_A0_SMEM
+    const fr_acc a0 = sh_a0[threadIdx.x];
+#endif
     fr v[5] = {H0, H1, Hinf, fr_acc_final(a0), FOLD ? fr_zero() : fr_acc_final(a1)};
     block_sum_fr<5>(v, scratch);
     if (threadIdx.x == 0) {
