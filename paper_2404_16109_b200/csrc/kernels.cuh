@@ -681,6 +681,9 @@ k_gather_keys_round1(const uint32_t* __restrict__ S, uint64_t n, const uint32_t*
 // by inversion).  WRITE_A: A is written for the caller (A is an output of Prove); otherwise A is
 // never materialised: round 2 gathers it again (k_round<..., GATHER>).  Same tile / pair layout and partial rows as
 // k_inv_bwd<true>: tile = 2048 pairs, thread t owns pairs 256 g + t (g = 0..7), W = E_hi[tile] E_lo[256 g + t].
+#ifndef ZKL_R1_ACC_SMEM
+#define ZKL_R1_ACC_SMEM 1
+#endif
 #ifndef ZKL_R1_CTAS
 #define ZKL_R1_CTAS 3   // 24 warps per SM hide the gathers' latency better than 16 without spills (measured -7%)
 #endif
@@ -694,7 +697,16 @@ k_round1_keys(const uint32_t* __restrict__ S, uint64_t n, const uint32_t* __rest
     // reduction are paid once per CTA.  The CTA's row is row b; rows b + gridDim.x j (j >= 1) are zeroed, so the
     // round still has one row per tile.
     fr hinf = fr_zero();
+#if ZKL_R1_ACC_SMEM
+    // the sums of A(., 0) and A(., 1) in shared memory (18 words per thread): fewer live registers at 80
+    __shared__ fr_acc sh_a[2][kInvThreads];
+    sh_a[0][threadIdx.x] = fr_acc_zero();
+    sh_a[1][threadIdx.x] = fr_acc_zero();
+    fr_acc& a0 = sh_a[0][threadIdx.x];
+    fr_acc& a1 = sh_a[1][threadIdx.x];
+#else
     fr_acc a0 = fr_acc_zero(), a1 = fr_acc_zero();
+#endif
 #pragma unroll 1
     for (int q = 0; q < tpc; ++q) {
         fr_wide acc = fr_wide_zero();
