@@ -38,9 +38,7 @@ template <bool FULL, typename F>
 __device__ __forceinline__ void mh_for_keys(const uint32_t* __restrict__ keys, uint64_t n, uint64_t c, F&& f) {
     constexpr int kIters = kMhChunk / (4 * kMhThreads), kUnroll = 8;
     const uint64_t base = c * kMhChunk;
-#pragma unroll 1
-    for (int it0 = 0; it0 < kIters; it0 += kUnroll) {
-        uint4 q[kUnroll];
+    auto load = [&](int it0, uint4 (&q)[kUnroll]) {
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
             const uint64_t i = base + 4 * ((uint64_t)threadIdx.x + (uint64_t)kMhThreads * (it0 + u));
@@ -53,6 +51,13 @@ __device__ __forceinline__ void mh_for_keys(const uint32_t* __restrict__ keys, u
                 q[u].w = i + 3 < n ? keys[i + 3] : kMhNone;
             }
         }
+    };
+    // the next 8 loads are in flight while the current 32 keys are counted
+    uint4 q[kUnroll], qn[kUnroll];
+    load(0, q);
+#pragma unroll 1
+    for (int it0 = 0; it0 < kIters; it0 += kUnroll) {
+        if (it0 + kUnroll < kIters) load(it0 + kUnroll, qn);
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
             f(q[u].x);
@@ -60,6 +65,8 @@ __device__ __forceinline__ void mh_for_keys(const uint32_t* __restrict__ keys, u
             f(q[u].z);
             f(q[u].w);
         }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) q[u] = qn[u];
     }
 }
 
