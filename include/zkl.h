@@ -205,7 +205,9 @@ int zkl_tlookup_prove_p1(zkl_ctx* ctx, const void* pp_dev, uint64_t cols, const 
  * zkl_ctx_wait, which also returns the first error of the pending calls, in call order (later calls' outputs
  * are then not delivered).  At most one pending prepare and one pending prove per ctx (else E_STATE): K
  * instances in flight = K contexts, each with its own CUDA stream and workspace, so the GPU overlaps one
- * instance's latency-bound tail with another's bandwidth/ALU-bound rounds.  Single-rank contexts only (E_ARG).
+ * instance's latency-bound tail with another's bandwidth/ALU-bound rounds.  At P > 1 (NCCL) the prepare's histogram
+ * and its all-reduce run on the low-priority stream and the proof's collectives are ordered after them; with the
+ * loopback communicator (host-synchronising collectives) the prepare stays synchronous.
  * A proof whose prepared keys missed falls back to the inversion path synchronously inside zkl_ctx_wait. */
 int zkl_ctx_set_async(zkl_ctx* ctx, int on);
 int zkl_ctx_wait(zkl_ctx* ctx);
