@@ -185,3 +185,28 @@ def test_prove_pair_host_matches_oracle(ctx, d, n):
     pf, m = ctx.prove_pair_host(x, y, tx, ty, ch.alpha_f, D, _chal(ch), TL.PAPER, want_m=True)
     assert np.array_equal(m, ref.m)
     assert pf.evals == ref.evals and pf.finals == ref.finals
+
+
+@pytest.mark.parametrize("d,n", [(20, 8), (21, 16)])
+def test_async_prepare_then_fiat_shamir(ctx, d, n):
+    """The bench's Fiat-Shamir step: async prepare_pair (the histogram on the low-priority stream, its workspace
+    beside the proof's) then prove_fs, at large D with a small and a full table: the transcript and derived
+    challenges equal the synchronous run's, and the oracle's on those challenges."""
+    x, y, tx, ty, ch = _pair_workload(d, n, 3 * d + n)
+    D, N = 1 << d, 1 << n
+    seed = hashlib.sha256(f"async-fs-{d}-{n}".encode()).digest()
+    ctx.reserve(D, N)
+    tab = ctx.table(ctx.import_pair(tx, ty, ch.alpha_f))
+    assert ctx.table_attach_pair(tab, tx, ty, ch.alpha_f)
+    _, m = ctx.prepare_pair(x, y, ch.alpha_f, D, tab, virtual_s=True)
+    ref, dref = ctx.prove_fs(None, D, tab, m, seed, TL.PAPER)
+    ctx.set_async(True)
+    _, m2 = ctx.prepare_pair(x, y, ch.alpha_f, D, tab, virtual_s=True)
+    res = ctx.prove_fs(None, D, tab, m2, seed, TL.PAPER)
+    ctx.wait()
+    ctx.set_async(False)
+    got, dgot = res.result()
+    assert dgot == dref and got.evals == ref.evals and got.finals == ref.finals
+    chal = C.chal_array(dref["beta"], dref["alpha1"], dref["alpha2"], dref["u"], dref["r"])
+    o = C.prove_pair_stream(x, y, tx, ty, ch.alpha_f, chal, TL.PAPER, 2)
+    assert ref.evals == o.evals and ref.finals == o.finals
