@@ -37,13 +37,15 @@ void make_hx_plan(HxPlan& h, uint64_t D, uint64_t cols) {
     h.total = o;
 }
 
-// pp = [generators G_0..G_{cols-1}, H (affine)] [their 16-entry tables] [64 x 16 window table of H]
+// pp = [generators G_0..G_{cols-1}, H (affine)] [their 16-entry tables, one per 32-bit scalar chunk g, of
+// d 2^{32 g} G_i] [64 x 16 window table of H]
 size_t hx_pp_bytes(uint64_t cols) {
-    return align_up(sizeof(g1a) * (cols + 1)) + align_up(sizeof(g1a) * (cols + 1) * kHxTab) + sizeof(g1a) * 64 * kHxTab;
+    return align_up(sizeof(g1a) * (cols + 1)) + align_up(sizeof(g1a) * kHxGroups * (cols + 1) * kHxTab) +
+           sizeof(g1a) * 64 * kHxTab;
 }
 const g1a* hx_htab(const void* pp, uint64_t cols) {
     return reinterpret_cast<const g1a*>((const uint8_t*)pp + align_up(sizeof(g1a) * (cols + 1)) +
-                                        align_up(sizeof(g1a) * (cols + 1) * kHxTab));
+                                        align_up(sizeof(g1a) * kHxGroups * (cols + 1) * kHxTab));
 }
 
 int hx_shape(zkl_ctx* ctx, uint64_t D, uint64_t cols) {
@@ -153,7 +155,8 @@ int zkl_hyrax_setup(zkl_ctx* ctx, uint64_t cols, void* pp, size_t pp_bytes) {
     g1a* gens = reinterpret_cast<g1a*>(pp);
     g1a* tab = reinterpret_cast<g1a*>((uint8_t*)pp + align_up(sizeof(g1a) * (cols + 1)));
     LAUNCH(ctx, k_hx_gens, (unsigned)((cols + 1 + 63) / 64), 64, 0, s, cols, gens);
-    LAUNCH(ctx, k_hx_tables, (unsigned)(((cols + 1) * kHxTab + 127) / 128), 128, 0, s, gens, cols + 1, tab);
+    LAUNCH(ctx, k_hx_tables, (unsigned)((kHxGroups * (cols + 1) * kHxTab + 127) / 128), 128, 0, s, gens, cols + 1,
+           tab);
     LAUNCH(ctx, k_hx_htables, (64 * kHxTab + 127) / 128, 128, 0, s, gens + cols, const_cast<g1a*>(hx_htab(pp, cols)));
     return sync_stream(ctx);
 }

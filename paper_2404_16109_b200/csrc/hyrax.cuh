@@ -90,17 +90,21 @@ __global__ void k_hx_gens(uint64_t cols, g1a* gens) {
     gens[i] = i < cols ? hx_hash_to_curve(tg, 11, (uint32_t)i) : hx_hash_to_curve(th, 11, 0);
 }
 
-// tab[i][d] = d gens[i], d = 0..15 (affine; d = 0 the point at infinity)
+// tab[g][i][d] = d 2^{32 g} gens[i], g = 0..7, d = 0..15 (affine; d = 0 the point at infinity): chunk g of a scalar
+// adds from its own table, so the chunks' partial sums combine with additions only (no 32-doubling Horner per chunk)
 __global__ void k_hx_tables(const g1a* __restrict__ gens, uint64_t count, g1a* tab) {
     const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (k >= count * kHxTab) return;
-    const uint64_t i = k / kHxTab;
+    if (k >= kHxGroups * count * kHxTab) return;
+    const int g = (int)(k / (count * kHxTab));
+    const uint64_t i = (k / kHxTab) % count;
     const int d = (int)(k % kHxTab);
     g1j acc = g1_infinity();
     for (int bit = 3; bit >= 0; --bit) {
         acc = g1_dbl(acc);
         if ((d >> bit) & 1) acc = g1_add_affine(acc, gens[i]);
     }
+    if (!g1_is_inf(acc))
+        for (int j = 0; j < 32 * g; ++j) acc = g1_dbl(acc);
     tab[k] = g1_to_affine(acc);
 }
 
@@ -148,12 +152,13 @@ __global__ void k_hx_canon(const uint32_t* __restrict__ S, uint64_t n, uint32_t*
 // k_hx_commit_partial: one thread per (row j, slice of kHxSlice columns, chunk g): windowed Straus over the 8
 // 4-bit windows of c_g (MSB window first) -> partial[j][s][g].  Short dependent chains, D / 2 threads.
 __global__ void __launch_bounds__(kHxThreads)
-k_hx_commit_partial(const uint32_t* __restrict__ Sc, uint64_t D, uint64_t cols, const g1a* __restrict__ tab,
+k_hx_commit_partial(const uint32_t* __restrict__ Sc, uint64_t D, uint64_t cols, const g1a* __restrict__ tab0,
                     uint64_t nslices, g1j* partial) {
     const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t rows = D / cols;
     if (t >= rows * nslices * kHxGroups) return;
     const int g = (int)(t % kHxGroups);
+    const g1a* __restrict__ tab = tab0 + (uint64_t)g * (cols + 1) * kHxTab;   // d 2^{32 g} G_i
     const uint64_t js = t / kHxGroups;
     const uint64_t j = js / nslices, s = js % nslices;
     const uint64_t i0 = s * kHxSlice;
@@ -216,11 +221,7 @@ __global__ void k_hx_commit_rows(const g1j* __restrict__ Q, uint64_t rows, const
     const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (j >= rows) return;
     g1j acc = Q[j * kHxGroups + kHxGroups - 1];
-    for (int g = kHxGroups - 2; g >= 0; --g) {
-        if (!g1_is_inf(acc))   // small scalars: the high chunks are empty and cost no doublings
-            for (int k = 0; k < 32; ++k) acc = g1_dbl(acc);
-        acc = g1_add(acc, Q[j * kHxGroups + g]);
-    }
+    for (int g = kHxGroups - 2; g >= 0; --g) acc = g1_add(acc, Q[j * kHxGroups + g]);   // already 2^{32 g}-scaled
     if (rho_canon) {   // rho H = sum_w hw[w][digit_w] (htab: the 64 x 16 window table of H)
         for (int w = 0; w < 64; ++w) {
             const uint32_t d = (rho_canon[j * 8 + (w >> 3)] >> ((w & 7) * 4)) & 15u;
